@@ -1,0 +1,235 @@
+"""CPU fp64 oracle for the RB online solvers (Nguyen & Chen, arXiv:1804.06363).
+
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import this module.
+It shares no code with the CUDA product path (`paper_1804_06363_b200/`), and
+neither imports the other; both take their seeded inputs from `synth/`.
+
+The arithmetic lives in `oracle.c` (plain C, -O2 -ffp-contract=off); this file
+is ctypes marshalling plus two convenience helpers that only compose oracle
+calls.  Citations (PAPER.md line / equation / algorithm) are in oracle.c and
+oracle.h.  Parity status of each function is listed in DESIGN.md ("Oracle
+pins"); every function here is pinned by a `-m "not gpu"` test.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+
+SYM_RBGS, FWD_RBGS, JACOBI = 0, 1, 2
+STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "REDUCED_NOT_SPD", 3: "CURVATURE", 4: "PRECOND",
+          5: "NONFINITE"}
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+                               "-fPIC", "-shared", "-o", _SO, src, "-lm"])
+    return _SO
+
+
+class _Opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("smoother", C.c_int),
+                ("sweeps", C.c_int), ("omega", C.c_double), ("delta", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+    return _lib
+
+
+def _d(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None
+
+
+def _i(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _blocks(blocks):
+    b = list(blocks) + [1] * (3 - len(blocks))
+    return (C.c_int * 3)(*b)
+
+
+class Grid:
+    """dim, m (interior nodes per axis), blocks (subdomains per axis)."""
+
+    def __init__(self, dim: int, m: int, blocks):
+        self.dim, self.m, self.blocks = int(dim), int(m), tuple(int(b) for b in blocks)
+        assert len(self.blocks) == self.dim
+        self.N = self.m ** self.dim
+        self.Q = int(np.prod(self.blocks))
+        self._cb = _blocks(self.blocks)
+
+    # -- operator / smoother ------------------------------------------------
+    def apply_A(self, theta, x):
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.N)
+        lib().or_apply_A(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(x), _d(y))
+        return y
+
+    def gs_halfsweep(self, theta, b, y, color):
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        y = np.array(y, dtype=np.float64, copy=True)
+        lib().or_gs_halfsweep(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(b), _d(y),
+                              int(color))
+        return y
+
+    def smooth(self, theta, b, y, kind=SYM_RBGS, sweeps=1, omega=1.0):
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        y = np.array(y, dtype=np.float64, copy=True)
+        lib().or_smooth(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(b), _d(y),
+                        int(kind), int(sweeps), C.c_double(omega))
+        return y
+
+    def dense_A(self, theta):
+        """explicit matrix by applying the matrix-free operator to unit vectors (tiny grids)."""
+        A = np.empty((self.N, self.N))
+        e = np.zeros(self.N)
+        for j in range(self.N):
+            e[j] = 1.0
+            A[:, j] = self.apply_A(theta, e)
+            e[j] = 0.0
+        return A
+
+    # -- basis objects ------------------------------------------------------
+    def offline_blocks(self, W):
+        W = np.asfortranarray(W, dtype=np.float64)
+        n = W.shape[1]
+        ANq = np.empty((self.Q, n, n))
+        fn = np.empty(n)
+        lib().or_offline_blocks(self.dim, C.c_int64(self.m), self._cb, n, _d(W), _d(ANq), _d(fn))
+        return ANq, fn
+
+    # -- solvers ------------------------------------------------------------
+    def _solve(self, fname, W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps, omega, delta):
+        n = 0 if W is None else W.shape[1]
+        Wf = np.asfortranarray(W, dtype=np.float64) if n else np.zeros((1, 1))
+        ANq = np.ascontiguousarray(ANq, dtype=np.float64) if n else np.zeros(1)
+        fn = np.ascontiguousarray(fn, dtype=np.float64) if n else np.zeros(1)
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        o = _Opts(tol, max_iter, smoother, sweeps, omega, delta)
+        x = np.empty(self.N)
+        its = C.c_int(0)
+        hist = np.full(max_iter + 2, np.nan)
+        a_n = np.full(max(n, 1), np.nan)
+        trr = C.c_double(0)
+        st = getattr(lib(), fname)(self.dim, C.c_int64(self.m), self._cb, n, _d(Wf), _d(ANq),
+                                   _d(fn), _d(mu), _d(bb), C.byref(o), _d(x), C.byref(its),
+                                   _d(hist), _d(a_n), C.byref(trr))
+        k = its.value
+        return dict(x=x, its=k, status=STATUS[st], hist=hist[:k + 1].copy(),
+                    a_n=a_n[:n].copy(), true_relres=trr.value)
+
+    def rbi(self, W, ANq, fn, mu, b=None, tol=1e-10, max_iter=500000, smoother=SYM_RBGS,
+            sweeps=1, omega=1.0, delta=1e-12):
+        return self._solve("or_rbi", W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps,
+                           omega, delta)
+
+    def rbcg(self, W, ANq, fn, mu, b=None, tol=1e-10, max_iter=20000, smoother=SYM_RBGS,
+             sweeps=1, omega=1.0, delta=1e-12):
+        return self._solve("or_rbcg", W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps,
+                           omega, delta)
+
+    def cg(self, mu, b=None, tol=1e-10, max_iter=100000):
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.N)
+        its = C.c_int(0)
+        st = lib().or_cg(self.dim, C.c_int64(self.m), self._cb, _d(mu), _d(bb), C.c_double(tol),
+                         int(max_iter), _d(x), C.byref(its))
+        return dict(x=x, its=its.value, status=STATUS[st])
+
+    def greedy(self, mu_train, n_max, adaptive=True, snapshot_tol=1e-12, drop_tol=1e-10):
+        mu_train = np.ascontiguousarray(mu_train, dtype=np.float64)
+        nt = mu_train.shape[0]
+        W = np.zeros((self.N, n_max), order="F")
+        ANq = np.zeros((self.Q, n_max, n_max))
+        fn = np.zeros(n_max)
+        sel = np.full(n_max, -1, dtype=np.int32)
+        ind = np.full(n_max, np.nan)
+        its = np.zeros(n_max, dtype=np.int32)
+        rej = C.c_int(0)
+        n = lib().or_greedy(self.dim, C.c_int64(self.m), self._cb, nt, _d(mu_train), n_max,
+                            int(adaptive), C.c_double(snapshot_tol), C.c_double(drop_tol),
+                            _d(W), _d(ANq), _d(fn), _i(sel), _d(ind), _i(its), C.byref(rej))
+        return dict(W=np.asfortranarray(W[:, :n]), ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(),
+                    selected=sel[:n].copy(), indicator=ind[:n].copy(), snap_iters=its[:n].copy(),
+                    n_rejected=rej.value, n=n)
+
+    def basis_from_samples(self, mus, snapshot_tol=1e-12, drop_tol=1e-10):
+        mus = np.ascontiguousarray(mus, dtype=np.float64)
+        cnt = mus.shape[0]
+        W = np.zeros((self.N, cnt), order="F")
+        ANq = np.zeros((self.Q, cnt, cnt))
+        fn = np.zeros(cnt)
+        its = np.zeros(cnt, dtype=np.int32)
+        rej = C.c_int(0)
+        n = lib().or_basis_from_samples(self.dim, C.c_int64(self.m), self._cb, cnt, _d(mus),
+                                        C.c_double(snapshot_tol), C.c_double(drop_tol), _d(W),
+                                        _d(ANq), _d(fn), _i(its), C.byref(rej))
+        return dict(W=np.asfortranarray(W[:, :n]), ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(),
+                    snap_iters=its[:n].copy(), n_rejected=rej.value, n=n)
+
+
+# -- dense primitives --------------------------------------------------------
+def cholesky(A):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    L = np.empty_like(A)
+    piv = lib().or_cholesky(n, _d(A), _d(L))
+    return L, piv
+
+
+def chol_solve(L, b):
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty_like(b)
+    lib().or_chol_solve(L.shape[0], _d(L), _d(b), _d(x))
+    return x
+
+
+def dot(x, y):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    lib().or_dot.restype = C.c_double
+    return lib().or_dot(C.c_int64(x.size), _d(x), _d(y))
+
+
+def mgs_append(W, v, drop_tol=1e-10):
+    """returns (W_new, rejected)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    Nn = v.size
+    n = 0 if W is None else W.shape[1]
+    Wb = np.zeros((Nn, n + 1), order="F")
+    if n:
+        Wb[:, :n] = W
+    rej = lib().or_mgs_append(C.c_int64(Nn), n, _d(Wb), _d(v), C.c_double(drop_tol))
+    return (Wb if not rej else (W if n else np.zeros((Nn, 0), order="F"))), bool(rej)
+
+
+def rb_solve(ANq, fn, mu):
+    ANq = np.ascontiguousarray(ANq, dtype=np.float64)
+    fn = np.ascontiguousarray(fn, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    n = fn.size
+    a = np.empty(n)
+    piv = lib().or_rb_solve(n, ANq.shape[0], _d(ANq), _d(fn), _d(mu), _d(a))
+    return a, piv

@@ -1,0 +1,110 @@
+/*
+ * oracle.h -- plain, slow, obviously-correct CPU fp64 oracle for the online
+ * phase of the reduced-basis iterative solvers of Nguyen & Chen
+ * (arXiv:1804.06363, /root/reference/PAPER.md).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA
+ * product path under paper_1804_06363_b200/.
+ *
+ * Conventions:
+ *  - grid: dim in {2,3}, m interior nodes per axis, h = 1/(m+1); unknown
+ *    P = (I-1) + m(J-1) + m^2(K-1), I,J,K in 1..m; Dirichlet zero outside.
+ *  - cell (a,b,c), a in 0..m, block index per axis floor((2a+1)p / (2(m+1))),
+ *    q = bx + px*by + px*py*bz; coefficient theta_q (theta = mu, Q = P).
+ *  - edge coefficient = cell average (AMB-1/AMB-4), A = (m+1)^2 K, f = 1.
+ *  - all vectors of length N = m^dim; W is column-major N x n (ld = N).
+ *  - dense small matrices are row-major n x n.
+ */
+#ifndef RBS_ORACLE_H
+#define RBS_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { OR_SMOOTH_SYM_RBGS = 0, OR_SMOOTH_FWD_RBGS = 1, OR_SMOOTH_JACOBI = 2 };
+enum { OR_CONVERGED = 0, OR_MAXIT = 1, OR_REDUCED_NOT_SPD = 2, OR_CURVATURE = 3,
+       OR_PRECOND = 4, OR_NONFINITE = 5 };
+
+typedef struct {
+    double tol;        /* relative residual tolerance (AMB-7) */
+    int max_iter;      /* AMB-9 */
+    int smoother;      /* OR_SMOOTH_* */
+    int sweeps;        /* nu */
+    double omega;      /* Jacobi damping */
+    double delta;      /* PRECOND breakdown threshold (AMB-11) */
+} or_opts;
+
+/* (A(theta) x) matrix-free, PAPER.md:98-103 (eq12) with AMB-1..4. */
+void or_apply_A(int dim, int64_t m, const int* blocks, const double* theta,
+                const double* x, double* y);
+/* one red-black Gauss-Seidel half-sweep of colour c on A y = b (AMB-5). */
+void or_gs_halfsweep(int dim, int64_t m, const int* blocks, const double* theta,
+                     const double* b, double* y, int color);
+/* smoother S(A, b, y) in place, PAPER.md:148-153 (eq8). */
+void or_smooth(int dim, int64_t m, const int* blocks, const double* theta,
+               const double* b, double* y, int kind, int sweeps, double omega);
+
+/* dense Cholesky A = L L^T (right-looking); returns -1 or failing pivot. */
+int or_cholesky(int n, const double* A, double* L);
+void or_chol_solve(int n, const double* L, const double* b, double* x);
+/* Neumaier-compensated dot product (AMB-20). */
+double or_dot(int64_t N, const double* x, const double* y);
+
+/* MGS with one unconditional re-orthogonalisation pass.
+ * W column-major with ld = N holding n columns; appends column n on success.
+ * returns 0 on success, 1 if rejected (post norm < drop_tol*||v||). */
+int or_mgs_append(int64_t N, int n, double* W, const double* v, double drop_tol);
+
+/* offline blocks A_{n,q} = W^T A_q W (i<=j then mirrored) and f_{n,1} = W^T 1
+ * (eq12c).  ANq: Q x n x n, fn: n. */
+void or_offline_blocks(int dim, int64_t m, const int* blocks, int n, const double* W,
+                       double* ANq, double* fn);
+
+/* RBI (algorithm1).  b == NULL means the problem RHS f = 1
+ * (then W^T f = fn is taken from the offline block, PAPER.md:171 / AMB-12).
+ * hist: max_iter+1 entries (relative residuals), a_n: first reduced coeffs (n).
+ * returns status; *its = iterations. */
+int or_rbi(int dim, int64_t m, const int* blocks, int n, const double* W,
+           const double* ANq, const double* fn, const double* mu, const double* b,
+           const or_opts* o, double* x, int* its, double* hist, double* a_n,
+           double* true_relres);
+
+/* RBCG (algorithm2); n == 0 is symmetric-GS-PCG. */
+int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
+            const double* ANq, const double* fn, const double* mu, const double* b,
+            const or_opts* o, double* x, int* its, double* hist, double* a_n,
+            double* true_relres);
+
+/* plain CG (context only). */
+int or_cg(int dim, int64_t m, const int* blocks, const double* mu, const double* b,
+          double tol, int max_iter, double* x, int* its);
+
+/* Greedy (algorithm0; adaptive=1: algorithm3).
+ * W_out: column-major N x n_max.  ANq_out: Q x n_max x n_max (only the leading
+ * n_out x n_out block of each q is meaningful, row stride n_max).
+ * returns n_out. */
+int or_greedy(int dim, int64_t m, const int* blocks, int n_train, const double* mu_train,
+              int n_max, int adaptive, double snapshot_tol, double drop_tol,
+              double* W_out, double* ANq_out, double* fn_out, int* selected,
+              double* indicator, int* snap_iters, int* n_rejected);
+
+/* Build a basis from a given sample list (the fine-grid half of the
+ * multi-fidelity approach): RBCG snapshots with the growing
+ * basis, MGS, incremental offline blocks.  returns n_out. */
+int or_basis_from_samples(int dim, int64_t m, const int* blocks, int count,
+                          const double* mus, double snapshot_tol, double drop_tol,
+                          double* W_out, double* ANq_out, double* fn_out,
+                          int* snap_iters, int* n_rejected);
+
+/* Galerkin RB solve for one mu: a_n = A_n(mu)^{-1} f_n. */
+int or_rb_solve(int n, int Q, const double* ANq, const double* fn, const double* mu,
+                double* a_n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

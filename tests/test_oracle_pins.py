@@ -1,0 +1,380 @@
+"""Pins of the CPU oracle against things other than itself.
+
+Every test here is `not gpu`.  Sources: closed forms (Laplacian eigenpairs),
+an independent P1-FEM assembly (PAPER.md:319 discretisation), textbook SGS-PCG
+(scipy), LAPACK, the paper's Lemmas 1-3, Galerkin
+optimality, and SPEC.md worked examples (tests/golden/spec_examples.json).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+import refs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+RNG = np.random.default_rng(12345)
+
+
+def rand_mu(Q, lo=0.1, hi=10.0, rng=RNG):
+    return lo * (hi / lo) ** rng.random(Q)
+
+
+# --------------------------------------------------------------------------- operator
+@pytest.mark.parametrize("dim,m,blocks", [(2, 7, (2, 2)), (2, 12, (3, 3)), (3, 5, (2, 2, 2)),
+                                          (3, 6, (2, 3, 2))])
+def test_operator_equals_cellwise_assembly(orc, dim, m, blocks):
+    g = orc.Grid(dim, m, blocks)
+    mu = rand_mu(g.Q)
+    A = g.dense_A(mu)
+    R = refs.cellwise_fd(dim, m, blocks, mu).toarray()
+    assert np.abs(A - R).max() <= 1e-13 * np.abs(R).max()
+    assert np.array_equal(A, A.T)  # bitwise symmetric
+
+
+@pytest.mark.parametrize("m,blocks", [(7, (2, 2)), (11, (3, 3)), (8, (2, 2))])
+@pytest.mark.parametrize("diag", ["main", "anti"])
+def test_operator_equals_p1_fem_2d(orc, m, blocks, diag):
+    """AMB-1: the cell-averaged 5-point system is the P1-FEM system."""
+    g = orc.Grid(2, m, blocks)
+    mu = rand_mu(g.Q)
+    K = refs.fem_p1_2d(m, blocks, mu, diag).toarray()
+    A = g.dense_A(mu)
+    h2 = 1.0 / (m + 1) ** 2
+    assert np.abs(h2 * A - K).max() <= 1e-13 * np.abs(K).max()
+    # FEM load of f = 1 is h^2 per node: A x = 1 <=> K x = load
+    assert np.allclose(refs.fem_load_2d(m), h2 * np.ones(m * m), rtol=0, atol=1e-18)
+
+
+@pytest.mark.parametrize("dim,m,ks", [(2, 15, (1, 1)), (2, 15, (3, 7)), (2, 16, (16, 2)),
+                                      (3, 7, (1, 2, 3)), (3, 8, (8, 1, 5))])
+def test_constant_theta_is_scaled_laplacian(orc, dim, m, ks):
+    """theta == c: A v = c lambda v for the sine eigenvectors (closed form)."""
+    blocks = (2,) * dim
+    g = orc.Grid(dim, m, blocks)
+    c = 2.75
+    lam, v = refs.laplacian_eig(dim, m, ks)
+    Av = g.apply_A(np.full(g.Q, c), v)
+    assert np.abs(Av - c * lam * v).max() <= 1e-12 * c * lam
+
+
+def test_affine_linearity(orc):
+    """A(theta) = sum_q theta_q A(e_q)."""
+    g = orc.Grid(3, 6, (2, 2, 2))
+    mu = rand_mu(g.Q)
+    x = RNG.standard_normal(g.N)
+    tot = np.zeros(g.N)
+    for q in range(g.Q):
+        e = np.zeros(g.Q); e[q] = 1.0
+        tot += mu[q] * g.apply_A(e, x)
+    ref = g.apply_A(mu, x)
+    assert np.abs(tot - ref).max() <= 1e-13 * np.abs(ref).max() * g.Q
+
+
+def test_Aq_psd_and_A_spd(orc):
+    g = orc.Grid(2, 9, (3, 3))
+    for q in range(g.Q):
+        e = np.zeros(g.Q); e[q] = 1.0
+        assert np.linalg.eigvalsh(g.dense_A(e)).min() > -1e-10
+    L, piv = orc.cholesky(g.dense_A(rand_mu(g.Q)))
+    assert piv == -1
+
+
+# --------------------------------------------------------------------------- smoother
+@pytest.mark.parametrize("dim,m,blocks", [(2, 6, (2, 2)), (2, 7, (3, 3)), (3, 4, (2, 2, 2))])
+def test_rbgs_is_textbook_gs_in_red_black_order(orc, dim, m, blocks):
+    g = orc.Grid(dim, m, blocks)
+    mu = rand_mu(g.Q)
+    A = refs.cellwise_fd(dim, m, blocks, mu).toarray()
+    b = RNG.standard_normal(g.N)
+    y0 = RNG.standard_normal(g.N)
+    order = refs.red_black_order(dim, m)
+    # textbook forward GS in red-then-black order
+    y = y0.copy()
+    for i in order:
+        y[i] = (b[i] - A[i] @ y + A[i, i] * y[i]) / A[i, i]
+    red = g.gs_halfsweep(mu, b, y0, 0)
+    got = g.gs_halfsweep(mu, b, red, 1)
+    assert np.abs(got - y).max() <= 1e-13 * np.abs(y).max()
+    assert np.array_equal(g.smooth(mu, b, y0, orc.FWD_RBGS, 1), got)
+    # (1,1[,1]) colour convention: first interior node red in 2D, black in 3D
+    par = dim % 2
+    assert (red[0] != y0[0]) == (par == 0)
+
+
+def test_symmetric_rbgs_is_rbr_bitwise(orc):
+    """R,B,B,R == R,B,R bitwise (the repeated black half-sweep is a no-op, AMB-6)."""
+    g = orc.Grid(2, 13, (3, 3))
+    mu = rand_mu(g.Q)
+    b = RNG.standard_normal(g.N)
+    y0 = RNG.standard_normal(g.N)
+    y = g.gs_halfsweep(mu, b, y0, 0)
+    y = g.gs_halfsweep(mu, b, y, 1)
+    y = g.gs_halfsweep(mu, b, y, 0)
+    assert np.array_equal(g.smooth(mu, b, y0, orc.SYM_RBGS, 1), y)
+
+
+def test_smoother_fixed_point_and_energy(orc):
+    g = orc.Grid(2, 11, (2, 2))
+    mu = rand_mu(g.Q)
+    A = refs.cellwise_fd(2, 11, (2, 2), mu).toarray()
+    b = RNG.standard_normal(g.N)
+    xs = np.linalg.solve(A, b)
+    for kind in (orc.SYM_RBGS, orc.FWD_RBGS):
+        z = g.smooth(mu, b, xs, kind, 1)
+        assert np.abs(z - xs).max() <= 1e-13 * np.abs(xs).max()
+    y = RNG.standard_normal(g.N)
+    en = lambda v: np.sqrt((v - xs) @ A @ (v - xs))
+    for _ in range(5):
+        y2 = g.smooth(mu, b, y, orc.SYM_RBGS, 1)
+        assert en(y2) <= en(y) * (1 + 1e-14)
+        y = y2
+
+
+# --------------------------------------------------------------------------- dense
+def test_spec_cholesky_examples(orc):
+    for ex in GOLD["cholesky"]:
+        L, piv = orc.cholesky(np.array(ex["M"]))
+        assert piv == -1 and np.allclose(L, ex["L"], atol=1e-15), ex["cite"]
+    for ex in GOLD["cholesky_fail"]:
+        _, piv = orc.cholesky(np.array(ex["M"]))
+        assert piv == ex["pivot"], ex["cite"]
+    for ex in GOLD["chol_solve"]:
+        L, _ = orc.cholesky(np.array(ex["M"]))
+        assert np.allclose(orc.chol_solve(L, np.array(ex["b"])), ex["x"], atol=1e-15), ex["cite"]
+    for ex in GOLD["dot"]:
+        assert orc.dot(np.array(ex["x"]), np.array(ex["y"])) == ex["value"]
+
+
+@pytest.mark.parametrize("n", [1, 5, 17, 40, 64])
+def test_cholesky_vs_lapack(orc, n):
+    X = RNG.standard_normal((n, n))
+    M = X @ X.T + n * np.eye(n)
+    L, piv = orc.cholesky(M)
+    assert piv == -1
+    assert np.abs(L - np.linalg.cholesky(M)).max() <= 1e-12 * np.abs(L).max()
+    b = RNG.standard_normal(n)
+    assert np.abs(orc.chol_solve(L, b) - np.linalg.solve(M, b)).max() <= 1e-10 * np.abs(
+        np.linalg.solve(M, b)).max()
+    # leading principal block identity (AMB-19)
+    k = max(1, n // 2)
+    Lk, _ = orc.cholesky(M[:k, :k])
+    assert np.array_equal(Lk, L[:k, :k])
+
+
+def test_dot_is_compensated(orc):
+    x = np.array([1e16, 1.0, -1e16, 1.0])
+    assert orc.dot(x, np.ones(4)) == 2.0
+
+
+def test_spec_mgs_examples(orc):
+    for ex in GOLD["mgs"]:
+        W = np.array(ex["W"]).T
+        Wn, rej = orc.mgs_append(W, np.array(ex["v"]))
+        if ex.get("rejected"):
+            assert rej, ex["cite"]
+        else:
+            assert not rej and np.allclose(Wn[:, -1], ex["new"], atol=1e-15), ex["cite"]
+    W = None
+    for _ in range(12):
+        W, rej = orc.mgs_append(W, RNG.standard_normal(300))
+        assert not rej
+    assert np.abs(W.T @ W - np.eye(12)).max() < 1e-14
+    _, rej = orc.mgs_append(W, W @ RNG.standard_normal(12))  # dependent vector
+    assert rej
+
+
+# --------------------------------------------------------------------------- basis / solvers
+@pytest.fixture(scope="module")
+def small2d(orc):
+    g = orc.Grid(2, 15, (2, 2))
+    tr = 0.1 * 100 ** np.random.default_rng(7).random((40, 4))
+    res = g.greedy(tr, 8)
+    return g, tr, res
+
+
+def test_offline_online_consistency(orc, small2d):
+    """sum_q theta_q A_{n,q} = W^T A(theta) W and f_n = W^T f."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    assert np.abs(W.T @ W - np.eye(res["n"])).max() < 1e-12
+    ANq2, fn2 = g.offline_blocks(W)
+    assert np.abs(ANq2 - ANq).max() <= 1e-12 * np.abs(ANq).max()  # incremental == recompute
+    for q in range(g.Q):
+        assert np.array_equal(ANq[q], ANq[q].T)
+    for _ in range(20):
+        mu = rand_mu(g.Q)
+        A = refs.cellwise_fd(2, g.m, g.blocks, mu).toarray()
+        An = np.einsum("q,qij->ij", mu, ANq)
+        ref = W.T @ A @ W
+        assert np.abs(An - ref).max() <= 1e-12 * np.abs(ref).max()
+        assert np.linalg.eigvalsh(An).min() > 0
+    assert np.abs(fn - W.T @ np.ones(g.N)).max() <= 1e-12 * np.abs(fn).max()
+
+
+def test_lemma1_rbi_and_rbcg_one_iteration(orc, small2d):
+    """x in span(W) => RBI and RBCG converge in one iteration."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    mu = rand_mu(g.Q)
+    c = RNG.standard_normal(res["n"])
+    b = g.apply_A(mu, W @ c)
+    for solve in (g.rbi, g.rbcg):
+        out = solve(W, ANq, fn, mu, b=b)
+        assert out["status"] == "CONVERGED" and out["its"] == 1
+        assert np.linalg.norm(out["x"] - W @ c) <= 1e-10 * np.linalg.norm(W @ c)
+        assert np.abs(out["a_n"] - c).max() <= 1e-10 * np.abs(c).max()
+
+
+def test_lemma2_stagnation_without_smoother(orc, small2d):
+    """sweeps = 0 => x_k = x_hat for all k >= 1, MAXIT."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    mu = rand_mu(g.Q)
+    xhat = W @ orc.rb_solve(ANq, fn, mu)[0]
+    for k in (1, 2, 5):
+        out = g.rbi(W, ANq, fn, mu, sweeps=0, max_iter=k)
+        assert out["status"] == "MAXIT"
+        assert np.linalg.norm(out["x"] - xhat) <= 1e-12 * np.linalg.norm(xhat)
+    # RBCG with nu = 0: W^T r_1 = 0 so the second preconditioner gives rho' ~ 0
+    out = g.rbcg(W, ANq, fn, mu, sweeps=0)
+    assert out["status"] == "PRECOND" and out["its"] == 1
+
+
+def test_lemma3_galerkin_orthogonality(orc, small2d):
+    """W e_n is the RB approximation of the error: after one
+    RBI step without smoothing, W^T (f - A x) = 0."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    mu = rand_mu(g.Q)
+    b = RNG.standard_normal(g.N)
+    out = g.rbi(W, ANq, fn, mu, b=b, sweeps=0, max_iter=1)
+    r = b - g.apply_A(mu, out["x"])
+    assert np.linalg.norm(W.T @ r) <= 1e-12 * np.linalg.norm(W.T @ b)
+
+
+@pytest.mark.parametrize("dim,m,blocks", [(2, 15, (2, 2)), (3, 7, (2, 2, 2))])
+def test_solvers_reach_direct_solution(orc, dim, m, blocks):
+    g = orc.Grid(dim, m, blocks)
+    rng = np.random.default_rng(3)
+    tr = 0.1 * 100 ** rng.random((30, g.Q))
+    res = g.greedy(tr, 6)
+    for mu in 0.1 * 100 ** rng.random((3, g.Q)):
+        A = refs.cellwise_fd(dim, m, blocks, mu).tocsc()
+        xs = spla.spsolve(A, np.ones(g.N))
+        for solve in (g.rbcg, g.rbi):
+            out = solve(res["W"], res["ANq"], res["fn"], mu)
+            assert out["status"] == "CONVERGED"
+            assert out["true_relres"] < 1e-10
+            assert np.linalg.norm(out["x"] - xs) <= 1e-8 * np.linalg.norm(xs)
+            assert out["hist"][-1] < 1e-10 and len(out["hist"]) == out["its"] + 1
+
+
+def test_constant_theta_solution_matches_closed_form(orc):
+    """theta == c: x* = sum_k (<v_k,1>/|v_k|^2)/(c lambda_k) v_k (DST, closed form)."""
+    m, c = 15, 3.5
+    g = orc.Grid(2, m, (2, 2))
+    xs = np.zeros(g.N)
+    for k1 in range(1, m + 1):
+        for k2 in range(1, m + 1):
+            lam, v = refs.laplacian_eig(2, m, (k1, k2))
+            xs += (v @ np.ones(g.N)) / (v @ v) / (c * lam) * v
+    out = g.rbcg(None, None, None, np.full(4, c))
+    assert out["status"] == "CONVERGED"
+    assert np.linalg.norm(out["x"] - xs) <= 1e-9 * np.linalg.norm(xs)
+
+
+@pytest.mark.parametrize("dim,m,blocks", [(2, 20, (3, 3)), (3, 7, (2, 2, 2))])
+def test_empty_basis_rbcg_is_ssor_pcg(orc, dim, m, blocks):
+    """n = 0: RBCG = CG preconditioned by symmetric RB-GS (textbook SGS-PCG)."""
+    g = orc.Grid(dim, m, blocks)
+    mu = rand_mu(g.Q, rng=np.random.default_rng(11))
+    A = refs.cellwise_fd(dim, m, blocks, mu).tocsr()
+    order = refs.red_black_order(dim, m)
+    M = spla.LinearOperator(A.shape, matvec=lambda r: refs.sgs_rb_apply(A, order, r))
+    count = [0]
+    b = np.ones(g.N)
+    spla.cg(A, b, M=M, rtol=1e-10, atol=0.0, maxiter=5000,
+            callback=lambda xk: count.__setitem__(0, count[0] + 1))
+    out = g.rbcg(None, None, None, mu)
+    assert out["status"] == "CONVERGED"
+    assert abs(out["its"] - count[0]) <= 1
+
+
+def test_rbcg_fewer_iterations_than_cg(orc):
+    """context: RBCG << CG on a family with fast n-width decay."""
+    g = orc.Grid(2, 31, (2, 2))
+    rng = np.random.default_rng(5)
+    res = g.greedy(0.1 * 100 ** rng.random((40, 4)), 8)
+    mu = 0.1 * 100 ** rng.random(4)
+    assert g.rbcg(res["W"], res["ANq"], res["fn"], mu)["its"] * 3 < g.cg(mu)["its"]
+
+
+# --------------------------------------------------------------------------- greedy
+def test_greedy_first_vector_is_normalised_snapshot(orc):
+    g = orc.Grid(2, 12, (2, 2))
+    tr = 0.1 * 100 ** np.random.default_rng(9).random((10, 4))
+    res = g.greedy(tr, 1)
+    xs = spla.spsolve(refs.cellwise_fd(2, 12, (2, 2), tr[0]).tocsc(), np.ones(g.N))
+    w = xs / np.linalg.norm(xs)
+    assert res["selected"][0] == 0
+    assert np.linalg.norm(res["W"][:, 0] - w) <= 1e-10
+
+
+def test_greedy_energy_error_monotone(orc):
+    """AMB-16: max over Xi_train of ||x - W_N a_N||_A is nonincreasing in N."""
+    g = orc.Grid(2, 13, (3, 3))
+    rng = np.random.default_rng(21)
+    tr = 0.1 * 100 ** rng.random((25, 9))
+    res = g.greedy(tr, 8)
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    truth = []
+    for mu in tr:
+        A = refs.cellwise_fd(2, 13, (3, 3), mu).tocsc()
+        truth.append((A, spla.spsolve(A, np.ones(g.N))))
+    prev = np.full(len(tr), np.inf)
+    for N in range(1, res["n"] + 1):
+        errs = []
+        for t, mu in enumerate(tr):
+            A, xs = truth[t]
+            a, piv = orc.rb_solve(ANq[:, :N, :N].copy(), fn[:N].copy(), mu)
+            d = xs - W[:, :N] @ a
+            e = np.sqrt(max(d @ (A @ d), 0.0))
+            floor = 1e-13 * np.sqrt(xs @ (A @ xs))
+            assert e <= prev[t] * (1 + 1e-9) + floor
+            errs.append(e)
+        prev = np.array(errs)
+
+
+def test_greedy_rejects_dependent_snapshot(orc):
+    """2 mu = scaled copies => x(2mu) = x(mu)/2 is dependent and is rejected."""
+    g = orc.Grid(2, 10, (2, 2))
+    mu = np.array([1.0, 2.0, 0.5, 3.0])
+    res = g.greedy(np.vstack([mu, 2 * mu]), 2)
+    assert res["n"] == 1 and res["n_rejected"] == 1
+
+
+def test_greedy_deterministic_and_plain_equals_adaptive(orc):
+    g = orc.Grid(2, 15, (2, 2))
+    tr = 0.1 * 100 ** np.random.default_rng(4).random((30, 4))
+    r1 = g.greedy(tr, 6)
+    r2 = g.greedy(tr, 6)
+    assert np.array_equal(r1["W"], r2["W"]) and np.array_equal(r1["selected"], r2["selected"])
+    r3 = g.greedy(tr, 6, adaptive=False)
+    assert np.array_equal(r1["selected"], r3["selected"])
+    s = np.linalg.svd(r1["W"].T @ r3["W"], compute_uv=False)
+    assert s.min() > 1 - 1e-10  # principal angles ~ 0
+
+
+def test_multifidelity_basis(orc):
+    """samples from a coarse greedy, snapshots on the fine grid."""
+    tr = 0.1 * 100 ** np.random.default_rng(8).random((30, 4))
+    coarse = orc.Grid(2, 15, (2, 2)).greedy(tr, 5)
+    fine = orc.Grid(2, 31, (2, 2))
+    mf = fine.basis_from_samples(tr[coarse["selected"]])
+    assert mf["n"] == 5
+    assert np.abs(mf["W"].T @ mf["W"] - np.eye(5)).max() < 1e-12
+    out = fine.rbcg(mf["W"], mf["ANq"], mf["fn"], tr[3])
+    assert out["status"] == "CONVERGED"
