@@ -1,0 +1,190 @@
+/*
+ * rbs.h -- C ABI of the B200-native batched reduced-basis (RB) online solver.
+ *
+ * Method: Nguyen & Chen, "Reduced-basis method for the iterative solution of
+ * parametrized SPD linear systems", arXiv:1804.06363.  Citations
+ * are PAPER.md line numbers plus the equation / algorithm label.
+ *
+ * Problem (eq1, 98-103 eq12):  A(mu) x(mu) = f(mu),
+ *   A(mu) = sum_q theta_q(mu) A_q,   f(mu) = sum_r phi_r(mu) f_r,
+ * with A_q the matrix-free cell-averaged 5-point (2D) / 7-point (3D)
+ * diffusion stencils of a piecewise-constant coefficient on a block
+ * partition of the unit square / cube (DESIGN.md AMB-1..4), theta_q = mu_q.
+ *
+ * Conventions for every entry point:
+ *  - Status: every call returns rbs_status; nothing aborts, no C++ exception
+ *    crosses the ABI.  Details of the last failure: rbs_last_error(ctx).
+ *  - Memory: the library allocates NO device memory.  Device buffers are
+ *    caller-owned (allocated by PyTorch in the Python binding), sizes are
+ *    queried first (rbs_*_size).  Pointers are borrowed for the duration of
+ *    the call unless stated otherwise ("retained").
+ *  - Streams: work is enqueued on the given cudaStream_t (void*; NULL = legacy
+ *    default stream).  Calls that return host results synchronise it.
+ *  - Node ordering of N-vectors: lexicographic, x fastest:
+ *    P = (I-1) + m(J-1) + m^2(K-1), I,J,K in 1..m (homogeneous Dirichlet).
+ *  - Batched vectors at the boundary are query-major [B][N] fp64.  The
+ *    internal layout is node-major [N][B_pad] (lane = query); the library
+ *    transposes on entry/exit.
+ *  - Not thread-safe: one context per device and per host thread.
+ */
+#ifndef RBS_H
+#define RBS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBS_VERSION 1
+#define RBS_MAX_BATCH 64     /* queries per rbs_solve_batch call */
+#define RBS_MAX_N 64         /* RB dimension n */
+#define RBS_MAX_Q 64         /* affine terms */
+
+typedef struct rbs_ctx rbs_ctx;
+
+typedef enum {
+    RBS_OK = 0,
+    RBS_E_ARG = 1,          /* invalid argument (NULL pointer, bad enum, ...) */
+    RBS_E_DIM = 2,          /* dimension mismatch / size out of range */
+    RBS_E_STATE = 3,        /* call out of order (e.g. solve before basis) */
+    RBS_E_NOT_SPD = 4,      /* offline: reduced matrix not SPD */
+    RBS_E_CUDA = 5,         /* CUDA runtime error (see rbs_last_error) */
+    RBS_E_NOMEM = 6,        /* caller buffer smaller than the queried size */
+    RBS_E_UNSUPPORTED = 7   /* valid but not supported by this build */
+} rbs_status;
+
+/* per-query termination (a per-query breakdown never fails the call) */
+typedef enum {
+    RBS_Q_CONVERGED = 0,        /* ||r||/||f|| < tol (eq:relerr) */
+    RBS_Q_MAXIT = 1,            /* max_iter reached */
+    RBS_Q_REDUCED_NOT_SPD = 2,  /* Cholesky of A_N(mu) hit a pivot <= 0 */
+    RBS_Q_CURVATURE = 3,        /* RBCG: p^T A p <= 0 */
+    RBS_Q_PRECOND = 4,          /* RBCG: y^T r <= delta ||y|| ||r|| (DESIGN.md AMB-11) */
+    RBS_Q_NONFINITE = 5         /* NaN / Inf encountered */
+} rbs_qstatus;
+
+enum { RBS_RBI = 0, RBS_RBCG = 1 };
+enum { RBS_SMOOTH_SYM_RBGS = 0, RBS_SMOOTH_FWD_RBGS = 1 };
+enum { RBS_MEM_DEVICE = 0, RBS_MEM_HOST = 1 };
+enum { RBS_GREEDY_PLAIN = 0, RBS_GREEDY_ADAPTIVE = 1 };
+
+int rbs_version(void);
+const char* rbs_status_string(rbs_status s);
+
+/* Create a context bound to CUDA device `cuda_device` (checks sm_100). */
+rbs_status rbs_create(int cuda_device, rbs_ctx** out);
+void rbs_destroy(rbs_ctx* ctx);
+/* Detail of the last failure of a call on ctx ("" if none).  Owned by ctx. */
+const char* rbs_last_error(const rbs_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Affine family (eq12).
+ *
+ * rbs_set_operator_blocks: dim in {2,3}; m[0..dim-1] interior nodes per axis
+ * (must be equal: h = 1/(m+1) on every axis; 1 <= m <= 65535; N = m^dim);
+ * blocks[0..dim-1] subdomains per axis (1..16).  Q = prod(blocks).  Cell
+ * (a,b,c) belongs to block floor((2a+1) p / (2(m+1))) per axis; q = bx +
+ * px*by + px*py*bz; A_q = A(e_q).  Invalidates any loaded basis.
+ * Errors: RBS_E_ARG / RBS_E_DIM.
+ */
+rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], const int blocks[3]);
+
+/* R = 1, f_1 = value * ones(N), phi_1 = 1 (the BASELINE configs use 1.0). */
+rbs_status rbs_set_rhs_constant(rbs_ctx* ctx, double value);
+
+/* ---------------------------------------------------------------------------
+ * Basis W (N x n, orthonormal columns) and offline blocks
+ * A_{n,q} = W^T A_q W, f_{n,1} = W^T f_1 (eq12c).
+ *
+ * rbs_basis_storage_size: device bytes the context needs to keep W (in the
+ *   internal node-major padded layout) and the offline blocks.
+ * rbs_load_basis: copies W_dev (column-major, leading dimension ldw >= N,
+ *   borrowed) into storage_dev (caller-owned, RETAINED until the next
+ *   load/destroy).  ANq_host (Q x n x n row-major) / fn_host (n) may be NULL,
+ *   then they are computed on the device from W (stencil applications +
+ *   projections); otherwise they are copied.  Synchronises `stream`.
+ *   1 <= n <= RBS_MAX_N (n = 0 allowed: empty basis, RBCG = SGS-PCG).
+ *   Errors: RBS_E_STATE (no operator), RBS_E_DIM, RBS_E_NOMEM, RBS_E_CUDA.
+ * rbs_get_offline_blocks: copies the blocks in use to host (Q*n*n, n).
+ */
+rbs_status rbs_basis_storage_size(const rbs_ctx* ctx, int n, size_t* bytes);
+rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
+                          const double* ANq_host, const double* fn_host,
+                          void* storage_dev, size_t storage_bytes, void* stream);
+rbs_status rbs_get_offline_blocks(const rbs_ctx* ctx, double* ANq_host, double* fn_host);
+
+/* ---------------------------------------------------------------------------
+ * Batched online solve (RBI: algorithm1; RBCG: PAPER.md:
+ * 260-279 algorithm2) of B queries against the loaded basis.
+ */
+typedef struct {
+    int method;          /* RBS_RBI | RBS_RBCG (default RBCG) */
+    double tol;          /* relative residual ||r||/||f|| (default 1e-10, AMB-7) */
+    int max_iter;        /* default 20000 (RBCG) -- RBI callers set e.g. 500000 */
+    int smoother;        /* RBS_SMOOTH_SYM_RBGS (default) | RBS_SMOOTH_FWD_RBGS (AMB-5/6) */
+    int sweeps;          /* nu >= 0 (default 1); 0 = no smoothing (Lemma 2 tests) */
+    double delta;        /* PRECOND threshold (default 1e-12, AMB-11) */
+    int record_history;  /* 1: fill history[B][max_iter+1] */
+    int x_location;      /* RBS_MEM_DEVICE (default) | RBS_MEM_HOST for X */
+    int graph_chunk;     /* iterations per captured CUDA graph (default 16, even) */
+} rbs_solve_opts;
+
+void rbs_default_opts(rbs_solve_opts* opts);
+
+/* Device workspace bytes for a batch of B queries with these options. */
+rbs_status rbs_solve_workspace_size(const rbs_ctx* ctx, int B, const rbs_solve_opts* opts,
+                                    size_t* bytes);
+
+/*
+ * rbs_solve_batch:
+ *  B         1..RBS_MAX_BATCH queries.
+ *  mu_host   B x P host array (P = Q), theta_q = mu_q.  Values outside the
+ *            sampling box are accepted; A(mu) must be SPD for convergence.
+ *  rhs_dev   NULL (use f of rbs_set_rhs_constant) or a B x N device array of
+ *            per-query right-hand sides (e.g. Lemma-1 tests).
+ *  X         B x N output (device, or host when opts->x_location == HOST).
+ *  iters, qstatus, relres (last recurrence/true residual ratio), true_relres
+ *            (||f - A x||/||f|| recomputed after exit): host arrays of B
+ *            (any may be NULL).
+ *  a_n       host B x n: reduced coefficients of the first RB correction
+ *            (x_hat = W a_n) or NULL.
+ *  history   host B x (max_iter+1) relative residuals, NaN-padded; requires
+ *            opts->record_history (else ignored; may be NULL).
+ *  workspace_dev / workspace_bytes: >= rbs_solve_workspace_size.
+ *  Synchronises `stream` before returning.
+ *  Errors: RBS_E_STATE (no basis), RBS_E_DIM, RBS_E_ARG, RBS_E_NOMEM, RBS_E_CUDA.
+ */
+rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* opts,
+                           const double* rhs_dev, double* X, int* iters, int* qstatus,
+                           double* relres, double* true_relres, double* a_n, double* history,
+                           void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* Number of kernel launches issued by the last rbs_solve_batch (instrumentation). */
+int64_t rbs_last_launch_count(const rbs_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Offline greedy build (algorithm0; adaptive: PAPER.md:294-308
+ * algorithm3, snapshots by RBCG with W_{N-1}; DESIGN.md AMB-13).
+ *  mu_train_host  n_train x P (host).  mu_1 = mu_train[0].
+ *  W_out_dev      column-major N x n_max device array (caller-owned).
+ *  ANq_host_out   Q x n_max x n_max (row stride n_max) offline blocks or NULL.
+ *  fn_host_out    n_max or NULL.
+ *  selected, indicator, snap_iters: host arrays of n_max (may be NULL).
+ *  Snapshot solve: RBCG, relative tolerance snapshot_tol; MGS with one
+ *  re-orthogonalisation, reject if ||w|| < drop_tol ||x||.
+ * The context's basis state is replaced by the built basis (held in
+ * workspace_dev, which is RETAINED like storage_dev of rbs_load_basis).
+ */
+rbs_status rbs_greedy_workspace_size(const rbs_ctx* ctx, int n_train, int n_max, size_t* bytes);
+rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train_host, int n_max,
+                            int mode, double snapshot_tol, double drop_tol, double* W_out_dev,
+                            double* ANq_host_out, double* fn_host_out, int* n_out, int* selected,
+                            double* indicator, int* snap_iters, int* n_rejected,
+                            void* workspace_dev, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBS_H */

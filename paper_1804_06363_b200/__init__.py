@@ -1,0 +1,296 @@
+"""Thin Python binding of librbs.so (include/rbs.h): argument marshalling only.
+
+Every step of the RB online solve runs in the library's sm_100a kernels.
+PyTorch is used for device memory and streams.  There is no CPU fallback: if
+librbs.so is missing or cannot be loaded, importing the binding raises.
+
+Functions carry the C names (rbs_create, rbs_set_operator_blocks,
+rbs_load_basis, rbs_solve_batch, rbs_build_greedy, ...); `Solver` is a small
+convenience wrapper that owns the torch buffers a context needs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "librbs.so")
+
+RBS_RBI, RBS_RBCG = 0, 1
+RBS_SMOOTH_SYM_RBGS, RBS_SMOOTH_FWD_RBGS = 0, 1
+RBS_MEM_DEVICE, RBS_MEM_HOST = 0, 1
+RBS_GREEDY_PLAIN, RBS_GREEDY_ADAPTIVE = 0, 1
+QSTATUS = {0: "CONVERGED", 1: "MAXIT", 2: "REDUCED_NOT_SPD", 3: "CURVATURE", 4: "PRECOND",
+           5: "NONFINITE"}
+
+
+class RbsError(RuntimeError):
+    pass
+
+
+class rbs_solve_opts(C.Structure):
+    _fields_ = [("method", C.c_int), ("tol", C.c_double), ("max_iter", C.c_int),
+                ("smoother", C.c_int), ("sweeps", C.c_int), ("delta", C.c_double),
+                ("record_history", C.c_int), ("x_location", C.c_int), ("graph_chunk", C.c_int)]
+
+
+_lib = None
+
+_SIGS = {
+    "rbs_version": (C.c_int, []),
+    "rbs_status_string": (C.c_char_p, [C.c_int]),
+    "rbs_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "rbs_destroy": (None, [C.c_void_p]),
+    "rbs_last_error": (C.c_char_p, [C.c_void_p]),
+    "rbs_last_launch_count": (C.c_int64, [C.c_void_p]),
+    "rbs_set_operator_blocks": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int)]),
+    "rbs_set_rhs_constant": (C.c_int, [C.c_void_p, C.c_double]),
+    "rbs_basis_storage_size": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_size_t)]),
+    "rbs_load_basis": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "rbs_get_offline_blocks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rbs_default_opts": (None, [C.POINTER(rbs_solve_opts)]),
+    "rbs_solve_workspace_size": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(rbs_solve_opts),
+                                           C.POINTER(C.c_size_t)]),
+    "rbs_solve_batch": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(rbs_solve_opts),
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                  C.c_void_p]),
+    "rbs_greedy_workspace_size": (C.c_int, [C.c_void_p, C.c_int, C.c_int,
+                                            C.POINTER(C.c_size_t)]),
+    "rbs_build_greedy": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                   C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.POINTER(C.c_int), C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.POINTER(C.c_int), C.c_void_p, C.c_size_t, C.c_void_p]),
+}
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load librbs.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise RbsError(f"{_SO} not built; run `python -m paper_1804_06363_b200.build`")
+        L = C.CDLL(_SO)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(a.data_ptr())
+
+
+def _check(ctx, st, what):
+    if st != 0:
+        detail = lib().rbs_last_error(ctx).decode() if ctx else ""
+        raise RbsError(f"{what}: {lib().rbs_status_string(st).decode()} {detail}")
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+# ---- C-named marshalling functions ------------------------------------------
+def rbs_create(device: int = 0):
+    h = C.c_void_p()
+    _check(None, lib().rbs_create(int(device), C.byref(h)), "rbs_create")
+    return h
+
+
+def rbs_destroy(ctx):
+    lib().rbs_destroy(ctx)
+
+
+def rbs_set_operator_blocks(ctx, dim, m, blocks):
+    mm = (C.c_int64 * 3)(*([int(m)] * 3))
+    bb = (C.c_int * 3)(*(list(blocks) + [1] * (3 - len(blocks))))
+    _check(ctx, lib().rbs_set_operator_blocks(ctx, int(dim), mm, bb), "rbs_set_operator_blocks")
+
+
+def rbs_set_rhs_constant(ctx, value):
+    _check(ctx, lib().rbs_set_rhs_constant(ctx, float(value)), "rbs_set_rhs_constant")
+
+
+def rbs_basis_storage_size(ctx, n):
+    s = C.c_size_t()
+    _check(ctx, lib().rbs_basis_storage_size(ctx, int(n), C.byref(s)), "rbs_basis_storage_size")
+    return s.value
+
+
+def rbs_load_basis(ctx, n, W_dev, ldw, ANq_host, fn_host, storage, stream=None):
+    _check(ctx, lib().rbs_load_basis(ctx, int(n), _ptr(W_dev), int(ldw), _ptr(ANq_host),
+                                     _ptr(fn_host), _ptr(storage), storage.numel(),
+                                     _stream(stream)), "rbs_load_basis")
+
+
+def rbs_get_offline_blocks(ctx, Q, n):
+    A = np.empty((Q, n, n))
+    f = np.empty(n)
+    _check(ctx, lib().rbs_get_offline_blocks(ctx, _ptr(A), _ptr(f)), "rbs_get_offline_blocks")
+    return A, f
+
+
+def rbs_default_opts(**kw):
+    o = rbs_solve_opts()
+    lib().rbs_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def rbs_solve_workspace_size(ctx, B, opts):
+    s = C.c_size_t()
+    _check(ctx, lib().rbs_solve_workspace_size(ctx, int(B), C.byref(opts), C.byref(s)),
+           "rbs_solve_workspace_size")
+    return s.value
+
+
+def rbs_solve_batch(ctx, B, mu_host, opts, rhs_dev, X, iters, qstatus, relres, true_relres,
+                    a_n, history, workspace, stream=None):
+    _check(ctx, lib().rbs_solve_batch(ctx, int(B), _ptr(mu_host), C.byref(opts), _ptr(rhs_dev),
+                                      _ptr(X), _ptr(iters), _ptr(qstatus), _ptr(relres),
+                                      _ptr(true_relres), _ptr(a_n), _ptr(history),
+                                      _ptr(workspace), workspace.numel(), _stream(stream)),
+           "rbs_solve_batch")
+
+
+def rbs_last_launch_count(ctx):
+    return int(lib().rbs_last_launch_count(ctx))
+
+
+def rbs_greedy_workspace_size(ctx, n_train, n_max):
+    s = C.c_size_t()
+    _check(ctx, lib().rbs_greedy_workspace_size(ctx, int(n_train), int(n_max), C.byref(s)),
+           "rbs_greedy_workspace_size")
+    return s.value
+
+
+def rbs_build_greedy(ctx, mu_train, n_max, mode, snapshot_tol, drop_tol, W_out, workspace,
+                     stream=None):
+    mu_train = np.ascontiguousarray(mu_train, dtype=np.float64)
+    nt, P = mu_train.shape
+    ANq = np.zeros((P, n_max, n_max))
+    fn = np.zeros(n_max)
+    n_out = C.c_int(0)
+    rej = C.c_int(0)
+    sel = np.full(n_max, -1, dtype=np.int32)
+    ind = np.full(n_max, np.nan)
+    its = np.zeros(n_max, dtype=np.int32)
+    _check(ctx, lib().rbs_build_greedy(ctx, nt, _ptr(mu_train), int(n_max), int(mode),
+                                       float(snapshot_tol), float(drop_tol), _ptr(W_out),
+                                       _ptr(ANq), _ptr(fn), C.byref(n_out), _ptr(sel), _ptr(ind),
+                                       _ptr(its), C.byref(rej), _ptr(workspace),
+                                       workspace.numel(), _stream(stream)), "rbs_build_greedy")
+    n = n_out.value
+    return dict(n=n, ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(), selected=sel[:n].copy(),
+                indicator=ind[:n].copy(), snap_iters=its[:n].copy(), n_rejected=rej.value)
+
+
+# ---- convenience wrapper -----------------------------------------------------
+class Solver:
+    """Owns a context plus the torch buffers it borrows (storage, workspace)."""
+
+    def __init__(self, dim, m, blocks, device=0, rhs_constant=1.0):
+        import torch
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        self.ctx = rbs_create(device)
+        self.dim, self.m, self.blocks = int(dim), int(m), tuple(blocks)
+        self.N = self.m ** self.dim
+        self.Q = int(np.prod(self.blocks))
+        rbs_set_operator_blocks(self.ctx, dim, m, blocks)
+        rbs_set_rhs_constant(self.ctx, rhs_constant)
+        self.n = None
+        self._storage = None
+        self._ws = {}
+
+    def __del__(self):
+        try:
+            rbs_destroy(self.ctx)
+        except Exception:
+            pass
+
+    def _bytes(self, nbytes):
+        return self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.device)
+
+    def load_basis(self, W, ANq=None, fn=None, stream=None):
+        """W: (N, n) array (numpy or torch); stored column-major on the device."""
+        torch = self.torch
+        Wt = torch.as_tensor(np.asarray(W) if not torch.is_tensor(W) else W, dtype=torch.float64)
+        n = Wt.shape[1]
+        Wc = Wt.t().contiguous().to(self.device)  # (n, N) row-major == (N, n) column-major
+        self._storage = self._bytes(rbs_basis_storage_size(self.ctx, n))
+        A = None if ANq is None else np.ascontiguousarray(ANq, dtype=np.float64)
+        f = None if fn is None else np.ascontiguousarray(fn, dtype=np.float64)
+        rbs_load_basis(self.ctx, n, Wc, self.N, A, f, self._storage, stream)
+        self.n = n
+        self._ws.clear()
+        return self
+
+    def offline_blocks(self):
+        return rbs_get_offline_blocks(self.ctx, self.Q, self.n)
+
+    def opts(self, **kw):
+        return rbs_default_opts(**kw)
+
+    def workspace(self, B, opts):
+        key = (B, opts.method, opts.max_iter, opts.record_history, opts.x_location)
+        if key not in self._ws:
+            self._ws[key] = self._bytes(rbs_solve_workspace_size(self.ctx, B, opts))
+        return self._ws[key]
+
+    def solve_batch(self, mu, rhs=None, X=None, stream=None, want_a_n=True, **kw):
+        """mu: (B, P) host array.  rhs: optional (B, N) cuda tensor.  Returns dict."""
+        torch = self.torch
+        o = self.opts(**kw)
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        B = mu.shape[0]
+        if X is None:
+            if o.x_location == RBS_MEM_HOST:
+                X = torch.empty((B, self.N), dtype=torch.float64, pin_memory=True)
+            else:
+                X = torch.empty((B, self.N), dtype=torch.float64, device=self.device)
+        its = np.zeros(B, dtype=np.int32)
+        st = np.zeros(B, dtype=np.int32)
+        rel = np.zeros(B)
+        trr = np.zeros(B)
+        a_n = np.zeros((B, max(self.n or 0, 1))) if want_a_n else None
+        hist = np.full((B, o.max_iter + 1), np.nan) if o.record_history else None
+        ws = self.workspace(B, o)
+        rbs_solve_batch(self.ctx, B, mu, o, rhs, X, its, st, rel, trr, a_n, hist, ws, stream)
+        out = dict(X=X, its=its, status=[QSTATUS[int(s)] for s in st], qstatus=st, relres=rel,
+                   true_relres=trr, a_n=None if a_n is None else a_n[:, :(self.n or 0)],
+                   launches=rbs_last_launch_count(self.ctx))
+        if hist is not None:
+            out["history"] = [hist[b, :its[b] + 1].copy() for b in range(B)]
+        return out
+
+    def build_greedy(self, mu_train, n_max, adaptive=True, snapshot_tol=1e-12, drop_tol=1e-10,
+                     stream=None, load=True):
+        torch = self.torch
+        mu_train = np.ascontiguousarray(mu_train, dtype=np.float64)
+        Wcol = torch.zeros((n_max, self.N), dtype=torch.float64, device=self.device)
+        ws = self._bytes(rbs_greedy_workspace_size(self.ctx, mu_train.shape[0], n_max))
+        res = rbs_build_greedy(self.ctx, mu_train, n_max,
+                               RBS_GREEDY_ADAPTIVE if adaptive else RBS_GREEDY_PLAIN,
+                               snapshot_tol, drop_tol, Wcol, ws, stream)
+        n = res["n"]
+        res["W"] = Wcol[:n].t()  # (N, n) view of the column-major result
+        if load:
+            self.load_basis(res["W"], res["ANq"], res["fn"], stream)
+        return res

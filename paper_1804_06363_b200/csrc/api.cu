@@ -1,0 +1,754 @@
+// api.cu -- C ABI (include/rbs.h) of the B200 batched RB online solver.
+//
+// Host runtime: context + validation, basis packing and on-device offline
+// blocks (eq12c), and the batched RBI / RBCG drivers
+// (algorithm1, 260-279 algorithm2).  The iteration loop is
+// captured once into a CUDA graph of `graph_chunk` iterations and replayed;
+// per-query convergence is tracked on the device (masks + a done flag) and
+// the host polls the flag one graph behind, so the loop never stalls on a
+// host round trip.  The library allocates no device memory: all buffers are
+// carved out of caller-owned storage / workspace.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rbs.h"
+#include "kernels.cuh"
+
+using namespace rbs;
+
+struct rbs_ctx {
+    int device = 0;
+    int num_sms = 148;
+    std::string err;
+    // operator
+    bool has_op = false;
+    Geo g{};
+    int64_t N8 = 0;
+    double fconst = 1.0;
+    // basis
+    bool has_basis = false;
+    int n = 0, npad = 0;
+    double* Wi = nullptr;    // [N8][npad]
+    double* dANq = nullptr;  // [Q][npad][npad]
+    double* scratch = nullptr;
+    std::vector<double> hANq, hfn;  // Q*n*n, n (fn = W^T 1)
+    // instrumentation / polling
+    int64_t launches = 0;
+    int* h_flag = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    std::string gkey;
+    int g_per_chunk = 0;
+};
+
+namespace {
+
+rbs_status fail(rbs_ctx* c, rbs_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(ctx, RBS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKL()                                                                               \
+    do {                                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(ctx, RBS_E_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int pow2_batch(int B) {
+    int p = 8;
+    while (p < B) p <<= 1;
+    return p;
+}
+inline int ilog2(int v) {
+    int l = 0;
+    while ((1 << l) < v) ++l;
+    return l;
+}
+
+// number of CTAs of the projection pass: depends on N only (determinism)
+inline int proj_ctas(const Geo& g) {
+    int64_t groups = (g.N + 3) / 4;
+    int64_t c = (groups + 31) / 32;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(c, 296));
+}
+inline int flat_ctas(const Geo& g) {
+    int64_t c = (g.N + 31) / 32;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(c, 1184));
+}
+inline int grid_for(int64_t work, int per, int cap) {
+    int64_t c = (work + per - 1) / per;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(c, cap));
+}
+
+// bump allocator over a caller buffer
+struct Carve {
+    char* base;
+    size_t off = 0;
+    explicit Carve(void* b) : base((char*)b) {}
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = base ? (T*)(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+size_t proj_smem(const Geo& g, int Bp, int npad) {
+    const int nlc = 8 / (Bp / 8) > 0 ? 8 / (Bp / 8) : 1;
+    return (size_t)(g.Q * Bp + Bp + nlc * (npad + 1) * Bp) * 8 + (size_t)Bp * 4 + 16;
+}
+size_t flat_smem(const Geo& g, int Bp) { return (size_t)g.Q * Bp * 8 + (size_t)Bp * 4 + 16; }
+
+template <int MODE>
+void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const ProjArgs& a) {
+    if (g.dim == 2) k_proj<MODE, 2><<<grid, kThreads, smem, st>>>(a);
+    else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
+}
+
+bool g_attr_done = false;
+void set_attrs() {
+    if (g_attr_done) return;
+    const int big = 200 * 1024;
+    cudaFuncSetAttribute(k_proj<MODE_CG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_proj<MODE_CG, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_proj<MODE_RESID, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_proj<MODE_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_proj<MODE_PLAIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_proj<MODE_PLAIN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_gs<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_gs<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_gs<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_gs<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_cgp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_cgp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    g_attr_done = true;
+}
+
+// storage of a basis of dimension n
+struct BasisLayout {
+    double *Wi, *ANq, *Z, *part, *rows;
+    size_t bytes;
+};
+BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
+    const int npad = (int)round_up(n, 8);
+    Carve cv(base);
+    BasisLayout L;
+    L.Wi = cv.take<double>((size_t)c->N8 * std::max(npad, 8));
+    L.ANq = cv.take<double>((size_t)c->g.Q * npad * npad + 8);
+    L.Z = cv.take<double>((size_t)c->N8 * 8);
+    L.part = cv.take<double>((size_t)8 * (npad + 1) * proj_ctas(c->g));
+    L.rows = cv.take<double>((size_t)8 * (npad + 1));
+    L.bytes = cv.off + 256;
+    return L;
+}
+
+// solve workspace
+struct SolveLayout {
+    double *X, *R, *P0, *P1, *Y, *F, *Xout;
+    double *theta, *fproj, *L, *E, *a_n, *partP, *partF;
+    double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist;
+    int *active, *status, *its, *pivot, *ints;
+    size_t bytes;
+};
+SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool rhs, void* base) {
+    const int Bp = pow2_batch(B), npad = c->npad;
+    const size_t vec = (size_t)c->N8 * Bp;
+    const int nct = proj_ctas(c->g), nctf = flat_ctas(c->g);
+    Carve cv(base);
+    SolveLayout L{};
+    const bool cg = o->method == RBS_RBCG;
+    L.X = cv.take<double>(vec);
+    L.R = cg ? cv.take<double>(vec) : nullptr;
+    L.P0 = cg ? cv.take<double>(vec) : nullptr;
+    L.P1 = cg ? cv.take<double>(vec) : nullptr;
+    L.Y = cg ? cv.take<double>(vec) : nullptr;
+    L.F = rhs ? cv.take<double>(vec) : nullptr;
+    L.Xout = o->x_location == RBS_MEM_HOST ? cv.take<double>((size_t)B * c->g.N) : nullptr;
+    L.theta = cv.take<double>((size_t)c->g.Q * Bp);
+    L.fproj = cv.take<double>((size_t)Bp * (npad + 1));
+    L.L = cv.take<double>((size_t)Bp * npad * npad + 8);
+    L.E = cv.take<double>((size_t)std::max(npad, 8) * Bp);
+    L.a_n = cv.take<double>((size_t)Bp * npad + 8);
+    L.partP = cv.take<double>((size_t)Bp * (npad + 1) * nct);
+    L.partF = cv.take<double>((size_t)Bp * 2 * nctf);
+    L.alpha = cv.take<double>(Bp);
+    L.beta = cv.take<double>(Bp);
+    L.rho = cv.take<double>(Bp);
+    L.rr = cv.take<double>(Bp);
+    L.fnorm = cv.take<double>(Bp);
+    L.relres = cv.take<double>(Bp);
+    L.hist = o->record_history ? cv.take<double>((size_t)Bp * (o->max_iter + 1)) : nullptr;
+    L.active = cv.take<int>(Bp);
+    L.status = cv.take<int>(Bp);
+    L.its = cv.take<int>(Bp);
+    L.pivot = cv.take<int>(Bp);
+    L.ints = cv.take<int>(8);
+    L.bytes = cv.off + 256;
+    return L;
+}
+
+rbs_status check_opts(rbs_ctx* ctx, const rbs_solve_opts* o) {
+    if (!o) return fail(ctx, RBS_E_ARG, "opts is NULL");
+    if (o->method != RBS_RBI && o->method != RBS_RBCG) return fail(ctx, RBS_E_ARG, "bad method");
+    if (o->smoother != RBS_SMOOTH_SYM_RBGS && o->smoother != RBS_SMOOTH_FWD_RBGS)
+        return fail(ctx, RBS_E_UNSUPPORTED, "smoother must be SYM_RBGS or FWD_RBGS");
+    if (o->sweeps < 0 || o->sweeps > 64) return fail(ctx, RBS_E_ARG, "sweeps out of range");
+    if (o->max_iter < 0) return fail(ctx, RBS_E_ARG, "max_iter < 0");
+    if (!(o->tol >= 0.0)) return fail(ctx, RBS_E_ARG, "tol must be >= 0");
+    if (o->x_location != RBS_MEM_DEVICE && o->x_location != RBS_MEM_HOST)
+        return fail(ctx, RBS_E_ARG, "bad x_location");
+    if (o->graph_chunk < 2 || (o->graph_chunk & 1)) return fail(ctx, RBS_E_ARG, "graph_chunk must be even >= 2");
+    return RBS_OK;
+}
+
+// half-sweep colour sequence: symmetric sweep = R,B,B,R; repeated half-sweeps
+// of one colour are bitwise no-ops (AMB-6) and are dropped.
+std::vector<int> color_seq(int smoother, int sweeps) {
+    std::vector<int> s;
+    for (int k = 0; k < sweeps; ++k) {
+        const int sym[4] = {0, 1, 1, 0}, fwd[2] = {0, 1};
+        const int* seq = smoother == RBS_SMOOTH_SYM_RBGS ? sym : fwd;
+        const int len = smoother == RBS_SMOOTH_SYM_RBGS ? 4 : 2;
+        for (int t = 0; t < len; ++t)
+            if (s.empty() || s.back() != seq[t]) s.push_back(seq[t]);
+    }
+    return s;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int rbs_version(void) { return RBS_VERSION; }
+
+const char* rbs_status_string(rbs_status s) {
+    switch (s) {
+        case RBS_OK: return "RBS_OK";
+        case RBS_E_ARG: return "RBS_E_ARG";
+        case RBS_E_DIM: return "RBS_E_DIM";
+        case RBS_E_STATE: return "RBS_E_STATE";
+        case RBS_E_NOT_SPD: return "RBS_E_NOT_SPD";
+        case RBS_E_CUDA: return "RBS_E_CUDA";
+        case RBS_E_NOMEM: return "RBS_E_NOMEM";
+        case RBS_E_UNSUPPORTED: return "RBS_E_UNSUPPORTED";
+    }
+    return "RBS_E_UNKNOWN";
+}
+
+rbs_status rbs_create(int cuda_device, rbs_ctx** out) {
+    rbs_ctx* ctx = nullptr;
+    if (!out) return RBS_E_ARG;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || cuda_device < 0 || cuda_device >= count)
+        return RBS_E_CUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return RBS_E_CUDA;
+    if (prop.major != 10) return RBS_E_UNSUPPORTED;
+    if (cudaSetDevice(cuda_device) != cudaSuccess) return RBS_E_CUDA;
+    ctx = new rbs_ctx();
+    ctx->device = cuda_device;
+    ctx->num_sms = prop.multiProcessorCount;
+    if (cudaHostAlloc(&ctx->h_flag, 4 * sizeof(int), cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev[1], cudaEventDisableTiming) != cudaSuccess) {
+        delete ctx;
+        return RBS_E_CUDA;
+    }
+    set_attrs();
+    *out = ctx;
+    return RBS_OK;
+}
+
+void rbs_destroy(rbs_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+}
+
+const char* rbs_last_error(const rbs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+int64_t rbs_last_launch_count(const rbs_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], const int blocks[3]) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!m || !blocks) return fail(ctx, RBS_E_ARG, "m/blocks is NULL");
+    if (dim != 2 && dim != 3) return fail(ctx, RBS_E_DIM, "dim must be 2 or 3");
+    for (int d = 0; d < dim; ++d) {
+        if (m[d] != m[0]) return fail(ctx, RBS_E_UNSUPPORTED, "m must be equal on every axis");
+        if (blocks[d] < 1 || blocks[d] > 16) return fail(ctx, RBS_E_DIM, "blocks must be in 1..16");
+    }
+    if (m[0] < 1 || m[0] > 65535) return fail(ctx, RBS_E_DIM, "m must be in 1..65535");
+    const int64_t N = dim == 2 ? m[0] * m[0] : m[0] * m[0] * m[0];
+    if (N >= (int64_t(1) << 31)) return fail(ctx, RBS_E_DIM, "N too large (>= 2^31)");
+    Geo g{};
+    g.dim = dim;
+    g.m = (int)m[0];
+    g.N = N;
+    g.px = blocks[0];
+    g.py = blocks[1];
+    g.pz = dim == 3 ? blocks[2] : 1;
+    g.Q = g.px * g.py * g.pz;
+    if (g.Q > RBS_MAX_Q) return fail(ctx, RBS_E_DIM, "Q > RBS_MAX_Q");
+    g.fm = make_fastdiv((uint32_t)g.m);
+    g.f2m1 = make_fastdiv((uint32_t)(2 * (g.m + 1)));
+    g.scale = (double)(g.m + 1) * (double)(g.m + 1);
+    g.h2 = 1.0 / g.scale;
+    ctx->g = g;
+    ctx->N8 = round_up(N, 8);
+    ctx->has_op = true;
+    ctx->has_basis = false;
+    return RBS_OK;
+}
+
+rbs_status rbs_set_rhs_constant(rbs_ctx* ctx, double value) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!std::isfinite(value)) return fail(ctx, RBS_E_ARG, "rhs constant must be finite");
+    ctx->fconst = value;
+    return RBS_OK;
+}
+
+rbs_status rbs_basis_storage_size(const rbs_ctx* c, int n, size_t* bytes) {
+    rbs_ctx* ctx = const_cast<rbs_ctx*>(c);
+    if (!ctx || !bytes) return RBS_E_ARG;
+    if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
+    if (n < 0 || n > RBS_MAX_N) return fail(ctx, RBS_E_DIM, "n out of range");
+    *bytes = basis_layout(ctx, n, nullptr).bytes;
+    return RBS_OK;
+}
+
+rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
+                          const double* ANq_host, const double* fn_host, void* storage_dev,
+                          size_t storage_bytes, void* stream) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
+    if (n < 0 || n > RBS_MAX_N) return fail(ctx, RBS_E_DIM, "n out of range 0..64");
+    if (n > 0 && (!W_dev || ldw < ctx->g.N)) return fail(ctx, RBS_E_DIM, "W_dev NULL or ldw < N");
+    if (!storage_dev) return fail(ctx, RBS_E_ARG, "storage_dev is NULL");
+    BasisLayout L = basis_layout(ctx, n, storage_dev);
+    if (storage_bytes < L.bytes) return fail(ctx, RBS_E_NOMEM, "storage too small");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geo& g = ctx->g;
+    const int npad = (int)round_up(n, 8);
+    ctx->has_basis = false;
+    ctx->n = n;
+    ctx->npad = npad;
+    ctx->Wi = L.Wi;
+    ctx->dANq = L.ANq;
+    ctx->scratch = L.Z;
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+    const int Q = g.Q;
+    if (n > 0) {
+        k_pack_W<<<grid_for(ctx->N8 * npad, 256, 4 * ctx->num_sms * 8), 256, 0, st>>>(
+            W_dev, ldw, g.N, ctx->N8, n, npad, L.Wi);
+        CKL();
+    }
+    ctx->hANq.assign((size_t)Q * n * n, 0.0);
+    ctx->hfn.assign(n, 0.0);
+    if (n > 0 && ANq_host) {
+        std::memcpy(ctx->hANq.data(), ANq_host, sizeof(double) * Q * n * n);
+    } else if (n > 0) {
+        // A_{n,q} = W^T A_q W, 8 columns at a time: Z = A_q W[:, j0:j0+8], then
+        // the DMMA projection W^T Z; entries (i <= j) mirrored (oracle O-3).
+        const int nct = proj_ctas(g);
+        std::vector<double> rows((size_t)8 * (npad + 1));
+        for (int q = 0; q < Q; ++q)
+            for (int j0 = 0; j0 < npad; j0 += 8) {
+                const int grid = grid_for(g.N * 8, kThreads, ctx->num_sms * 8);
+                if (g.dim == 2) k_apply_Aq<2><<<grid, kThreads, 0, st>>>(g, q, L.Wi, npad, j0, L.Z);
+                else k_apply_Aq<3><<<grid, kThreads, 0, st>>>(g, q, L.Wi, npad, j0, L.Z);
+                CKL();
+                ProjArgs a{};
+                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+                a.W = L.Wi; a.V = L.Z; a.part = L.part;
+                launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
+                CKL();
+                k_reduce_rows<<<8, 128, 0, st>>>(L.part, npad + 1, nct, L.rows);
+                CKL();
+                CK(cudaMemcpyAsync(rows.data(), L.rows, rows.size() * 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (int jj = 0; jj < 8 && j0 + jj < n; ++jj) {
+                    const int j = j0 + jj;
+                    for (int i = 0; i <= j; ++i) {
+                        const double v = rows[(size_t)jj * (npad + 1) + i];
+                        ctx->hANq[((size_t)q * n + i) * n + j] = v;
+                        ctx->hANq[((size_t)q * n + j) * n + i] = v;
+                    }
+                }
+            }
+    }
+    if (n > 0 && fn_host) {
+        std::memcpy(ctx->hfn.data(), fn_host, sizeof(double) * n);
+    } else if (n > 0) {
+        const int nct = proj_ctas(g);
+        ProjArgs a{};
+        a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+        a.W = L.Wi; a.V = nullptr; a.vconst = 1.0; a.part = L.part;
+        launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
+        CKL();
+        k_reduce_rows<<<8, 128, 0, st>>>(L.part, npad + 1, nct, L.rows);
+        CKL();
+        std::vector<double> rows((size_t)8 * (npad + 1));
+        CK(cudaMemcpyAsync(rows.data(), L.rows, rows.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int j = 0; j < n; ++j) ctx->hfn[j] = rows[j];
+    }
+    // padded device copy of the blocks
+    std::vector<double> pad((size_t)Q * npad * npad + 8, 0.0);
+    for (int q = 0; q < Q; ++q)
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                pad[((size_t)q * npad + i) * npad + j] = ctx->hANq[((size_t)q * n + i) * n + j];
+    CK(cudaMemcpyAsync(L.ANq, pad.data(), pad.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->has_basis = true;
+    return RBS_OK;
+}
+
+rbs_status rbs_get_offline_blocks(const rbs_ctx* c, double* ANq_host, double* fn_host) {
+    rbs_ctx* ctx = const_cast<rbs_ctx*>(c);
+    if (!ctx) return RBS_E_ARG;
+    if (!ctx->has_basis) return fail(ctx, RBS_E_STATE, "no basis loaded");
+    if (ANq_host) std::memcpy(ANq_host, ctx->hANq.data(), ctx->hANq.size() * 8);
+    if (fn_host) std::memcpy(fn_host, ctx->hfn.data(), ctx->hfn.size() * 8);
+    return RBS_OK;
+}
+
+void rbs_default_opts(rbs_solve_opts* o) {
+    if (!o) return;
+    o->method = RBS_RBCG;
+    o->tol = 1e-10;
+    o->max_iter = 20000;
+    o->smoother = RBS_SMOOTH_SYM_RBGS;
+    o->sweeps = 1;
+    o->delta = 1e-12;
+    o->record_history = 0;
+    o->x_location = RBS_MEM_DEVICE;
+    o->graph_chunk = 16;
+}
+
+rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opts* o, size_t* bytes) {
+    rbs_ctx* ctx = const_cast<rbs_ctx*>(c);
+    if (!ctx || !bytes) return RBS_E_ARG;
+    if (!ctx->has_basis) return fail(ctx, RBS_E_STATE, "no basis loaded");
+    if (B < 1 || B > RBS_MAX_BATCH) return fail(ctx, RBS_E_DIM, "B out of range 1..64");
+    rbs_status s = check_opts(ctx, o);
+    if (s != RBS_OK) return s;
+    *bytes = solve_layout(ctx, B, o, true, nullptr).bytes;
+    return RBS_OK;
+}
+
+rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* o,
+                           const double* rhs_dev, double* X, int* iters, int* qstatus,
+                           double* relres, double* true_relres, double* a_n, double* history,
+                           void* workspace_dev, size_t workspace_bytes, void* stream) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    ctx->launches = 0;
+    if (!ctx->has_basis) return fail(ctx, RBS_E_STATE, "no basis loaded");
+    if (B < 1 || B > RBS_MAX_BATCH) return fail(ctx, RBS_E_DIM, "B out of range 1..64");
+    if (!mu_host || !X || !workspace_dev) return fail(ctx, RBS_E_ARG, "mu_host/X/workspace is NULL");
+    rbs_status s0 = check_opts(ctx, o);
+    if (s0 != RBS_OK) return s0;
+    SolveLayout L = solve_layout(ctx, B, o, rhs_dev != nullptr, workspace_dev);
+    if (workspace_bytes < solve_layout(ctx, B, o, rhs_dev != nullptr, nullptr).bytes)
+        return fail(ctx, RBS_E_NOMEM, "workspace too small");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geo& g = ctx->g;
+    const int Bp = pow2_batch(B), lgB = ilog2(Bp), n = ctx->n, npad = ctx->npad, Q = g.Q;
+    const int nct = proj_ctas(g), nctf = flat_ctas(g);
+    const bool cg = o->method == RBS_RBCG;
+    const int64_t vecN = ctx->N8 * Bp;
+    const size_t psm = proj_smem(g, Bp, npad), fsm = flat_smem(g, Bp);
+    int64_t launches = 0;
+
+    // ---- parameters: theta_q = mu_q (Q = P), padded lanes get 1 -------------
+    std::vector<double> th((size_t)Q * Bp, 1.0);
+    for (int b = 0; b < B; ++b)
+        for (int q = 0; q < Q; ++q) {
+            const double v = mu_host[(size_t)b * Q + q];
+            th[(size_t)q * Bp + b] = v;
+        }
+    CK(cudaMemcpyAsync(L.theta, th.data(), th.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(L.ints, 0, 8 * sizeof(int), st));
+    int* kcount = L.ints;
+    int* done = L.ints + 1;
+    unsigned* ticket = (unsigned*)(L.ints + 2);
+    CK(cudaMemsetAsync(L.E, 0, (size_t)std::max(npad, 8) * Bp * 8, st));
+    CK(cudaMemsetAsync(L.a_n, 0, ((size_t)Bp * npad + 8) * 8, st));
+    if (L.hist) {
+        // NaN-fill history: 0xFF bytes are a NaN pattern
+        CK(cudaMemsetAsync(L.hist, 0xFF, (size_t)Bp * (o->max_iter + 1) * 8, st));
+    }
+    const int fgrid = grid_for(vecN, 256, ctx->num_sms * 8);
+
+    // ---- right-hand side, f_n and ||f|| per query ---------------------------
+    const double* Fv = nullptr;
+    if (rhs_dev) {
+        k_fill_batch<<<fgrid, 256, 0, st>>>(L.F, g.N, ctx->N8, Bp, B, rhs_dev, 0.0);
+        CKL();
+        ++launches;
+        Fv = L.F;
+        ProjArgs a{};
+        a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+        a.W = ctx->Wi; a.theta = L.theta; a.V = L.F; a.part = L.partP;
+        launch_proj<MODE_PLAIN>(g, nct, psm, st, a);
+        CKL();
+        k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct, L.fproj);
+        CKL();
+        launches += 2;
+    } else {
+        std::vector<double> fp((size_t)Bp * (npad + 1), 0.0);
+        for (int b = 0; b < Bp; ++b) {
+            for (int j = 0; j < n; ++j) fp[(size_t)b * (npad + 1) + j] = ctx->fconst * ctx->hfn[j];
+            fp[(size_t)b * (npad + 1) + npad] = ctx->fconst * ctx->fconst * (double)g.N;
+        }
+        CK(cudaMemcpyAsync(L.fproj, fp.data(), fp.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemsetAsync(L.X, 0, vecN * 8, st));
+    if (cg) {
+        CK(cudaMemsetAsync(L.P0, 0, vecN * 8, st));
+        CK(cudaMemsetAsync(L.P1, 0, vecN * 8, st));
+        k_fill_batch<<<fgrid, 256, 0, st>>>(L.R, g.N, ctx->N8, Bp, B, rhs_dev, ctx->fconst);
+        CKL();
+        ++launches;
+    }
+
+    SolveState S{};
+    S.B = B; S.Bp = Bp; S.n = n; S.npad = npad; S.nct = nct; S.nctf = nctf;
+    S.maxit = o->max_iter; S.method = cg ? 1 : 0; S.tol = o->tol; S.delta = o->delta;
+    S.ANq = ctx->dANq; S.Q = Q; S.theta = L.theta; S.fproj = L.fproj; S.L = L.L; S.E = L.E;
+    S.a_n = L.a_n; S.partP = L.partP; S.partF = L.partF; S.alpha = L.alpha; S.beta = L.beta;
+    S.rho = L.rho; S.rr = L.rr; S.fnorm = L.fnorm; S.relres = L.relres; S.active = L.active;
+    S.status = L.status; S.its = L.its; S.pivot = L.pivot; S.kcount = kcount; S.done = done;
+    S.ticket = ticket; S.hist = L.hist;
+
+    k_setup_reduced<<<Bp, 128, 0, st>>>(S, cg ? 0 : 1);
+    CKL();
+    ++launches;
+
+    const std::vector<int> seq = color_seq(o->smoother, o->sweeps);
+    const int pgrid = grid_for(((g.N + 7) / 8) * (Bp / 8), 8, ctx->num_sms * 16);
+
+    // ---- pass builders -------------------------------------------------------
+    auto prolong = [&](double* Yv, int acc) {
+        ProlongArgs a{};
+        a.N = g.N; a.Bp = Bp; a.npad = npad; a.W = ctx->Wi; a.E = L.E; a.active = L.active;
+        a.Y = Yv; a.accumulate = acc; a.done = done;
+        if (npad > 0) {
+            k_prolong<<<pgrid, kThreads, 0, st>>>(a);
+        } else if (!acc) {  // empty basis: y0 = 0
+            k_fill_batch<<<fgrid, 256, 0, st>>>(Yv, g.N, ctx->N8, Bp, 0, nullptr, 0.0);
+        } else {
+            return 0;
+        }
+        return 1;
+    };
+    auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last) {
+        GSArgs a{};
+        a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
+        a.Y = Yv; a.Rhs = rhs; a.rconst = rconst; a.part = L.partF; a.nctf = nctf; a.done = done;
+        int cnt = 0;
+        std::vector<int> cs = seq;
+        if (cs.empty() && last) cs.push_back(-1);
+        for (size_t t = 0; t < cs.size(); ++t) {
+            a.color = cs[t];
+            const bool l = last && t + 1 == cs.size();
+            if (g.dim == 2) {
+                if (l) k_gs<2, true><<<nctf, kThreads, fsm, st>>>(a);
+                else k_gs<2, false><<<nctf, kThreads, fsm, st>>>(a);
+            } else {
+                if (l) k_gs<3, true><<<nctf, kThreads, fsm, st>>>(a);
+                else k_gs<3, false><<<nctf, kThreads, fsm, st>>>(a);
+            }
+            ++cnt;
+        }
+        return cnt;
+    };
+    auto proj = [&](int mode, const double* P, bool use_active) {
+        ProjArgs a{};
+        a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+        a.W = ctx->Wi; a.theta = L.theta; a.active = use_active ? L.active : nullptr;
+        a.alpha = L.alpha; a.P = P; a.X = L.X; a.R = L.R; a.V = Fv; a.vconst = ctx->fconst;
+        a.part = L.partP; a.done = use_active ? done : nullptr;
+        if (mode == MODE_CG) launch_proj<MODE_CG>(g, nct, psm, st, a);
+        else launch_proj<MODE_RESID>(g, nct, psm, st, a);
+        return 1;
+    };
+    auto cgp = [&](const double* Pold, double* Pnew) {
+        CGPArgs a{};
+        a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
+        a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.part = L.partF; a.nctf = nctf;
+        a.done = done;
+        if (g.dim == 2) k_cgp<2><<<nctf, kThreads, fsm, st>>>(a);
+        else k_cgp<3><<<nctf, kThreads, fsm, st>>>(a);
+        return 1;
+    };
+
+    // ---- RBCG Step 2-3: y_0 = RBI(A, r_0, W, 1), rho_0 = r_0^T y_0 ------------
+    if (cg) {
+        launches += prolong(L.Y, 0);
+        launches += smooth(L.Y, L.R, 0.0, true);
+        k_beta<<<1, 512, 0, st>>>(S, 1);
+        ++launches;
+        CKL();
+    } else {
+        k_update_done<<<1, 1, 0, st>>>(L.active, Bp, done);
+        ++launches;
+        CKL();
+    }
+
+    // ---- iteration body, captured once per configuration --------------------
+    int per_iter = 0;
+    auto body = [&](int it) {
+        int c = 0;
+        if (cg) {
+            double* Pold = (it & 1) ? L.P1 : L.P0;
+            double* Pnew = (it & 1) ? L.P0 : L.P1;
+            c += cgp(Pold, Pnew);                               // Step 11 (prev) + A p
+            k_alpha<<<1, 512, 0, st>>>(S); ++c;                 // Step 5
+            c += proj(MODE_CG, Pnew, true);                     // Steps 6-7, ||r||, W^T r
+            k_reduce_solve<<<Bp, 128, 0, st>>>(S); ++c;         // Step 8, reduced solve
+            c += prolong(L.Y, 0);                               // Step 9: y0 = W e
+            c += smooth(L.Y, L.R, 0.0, true);                   //         y = S(A, r, y0)
+            k_beta<<<1, 512, 0, st>>>(S, 0); ++c;               // Step 10
+        } else {
+            c += prolong(L.X, 1);                               // Step 6
+            c += smooth(L.X, Fv, ctx->fconst, false);           // Step 7
+            c += proj(MODE_RESID, nullptr, true);               // Steps 2, 4
+            k_reduce_solve<<<Bp, 128, 0, st>>>(S); ++c;         // Steps 3, 5
+        }
+        return c;
+    };
+    const int chunk = o->graph_chunk;
+    char keybuf[512];
+    snprintf(keybuf, sizeof keybuf, "%p|%p|%d|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%d|%.17g",
+             workspace_dev, (void*)Fv, B, Bp, o->method, o->smoother, o->sweeps, o->max_iter, chunk,
+             o->tol, o->delta, o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist,
+             rhs_dev ? 1 : 0, n, npad, ctx->fconst);
+    const std::string key(keybuf);
+    if (!ctx->gexec || ctx->gkey != key) {
+        if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
+        cudaStream_t cap;
+        CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t keep = st;
+        st = cap;
+        per_iter = 0;
+        for (int it = 0; it < chunk; ++it) per_iter += body(it);
+        st = keep;
+        CK(cudaStreamEndCapture(cap, &graph));
+        CK(cudaGraphInstantiate(&ctx->gexec, graph, 0));
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cap);
+        ctx->gkey = key;
+        ctx->g_per_chunk = per_iter;
+    } else {
+        per_iter = ctx->g_per_chunk;
+    }
+    CKL();
+
+    // ---- replay until every query is frozen ---------------------------------
+    const int64_t max_launch = (int64_t)o->max_iter / chunk + 3;
+    volatile int* hf = ctx->h_flag;
+    hf[0] = hf[1] = 0;
+    for (int64_t l = 0;; ++l) {
+        CK(cudaGraphLaunch(ctx->gexec, st));
+        launches += per_iter;
+        CK(cudaMemcpyAsync((void*)(ctx->h_flag + (l & 1)), done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ctx->ev[l & 1], st));
+        if (l >= 1) {
+            CK(cudaEventSynchronize(ctx->ev[(l - 1) & 1]));
+            if (hf[(l - 1) & 1]) break;
+        }
+        if (l > max_launch) break;
+    }
+    CK(cudaStreamSynchronize(st));
+
+    // ---- outputs --------------------------------------------------------------
+    std::vector<int> hs(Bp), hi(Bp), hp(Bp);
+    std::vector<double> hrel(Bp), hfn(Bp), tr(Bp, NAN);
+    CK(cudaMemcpyAsync(hs.data(), L.status, Bp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hi.data(), L.its, Bp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp.data(), L.pivot, Bp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hrel.data(), L.relres, Bp * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hfn.data(), L.fnorm, Bp * 8, cudaMemcpyDeviceToHost, st));
+    if (cg) {
+        // true residual ||f - A x|| / ||f|| (not used for stopping)
+        proj(MODE_RESID, nullptr, false);
+        ++launches;
+        // reuse npad rows: the rr row of the partials is row npad
+        k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct, L.fproj);
+        ++launches;
+        CKL();
+        std::vector<double> rows((size_t)Bp * (npad + 1));
+        CK(cudaMemcpyAsync(rows.data(), L.fproj, rows.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int b = 0; b < Bp; ++b) tr[b] = std::sqrt(rows[(size_t)b * (npad + 1) + npad]) / hfn[b];
+    } else {
+        CK(cudaStreamSynchronize(st));
+        for (int b = 0; b < Bp; ++b) tr[b] = hrel[b];
+    }
+    // X: [N8][Bp] -> [B][N]
+    double* xdst = o->x_location == RBS_MEM_HOST ? L.Xout : X;
+    k_transpose_out<<<(unsigned)((g.N + 31) / 32), 256, 0, st>>>(L.X, g.N, Bp, B, xdst);
+    ++launches;
+    CKL();
+    if (o->x_location == RBS_MEM_HOST)
+        CK(cudaMemcpyAsync(X, L.Xout, (size_t)B * g.N * 8, cudaMemcpyDeviceToHost, st));
+    if (a_n && n > 0) {
+        std::vector<double> ha((size_t)Bp * npad);
+        CK(cudaMemcpyAsync(ha.data(), L.a_n, ha.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int b = 0; b < B; ++b)
+            for (int j = 0; j < n; ++j) a_n[(size_t)b * n + j] = ha[(size_t)b * npad + j];
+    }
+    if (history && L.hist)
+        CK(cudaMemcpyAsync(history, L.hist, (size_t)B * (o->max_iter + 1) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) {
+        if (iters) iters[b] = hi[b];
+        if (qstatus) qstatus[b] = hs[b];
+        if (relres) relres[b] = hrel[b];
+        if (true_relres) true_relres[b] = tr[b];
+    }
+    for (int b = 0; b < B; ++b)
+        if (hs[b] == Q_NOT_SPD) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "reduced matrix not SPD: query %d, pivot %d", b, hp[b]);
+            ctx->err = buf;
+            break;
+        }
+    ctx->launches = launches;
+    return RBS_OK;
+}
+
+}  // extern "C"
+
+#include "greedy.inc.cu"

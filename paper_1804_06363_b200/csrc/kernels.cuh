@@ -1,0 +1,684 @@
+// kernels.cuh -- sm_100a kernels of the batched RB online solver.
+//
+// Every streaming pass works on node-major batch vectors v[N8][Bp] (lane =
+// query, 8*Bp bytes per node contiguous) so that a warp's loads are fully
+// coalesced.  The W-contractions (projection W^T r, eq5;
+// prolongation W e, eq7) run on the FP64 tensor cores
+// (mma.sync m8n8k4 f64 -> SASS DMMA): tcgen05 has no f64 kind on sm_100a.
+// Reductions are deterministic two-stage sums (fixed CTA partition, fixed
+// in-CTA order, fixed stage-2 order): bitwise reproducible run to run.
+#pragma once
+#include "rbs_internal.cuh"
+
+namespace rbs {
+
+enum { MODE_CG = 0, MODE_RESID = 1, MODE_PLAIN = 2 };
+enum { Q_CONVERGED = 0, Q_MAXIT = 1, Q_NOT_SPD = 2, Q_CURVATURE = 3, Q_PRECOND = 4,
+       Q_NONFINITE = 5 };
+
+// ---------------------------------------------------------------------------
+// Projection family: per node-query value v (mode-dependent), then
+//   part[b][j][cta] = sum_{nodes of cta} W[i][j] v[i][b]   (j < npad)
+//   part[b][npad][cta] = sum v[i][b]^2
+// MODE_CG   (RBCG Steps 6-8): q = A p (recomputed from the
+//           p halo), x += alpha p, r -= alpha q, v = r (stored).
+// MODE_RESID (RBI Step 2): v = b - A x (not stored).
+// MODE_PLAIN: v = V (or the constant vconst).
+// Warp layout = DMMA B-fragment: lane l owns node 4g + (l&3), query 8bt + (l>>2).
+// ---------------------------------------------------------------------------
+struct ProjArgs {
+    Geo g;
+    int Bp, npad, nct;
+    int64_t ngroups;          // ceil(N/4)
+    const double* W;          // [N8][npad]
+    const double* theta;      // [Q][Bp]
+    const int* active;        // [Bp] or nullptr (all active)
+    const double* alpha;      // [Bp] (MODE_CG)
+    const double* P;          // MODE_CG
+    double* X;                // MODE_CG (rw), MODE_RESID (r)
+    double* R;                // MODE_CG (rw)
+    const double* V;          // MODE_RESID rhs / MODE_PLAIN input, or nullptr
+    double vconst;
+    double* part;             // [Bp][npad+1][nct]
+    const int* done;
+};
+
+template <int MODE, int DIM>
+__global__ void __launch_bounds__(kThreads) k_proj(ProjArgs a) {
+    if (a.done && *(volatile const int*)a.done) return;
+    extern __shared__ double smem[];
+    const int Bp = a.Bp, npad = a.npad, nbt = Bp >> 3, ntile = npad >> 3;
+    const int nlc = 8 / nbt;  // node lanes per CTA
+    double* s_th = smem;
+    double* s_alpha = s_th + a.g.Q * Bp;
+    double* s_red = s_alpha + Bp;
+    int* s_act = (int*)(s_red + nlc * (npad + 1) * Bp);
+    const int tid = threadIdx.x;
+    if (MODE != MODE_PLAIN)
+        for (int t = tid; t < a.g.Q * Bp; t += kThreads) s_th[t] = a.theta[t];
+    for (int t = tid; t < Bp; t += kThreads) {
+        s_alpha[t] = (MODE == MODE_CG) ? a.alpha[t] : 0.0;
+        s_act[t] = a.active ? a.active[t] : 1;
+    }
+    __syncthreads();
+
+    const int warp = tid >> 5, lane = tid & 31;
+    const int bt = warp % nbt, nl = warp / nbt;
+    const int b = bt * 8 + (lane >> 2);
+    const bool wact = nl < nlc;
+    const bool qact = s_act[b] != 0;
+    const int64_t g0 = (a.ngroups * blockIdx.x) / gridDim.x;
+    const int64_t g1 = (a.ngroups * (blockIdx.x + 1)) / gridDim.x;
+
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+    double rr = 0.0;
+    if (wact) {
+        for (int64_t gi = g0 + nl; gi < g1; gi += nlc) {
+            const int64_t i = gi * 4 + (lane & 3);
+            double v = 0.0;
+            if (i < a.g.N && qact) {
+                const int64_t e = i * Bp + b;
+                if (MODE == MODE_PLAIN) {
+                    v = a.V ? a.V[e] : a.vconst;
+                } else {
+                    int I, J, K;
+                    node_coords(a.g, (uint32_t)i, I, J, K);
+                    double k[2 * DIM], nb[2 * DIM];
+                    node_kappa<DIM>(a.g, s_th, Bp, b, I, J, K, k);
+                    if (MODE == MODE_CG) {
+                        const double pp = __ldg(a.P + e);
+                        node_nbrs<DIM>(a.g, a.P, Bp, i, b, I, J, K, nb);
+                        const double q = stencil_apply<DIM>(a.g, k, pp, nb);
+                        const double al = s_alpha[b];
+                        const double xv = fma(al, pp, a.X[e]);
+                        const double rv = fma(-al, q, a.R[e]);
+                        a.X[e] = xv;
+                        a.R[e] = rv;
+                        v = rv;
+                    } else {  // MODE_RESID
+                        const double xp = a.X[e];
+                        node_nbrs<DIM>(a.g, a.X, Bp, i, b, I, J, K, nb);
+                        const double q = stencil_apply<DIM>(a.g, k, xp, nb);
+                        v = (a.V ? a.V[e] : a.vconst) - q;
+                    }
+                }
+            }
+            rr = fma(v, v, rr);
+            const double* wrow = a.W + i * npad + (lane >> 2);
+#pragma unroll
+            for (int jt = 0; jt < 8; ++jt)
+                if (jt < ntile) dmma_8x8x4(acc[2 * jt], acc[2 * jt + 1], __ldg(wrow + jt * 8), v);
+        }
+    }
+    // rr of query b: lanes sharing l>>2 (fixed order)
+    rr += __shfl_xor_sync(0xffffffffu, rr, 1);
+    rr += __shfl_xor_sync(0xffffffffu, rr, 2);
+    if (wact) {
+        const int rowbase = nl * (npad + 1);
+#pragma unroll
+        for (int jt = 0; jt < 8; ++jt)
+            if (jt < ntile) {
+                const int j = jt * 8 + (lane >> 2);
+                const int bb = bt * 8 + 2 * (lane & 3);
+                s_red[(rowbase + j) * Bp + bb] = acc[2 * jt];
+                s_red[(rowbase + j) * Bp + bb + 1] = acc[2 * jt + 1];
+            }
+        if ((lane & 3) == 0) s_red[(rowbase + npad) * Bp + b] = rr;
+    }
+    __syncthreads();
+    const int rows = npad + 1;
+    for (int t = tid; t < rows * Bp; t += kThreads) {
+        const int j = t / Bp, bb = t - j * Bp;
+        double s = s_red[j * Bp + bb];
+        for (int l = 1; l < nlc; ++l) s += s_red[(l * rows + j) * Bp + bb];
+        a.part[((int64_t)bb * rows + j) * a.nct + blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Prolongation  Y = W E  (or Y += W E), PAPER.md:144-147 (eq7) / 165.
+// DMMA with M = 8 nodes, N = 8 queries, K = 4 basis vectors.
+// ---------------------------------------------------------------------------
+struct ProlongArgs {
+    int64_t N;
+    int Bp, npad;
+    const double* W;      // [N8][npad]
+    const double* E;      // [npad][Bp]
+    const int* active;    // [Bp]
+    double* Y;            // [N8][Bp]
+    int accumulate;
+    const int* done;
+};
+
+__global__ void __launch_bounds__(kThreads) k_prolong(ProlongArgs a) {
+    if (a.done && *(volatile const int*)a.done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const int64_t tw = (int64_t)gridDim.x * (kThreads / 32);
+    const int nbt = a.Bp >> 3, nk = a.npad >> 2;
+    const int64_t ntiles = ((a.N + 7) >> 3) * nbt;
+    for (int64_t idx = gw; idx < ntiles; idx += tw) {
+        const int64_t nt = idx / nbt;
+        const int bt = (int)(idx - nt * nbt);
+        const int64_t i0 = nt * 8;
+        double d0 = 0.0, d1 = 0.0;
+        const double* wrow = a.W + (i0 + (lane >> 2)) * a.npad + (lane & 3);
+        const double* ecol = a.E + (lane & 3) * a.Bp + bt * 8 + (lane >> 2);
+#pragma unroll 4
+        for (int kk = 0; kk < nk; ++kk)
+            dmma_8x8x4(d0, d1, __ldg(wrow + kk * 4), __ldg(ecol + (int64_t)kk * 4 * a.Bp));
+        const int64_t i = i0 + (lane >> 2);
+        const int b = bt * 8 + 2 * (lane & 3);
+        if (i < a.N) {
+            double* y = a.Y + i * a.Bp + b;
+            if (a.active[b]) y[0] = a.accumulate ? y[0] + d0 : d0;
+            if (a.active[b + 1]) y[1] = a.accumulate ? y[1] + d1 : d1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Red-black Gauss-Seidel half-sweep of `color` (AMB-5; eq8)
+// on A y = rhs, in place.  color < 0: no update.  LAST: also partials of
+// y^T rhs and y^T y per query (RBCG Step 10 / AMB-11).
+// Flat thread-per-element mapping (e = i*Bp + b), Bp a power of two.
+// ---------------------------------------------------------------------------
+struct GSArgs {
+    Geo g;
+    int Bp, lgB;
+    int64_t NB;               // N*Bp
+    const double* theta;      // [Q][Bp]
+    const int* active;
+    double* Y;
+    const double* Rhs;        // or nullptr -> rconst
+    double rconst;
+    int color;
+    double* part;             // [Bp][2][nctf]
+    int nctf;
+    const int* done;
+};
+
+template <int DIM, bool LAST>
+__global__ void __launch_bounds__(kThreads) k_gs(GSArgs a) {
+    if (a.done && *(volatile const int*)a.done) return;
+    extern __shared__ double smem[];
+    double* s_th = smem;
+    int* s_act = (int*)(s_th + a.g.Q * a.Bp);
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kThreads) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kThreads) s_act[t] = a.active[t];
+    __syncthreads();
+    double yr = 0.0, yy = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    const int b = (int)((blockIdx.x * (int64_t)kThreads + threadIdx.x) & (a.Bp - 1));
+    const bool act = s_act[b] != 0;
+    if (act) {
+        for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < a.NB; e += stride) {
+            const int64_t i = e >> a.lgB;
+            int I, J, K;
+            node_coords(a.g, (uint32_t)i, I, J, K);
+            const int par = (I + J + (DIM == 3 ? K : 0)) & 1;
+            const double rhs = a.Rhs ? a.Rhs[e] : a.rconst;
+            double y;
+            if (par == a.color) {
+                double k[2 * DIM], nb[2 * DIM];
+                node_kappa<DIM>(a.g, s_th, a.Bp, b, I, J, K, k);
+                node_nbrs<DIM>(a.g, a.Y, a.Bp, i, b, I, J, K, nb);
+                y = gs_value<DIM>(a.g, k, rhs, nb);
+                a.Y[e] = y;
+            } else if (LAST) {
+                y = a.Y[e];
+            }
+            if (LAST) {
+                yr = fma(y, rhs, yr);
+                yy = fma(y, y, yy);
+            }
+        }
+    }
+    if (LAST) {
+        __shared__ double s_yr[kThreads], s_yy[kThreads];
+        s_yr[threadIdx.x] = yr;
+        s_yy[threadIdx.x] = yy;
+        __syncthreads();
+        if (threadIdx.x < a.Bp) {
+            double sr = 0.0, sy = 0.0;
+            for (int t = threadIdx.x; t < kThreads; t += a.Bp) {
+                sr += s_yr[t];
+                sy += s_yy[t];
+            }
+            a.part[((int64_t)threadIdx.x * 2 + 0) * a.nctf + blockIdx.x] = sr;
+            a.part[((int64_t)threadIdx.x * 2 + 1) * a.nctf + blockIdx.x] = sy;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// RBCG Step 11 + Step 5 numerator:
+//   p_new = y + beta p_old (recomputed on the halo), q = A p_new,
+//   part[b][0][cta] = sum p_new q.   p is double-buffered.
+// ---------------------------------------------------------------------------
+struct CGPArgs {
+    Geo g;
+    int Bp, lgB;
+    int64_t NB;
+    const double* theta;
+    const int* active;
+    const double* beta;
+    const double* Y;
+    const double* Pold;
+    double* Pnew;
+    double* part;             // [Bp][2][nctf] (slot 0)
+    int nctf;
+    const int* done;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) k_cgp(CGPArgs a) {
+    if (a.done && *(volatile const int*)a.done) return;
+    extern __shared__ double smem[];
+    double* s_th = smem;
+    int* s_act = (int*)(s_th + a.g.Q * a.Bp);
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kThreads) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kThreads) s_act[t] = a.active[t];
+    __syncthreads();
+    double sig = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    const int b = (int)((blockIdx.x * (int64_t)kThreads + threadIdx.x) & (a.Bp - 1));
+    if (s_act[b]) {
+        const double bet = a.beta[b];
+        const int64_t sy = (int64_t)a.g.m * a.Bp, sz = sy * a.g.m;
+        for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < a.NB; e += stride) {
+            const int64_t i = e >> a.lgB;
+            int I, J, K;
+            node_coords(a.g, (uint32_t)i, I, J, K);
+            double k[2 * DIM], nb[2 * DIM];
+            node_kappa<DIM>(a.g, s_th, a.Bp, b, I, J, K, k);
+            const double pp = fma(bet, __ldg(a.Pold + e), __ldg(a.Y + e));
+#define PNB(off) fma(bet, __ldg(a.Pold + e + (off)), __ldg(a.Y + e + (off)))
+            nb[0] = I > 1 ? PNB(-a.Bp) : 0.0;
+            nb[1] = I < a.g.m ? PNB(a.Bp) : 0.0;
+            nb[2] = J > 1 ? PNB(-sy) : 0.0;
+            nb[3] = J < a.g.m ? PNB(sy) : 0.0;
+            if (DIM == 3) {
+                nb[4] = K > 1 ? PNB(-sz) : 0.0;
+                nb[5] = K < a.g.m ? PNB(sz) : 0.0;
+            }
+#undef PNB
+            const double q = stencil_apply<DIM>(a.g, k, pp, nb);
+            a.Pnew[e] = pp;
+            sig = fma(pp, q, sig);
+        }
+    }
+    __shared__ double s_sig[kThreads];
+    s_sig[threadIdx.x] = sig;
+    __syncthreads();
+    if (threadIdx.x < a.Bp) {
+        double s = 0.0;
+        for (int t = threadIdx.x; t < kThreads; t += a.Bp) s += s_sig[t];
+        a.part[((int64_t)threadIdx.x * 2 + 0) * a.nctf + blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-solve state shared by the bookkeeping kernels.
+// ---------------------------------------------------------------------------
+struct SolveState {
+    int B, Bp, n, npad, nct, nctf, maxit, method;
+    double tol, delta;
+    const double* ANq;        // [Q][npad][npad]
+    int Q;
+    double* theta;            // [Q][Bp]
+    double* fproj;            // [Bp][npad+1]: f_n and ||f||^2
+    double* L;                // [Bp][npad][npad]
+    double* E;                // [npad][Bp]
+    double* a_n;              // [Bp][npad]
+    double* partP;            // [Bp][npad+1][nct]
+    double* partF;            // [Bp][2][nctf]
+    double *alpha, *beta, *rho, *rr, *fnorm, *relres;
+    int *active, *status, *its, *pivot;
+    int* kcount;
+    int* done;
+    unsigned* ticket;
+    double* hist;             // [Bp][maxit+1] or nullptr
+};
+
+// deterministic warp sum of part[row][0..cnt)
+__device__ __forceinline__ double warp_sum_row(const double* p, int cnt, int lane) {
+    double s = 0.0;
+    for (int c = lane; c < cnt; c += 32) s += p[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// triangular solves L L^T e = rhs by one warp; lane owns rows lane, lane+32.
+__device__ void warp_chol_solve(const double* L, int ld, int n, double* z0, double* z1, int lane) {
+    for (int i = 0; i < n; ++i) {
+        const int own = i & 31, slot = i >> 5;
+        const double mine = slot ? *z1 : *z0;
+        const double zi = __shfl_sync(0xffffffffu, mine, own) / L[i * ld + i];
+        if (lane == own) { if (slot) *z1 = zi; else *z0 = zi; }
+        if (lane > i && lane < n) *z0 -= L[lane * ld + i] * zi;
+        if (lane + 32 > i && lane + 32 < n) *z1 -= L[(lane + 32) * ld + i] * zi;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        const int own = i & 31, slot = i >> 5;
+        const double mine = slot ? *z1 : *z0;
+        const double ei = __shfl_sync(0xffffffffu, mine, own) / L[i * ld + i];
+        if (lane == own) { if (slot) *z1 = ei; else *z0 = ei; }
+        if (lane < i) *z0 -= L[i * ld + lane] * ei;
+        if (lane + 32 < i) *z1 -= L[i * ld + lane + 32] * ei;
+    }
+}
+
+__device__ __forceinline__ void last_block_update(SolveState& s, bool bump_k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(s.ticket, 1u);
+        if (t == gridDim.x - 1) {
+            __threadfence();
+            int any = 0;
+            for (int b = 0; b < s.Bp; ++b) any |= ((volatile int*)s.active)[b];
+            *(volatile int*)s.done = any ? 0 : 1;
+            if (bump_k) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
+            *(volatile unsigned*)s.ticket = 0u;
+            __threadfence();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2 of W^T r / ||r||^2 + stop test + reduced solve (RBCG Steps 7-9,
+// RBI Steps 2-5).  One CTA per query.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_reduce_solve(SolveState s) {
+    if (*(volatile const int*)s.done) return;
+    __shared__ double s_rn[kMaxN + 1];
+    __shared__ int s_go;
+    const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows = s.npad + 1;
+    const bool act = s.active[b] != 0;
+    if (act) {
+        for (int r = warp; r <= s.n; r += 4) {
+            const int j = r < s.n ? r : s.npad;
+            const double v = warp_sum_row(s.partP + ((int64_t)b * rows + j) * s.nct, s.nct, lane);
+            if (lane == 0) s_rn[j] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const double rr2 = s_rn[s.npad];
+            const double h = sqrt(rr2) / s.fnorm[b];
+            const int it = *(volatile int*)s.kcount + 1;
+            if (s.hist) s.hist[(int64_t)b * (s.maxit + 1) + it] = h;
+            s.its[b] = it;
+            s.relres[b] = h;
+            s.rr[b] = rr2;
+            int go = 1;
+            if (!isfinite(h)) { s.status[b] = Q_NONFINITE; go = 0; }
+            else if (h < s.tol) { s.status[b] = Q_CONVERGED; go = 0; }
+            else if (s.method == 0 && it >= s.maxit) { s.status[b] = Q_MAXIT; go = 0; }
+            if (!go) s.active[b] = 0;
+            s_go = go;
+        }
+        __syncthreads();
+        if (s_go && s.n > 0 && warp == 0) {
+            const double* L = s.L + (int64_t)b * s.npad * s.npad;
+            double z0 = lane < s.n ? s_rn[lane] : 0.0;
+            double z1 = lane + 32 < s.n ? s_rn[lane + 32] : 0.0;
+            warp_chol_solve(L, s.npad, s.n, &z0, &z1, lane);
+            if (lane < s.n) s.E[lane * s.Bp + b] = z0;
+            if (lane + 32 < s.n) s.E[(lane + 32) * s.Bp + b] = z1;
+        }
+    }
+    last_block_update(s, s.method == 0);
+}
+
+// generic stage 2: out[b][j] = sum_c part[b][j][c], j < rows (one CTA per b)
+__global__ void __launch_bounds__(128) k_reduce_rows(const double* part, int rows, int nct,
+                                                     double* out) {
+    const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < rows; j += 4) {
+        const double v = warp_sum_row(part + ((int64_t)b * rows + j) * nct, nct, lane);
+        if (lane == 0) out[(int64_t)b * rows + j] = v;
+    }
+}
+
+// 1-CTA sum of partF slot `slot` for every query; result in s_out[b]
+__device__ void block_sum_slot(const SolveState& s, int slot, double* s_buf, double* s_out) {
+    const int gsz = blockDim.x / s.Bp;
+    const int b = threadIdx.x / gsz, t = threadIdx.x - b * gsz;
+    double v = 0.0;
+    if (b < s.Bp)
+        for (int c = t; c < s.nctf; c += gsz) v += s.partF[((int64_t)b * 2 + slot) * s.nctf + c];
+    s_buf[threadIdx.x] = v;
+    __syncthreads();
+    if (t == 0 && b < s.Bp) {
+        double a = 0.0;
+        for (int u = 0; u < gsz; ++u) a += s_buf[b * gsz + u];
+        s_out[b] = a;
+    }
+    __syncthreads();
+}
+
+// RBCG Step 5: alpha = rho / p^T A p, MAXIT / CURVATURE checks.
+__global__ void __launch_bounds__(512) k_alpha(SolveState s) {
+    if (*(volatile const int*)s.done) return;
+    __shared__ double s_buf[512], s_sig[kMaxBatch];
+    block_sum_slot(s, 0, s_buf, s_sig);
+    const int k = *(volatile int*)s.kcount;
+    if (threadIdx.x < s.Bp) {
+        const int b = threadIdx.x;
+        double al = 0.0;
+        if (s.active[b]) {
+            const double sig = s_sig[b];
+            if (k >= s.maxit) { s.status[b] = Q_MAXIT; s.its[b] = k; s.active[b] = 0; }
+            else if (!(sig > 0.0)) {
+                s.status[b] = isfinite(sig) ? Q_CURVATURE : Q_NONFINITE;
+                s.its[b] = k;
+                s.active[b] = 0;
+            } else al = s.rho[b] / sig;
+        }
+        s.alpha[b] = al;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int any = 0;
+        for (int b = 0; b < s.Bp; ++b) any |= s.active[b];
+        *s.done = any ? 0 : 1;
+    }
+}
+
+// RBCG Step 10: beta = y^T r (new) / y^T r (old); PRECOND check.
+__global__ void __launch_bounds__(512) k_beta(SolveState s, int init) {
+    if (*(volatile const int*)s.done) return;
+    __shared__ double s_buf[512], s_yr[kMaxBatch], s_yy[kMaxBatch];
+    block_sum_slot(s, 0, s_buf, s_yr);
+    block_sum_slot(s, 1, s_buf, s_yy);
+    if (threadIdx.x < s.Bp) {
+        const int b = threadIdx.x;
+        if (s.active[b]) {
+            const double yr = s_yr[b], yy = s_yy[b];
+            if (!(yr > s.delta * sqrt(yy) * sqrt(s.rr[b]))) {
+                s.status[b] = isfinite(yr) ? Q_PRECOND : Q_NONFINITE;
+                s.active[b] = 0;
+                s.beta[b] = 0.0;
+            } else {
+                s.beta[b] = init ? 0.0 : yr / s.rho[b];
+                s.rho[b] = yr;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int any = 0;
+        for (int b = 0; b < s.Bp; ++b) any |= s.active[b];
+        *s.done = any ? 0 : 1;
+        if (!init) *s.kcount = *s.kcount + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Once per query (eq12b, 69): A_n(theta) = sum_q theta_q
+// A_{n,q}; right-looking Cholesky in shared memory; a_n = A_n^{-1} f_n
+// (first RB correction, PAPER.md:171 / AMB-12); state init.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_setup_reduced(SolveState s, int rbi) {
+    __shared__ double sA[kMaxN * kMaxN];
+    __shared__ int s_fail;
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int n = s.n, ld = s.npad;
+    if (b >= s.B) {
+        if (tid == 0) { s.active[b] = 0; s.status[b] = Q_MAXIT; s.its[b] = 0; s.alpha[b] = 0.0;
+                        s.beta[b] = 0.0; s.rho[b] = 0.0; s.fnorm[b] = 1.0; s.rr[b] = 0.0; }
+        return;
+    }
+    for (int t = tid; t < n * n; t += blockDim.x) {
+        const int i = t / n, j = t - i * n;
+        double v = 0.0;
+        for (int q = 0; q < s.Q; ++q) v = fma(s.theta[q * s.Bp + b], s.ANq[((int64_t)q * ld + i) * ld + j], v);
+        sA[i * ld + j] = v;
+    }
+    if (tid == 0) s_fail = -1;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        if (tid == 0) {
+            const double d = sA[k * ld + k];
+            if (!(d > 0.0)) s_fail = k;
+            else sA[k * ld + k] = sqrt(d);
+        }
+        __syncthreads();
+        if (s_fail >= 0) break;
+        const double dk = sA[k * ld + k];
+        for (int i = k + 1 + tid; i < n; i += blockDim.x) sA[i * ld + k] /= dk;
+        __syncthreads();
+        const int m = n - k - 1;  // trailing (i,j), k < j <= i < n
+        for (int t = tid; t < m * m; t += blockDim.x) {
+            const int i = k + 1 + t / m, j = k + 1 + t % m;
+            if (j <= i) sA[i * ld + j] -= sA[i * ld + k] * sA[j * ld + k];
+        }
+        __syncthreads();
+    }
+    double* L = s.L + (int64_t)b * ld * ld;
+    for (int t = tid; t < n * ld; t += blockDim.x) {
+        const int i = t / ld, j = t - i * ld;
+        L[t] = (j <= i && j < n) ? sA[i * ld + j] : 0.0;
+    }
+    const double ff = s.fproj[(int64_t)b * (ld + 1) + ld];
+    const double fnorm = sqrt(ff);
+    if (tid == 0) {
+        s.fnorm[b] = fnorm > 0.0 ? fnorm : 1.0;
+        s.rr[b] = ff;
+        s.alpha[b] = 0.0;
+        s.beta[b] = 0.0;
+        s.rho[b] = 0.0;
+        s.its[b] = 0;
+        s.relres[b] = fnorm > 0.0 ? 1.0 : 0.0;
+        s.pivot[b] = s_fail;
+        if (s.hist) s.hist[(int64_t)b * (s.maxit + 1)] = fnorm > 0.0 ? 1.0 : 0.0;
+        int act = 1, st = Q_MAXIT;
+        if (s_fail >= 0) { act = 0; st = Q_NOT_SPD; }
+        else if (!(fnorm > 0.0)) { act = 0; st = Q_CONVERGED; }
+        else if (!isfinite(fnorm)) { act = 0; st = Q_NONFINITE; }
+        else if (rbi && 1.0 < s.tol) { act = 0; st = Q_CONVERGED; }
+        else if (rbi && s.maxit <= 0) { act = 0; st = Q_MAXIT; }
+        s.active[b] = act;
+        s.status[b] = st;
+    }
+    __syncthreads();
+    if (s_fail < 0 && n > 0 && tid < 32) {
+        // sA holds the factor in its lower triangle (only that part is read)
+        const double* fn = s.fproj + (int64_t)b * (ld + 1);
+        double z0 = tid < n ? fn[tid] : 0.0, z1 = tid + 32 < n ? fn[tid + 32] : 0.0;
+        warp_chol_solve(sA, ld, n, &z0, &z1, tid);
+        if (tid < n) { s.E[tid * s.Bp + b] = z0; s.a_n[(int64_t)b * ld + tid] = z0; }
+        if (tid + 32 < n) { s.E[(tid + 32) * s.Bp + b] = z1; s.a_n[(int64_t)b * ld + tid + 32] = z1; }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// layout / init helpers
+// ---------------------------------------------------------------------------
+// W column-major (ldw) -> node-major [N8][npad], zero padded
+__global__ void k_pack_W(const double* __restrict__ W, int64_t ldw, int64_t N, int64_t N8, int n,
+                         int npad, double* __restrict__ Wi) {
+    const int64_t tot = N8 * npad;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / npad;
+        const int j = (int)(t - i * npad);
+        Wi[t] = (i < N && j < n) ? W[(int64_t)j * ldw + i] : 0.0;
+    }
+}
+
+// node-major [N8][npad] -> column-major N x n
+__global__ void k_unpack_W(const double* __restrict__ Wi, int64_t N, int n, int npad,
+                           double* __restrict__ W) {
+    const int64_t tot = N * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / N, i = t - j * N;
+        W[t] = Wi[i * npad + j];
+    }
+}
+
+// v[N8][Bp] <- value (or from src [B][N] query-major when src != nullptr)
+__global__ void k_fill_batch(double* __restrict__ v, int64_t N, int64_t N8, int Bp, int B,
+                             const double* __restrict__ src, double value) {
+    const int64_t tot = N8 * Bp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / Bp;
+        const int b = (int)(t - i * Bp);
+        double x = 0.0;
+        if (i < N && b < B) x = src ? src[(int64_t)b * N + i] : value;
+        v[t] = x;
+    }
+}
+
+// out[B][N] (query-major) <- v[N8][Bp]; tiled transpose through shared memory
+__global__ void k_transpose_out(const double* __restrict__ v, int64_t N, int Bp, int B,
+                                double* __restrict__ out) {
+    __shared__ double tile[32][kMaxBatch + 1];
+    const int64_t i0 = (int64_t)blockIdx.x * 32;
+    for (int t = threadIdx.x; t < 32 * Bp; t += blockDim.x) {
+        const int r = t / Bp, b = t - r * Bp;
+        tile[r][b] = (i0 + r < N) ? v[(i0 + r) * Bp + b] : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 32 * B; t += blockDim.x) {
+        const int b = t >> 5, r = t & 31;
+        if (i0 + r < N) out[(int64_t)b * N + i0 + r] = tile[r][b];
+    }
+}
+
+// offline: Z[i][j] = (A_q W[:,j])_i for the columns of the packed basis
+// offline: Z[i][jj] = (A_q W[:, j0+jj])_i, jj < 8, for the packed basis
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) k_apply_Aq(Geo g, int q, const double* __restrict__ Wi,
+                                                       int npad, int j0, double* __restrict__ Z) {
+    __shared__ double s_th[64];
+    for (int t = threadIdx.x; t < g.Q; t += blockDim.x) s_th[t] = (t == q) ? 1.0 : 0.0;
+    __syncthreads();
+    const int64_t tot = g.N * 8;
+    for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < tot;
+         e += (int64_t)gridDim.x * kThreads) {
+        const int64_t i = e >> 3;
+        const int j = j0 + (int)(e & 7);
+        int I, J, K;
+        node_coords(g, (uint32_t)i, I, J, K);
+        double k[2 * DIM], nb[2 * DIM];
+        node_kappa<DIM>(g, s_th, 1, 0, I, J, K, k);
+        node_nbrs<DIM>(g, Wi, npad, i, j, I, J, K, nb);
+        Z[e] = stencil_apply<DIM>(g, k, Wi[i * npad + j], nb);
+    }
+}
+
+__global__ void k_update_done(const int* active, int Bp, int* done) {
+    int any = 0;
+    for (int b = 0; b < Bp; ++b) any |= active[b];
+    *done = any ? 0 : 1;
+}
+
+}  // namespace rbs

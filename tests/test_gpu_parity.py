@@ -1,0 +1,267 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Same seeded inputs (synth/), same basis (built by the oracle).  Criteria
+(BASELINE.json north_star):
+  iterations |d its| <= 1, ||x_gpu - x_or|| / ||x_or|| <= 1e-9,
+  reduced coefficients a_n to relative 1e-10, residual histories to 1e-6
+  relative (+1e-13 absolute rounding floor) at every common k.
+"""
+import numpy as np
+import pytest
+
+from synth import CONFIGS, query_set, train_set
+
+pytestmark = pytest.mark.gpu
+
+X_TOL, A_TOL, H_TOL, H_ABS = 1e-9, 1e-10, 1e-6, 1e-13
+
+
+@pytest.fixture(scope="module")
+def rbs():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1804_06363_b200 import build
+    build.build()
+    import paper_1804_06363_b200 as r
+    return r
+
+
+_BASES = {}
+
+
+def oracle_basis(orc, dim, m, blocks, n, n_train, seed):
+    key = (dim, m, tuple(blocks), n, n_train, seed)
+    if key not in _BASES:
+        g = orc.Grid(dim, m, blocks)
+        rng = np.random.default_rng(seed)
+        tr = 0.1 * 100 ** rng.random((n_train, g.Q))
+        _BASES[key] = (g, g.greedy(tr, n))
+    return _BASES[key]
+
+
+def c1_basis(orc):
+    c = CONFIGS["c1"]
+    key = ("c1",)
+    if key not in _BASES:
+        g = orc.Grid(c.dim, c.m, c.blocks)
+        _BASES[key] = (g, g.greedy(train_set(c), c.n))
+    return _BASES[key]
+
+
+def compare(gout, g_or, W, ANq, fn, mus, method, check_hist=True, **kw):
+    """run the oracle on each mu and compare with the GPU result dict."""
+    X = gout["X"].cpu().numpy()
+    worst = dict(x=0.0, a=0.0, h=0.0, dits=0)
+    for b, mu in enumerate(mus):
+        solve = g_or.rbcg if method == "rbcg" else g_or.rbi
+        ref = solve(W, ANq, fn, mu, **kw)
+        assert gout["status"][b] == ref["status"], (b, gout["status"][b], ref["status"])
+        d = abs(int(gout["its"][b]) - ref["its"])
+        assert d <= 1, (b, gout["its"][b], ref["its"])
+        xr = ref["x"]
+        ex = np.linalg.norm(X[b] - xr) / max(np.linalg.norm(xr), 1e-300)
+        assert ex <= X_TOL, (b, ex)
+        if W is not None and W.shape[1] > 0 and gout.get("a_n") is not None:
+            ea = np.abs(gout["a_n"][b] - ref["a_n"]).max() / np.abs(ref["a_n"]).max()
+            assert ea <= A_TOL, (b, ea)
+            worst["a"] = max(worst["a"], ea)
+        if check_hist and "history" in gout:
+            hg, hr = gout["history"][b], ref["hist"]
+            k = min(len(hg), len(hr))
+            dh = np.abs(hg[:k] - hr[:k])
+            # relative 1e-6, plus an absolute floor: a recomputed residual b - A x
+            # near 1e-10 carries rounding ~ eps ||A|| ||x|| / ||b||
+            assert np.all(dh <= H_TOL * np.abs(hr[:k]) + H_ABS), (b, np.max(dh - H_TOL * np.abs(hr[:k])))
+            eh = np.max(dh / np.maximum(np.abs(hr[:k]), 1e-300))
+            worst["h"] = max(worst["h"], eh)
+        worst["x"] = max(worst["x"], ex)
+        worst["dits"] = max(worst["dits"], d)
+    return worst
+
+
+# ----------------------------------------------------------------------------- offline blocks
+@pytest.mark.parametrize("dim,m,blocks,n", [(2, 37, (3, 3), 12), (3, 11, (2, 2, 2), 10),
+                                            (2, 63, (2, 2), 16)])
+def test_offline_blocks_on_device(orc, rbs, dim, m, blocks, n):
+    g, res = oracle_basis(orc, dim, m, blocks, n, 30, 1)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"])  # blocks computed on the GPU
+    A, f = s.offline_blocks()
+    assert np.abs(A - res["ANq"]).max() <= 1e-12 * np.abs(res["ANq"]).max()
+    assert np.abs(f - res["fn"]).max() <= 1e-12 * np.abs(res["fn"]).max()
+    for q in range(g.Q):
+        assert np.array_equal(A[q], A[q].T)
+
+
+# ----------------------------------------------------------------------------- c1 in full
+@pytest.mark.parametrize("method", ["rbcg", "rbi"])
+def test_c1_all_queries(orc, rbs, method):
+    c = CONFIGS["c1"]
+    g, res = c1_basis(orc)
+    s = rbs.Solver(c.dim, c.m, c.blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = query_set(c)
+    kw = dict(method=rbs.RBS_RBCG if method == "rbcg" else rbs.RBS_RBI,
+              max_iter=20000 if method == "rbcg" else 500000, record_history=1)
+    out = s.solve_batch(mus, **kw)
+    assert all(st == "CONVERGED" for st in out["status"])
+    assert np.all(out["true_relres"] < 1e-10 * 1.5)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, method,
+            max_iter=kw["max_iter"])
+
+
+@pytest.mark.parametrize("smoother,sweeps", [(1, 1), (0, 2), (1, 3)])
+def test_c1_smoother_variants(orc, rbs, smoother, sweeps):
+    c = CONFIGS["c1"]
+    g, res = c1_basis(orc)
+    s = rbs.Solver(c.dim, c.m, c.blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = query_set(c)[:4]
+    out = s.solve_batch(mus, smoother=smoother, sweeps=sweeps, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg", smoother=smoother,
+            sweeps=sweeps)
+
+
+# ----------------------------------------------------------------------------- ragged shapes
+@pytest.mark.parametrize("dim,m,blocks,n,B", [
+    (2, 37, (3, 3), 12, 5),      # ragged N (1369 = 4*342+1), npad 16, Bp 8
+    (2, 50, (2, 3), 9, 13),      # rectangular block layout, Bp 16
+    (3, 11, (2, 2, 2), 10, 3),   # 3D, N = 1331
+    (3, 9, (2, 2, 2), 8, 33),    # 3D, B = 33 -> Bp 64
+])
+@pytest.mark.parametrize("method", ["rbcg", "rbi"])
+def test_ragged_parity(orc, rbs, dim, m, blocks, n, B, method):
+    g, res = oracle_basis(orc, dim, m, blocks, n, 30, 2)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    rng = np.random.default_rng(100 + B)
+    mus = 0.1 * 100 ** rng.random((B, g.Q))
+    mi = 20000 if method == "rbcg" else 500000
+    out = s.solve_batch(mus, method=rbs.RBS_RBCG if method == "rbcg" else rbs.RBS_RBI,
+                        max_iter=mi, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, method, max_iter=mi)
+
+
+def test_fixed_iteration_mode(orc, rbs):
+    """tol = 0, max_iter = K: x_K parity separates drift from threshold flips."""
+    g, res = oracle_basis(orc, 2, 45, (3, 3), 10, 30, 3)
+    s = rbs.Solver(2, 45, (3, 3)).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = 0.1 * 100 ** np.random.default_rng(4).random((8, 9))
+    for method, K in (("rbcg", 25), ("rbi", 40)):
+        out = s.solve_batch(mus, method=rbs.RBS_RBCG if method == "rbcg" else rbs.RBS_RBI,
+                            tol=0.0, max_iter=K, record_history=1)
+        assert all(st == "MAXIT" for st in out["status"]) and np.all(out["its"] == K)
+        compare(out, g, res["W"], res["ANq"], res["fn"], mus, method, tol=0.0, max_iter=K)
+
+
+# ----------------------------------------------------------------------------- paper lemmas on GPU
+def test_lemma1_one_iteration(orc, rbs):
+    import torch
+    g, res = oracle_basis(orc, 2, 40, (2, 2), 8, 30, 5)
+    W = res["W"]
+    s = rbs.Solver(2, 40, (2, 2)).load_basis(W, res["ANq"], res["fn"])
+    rng = np.random.default_rng(6)
+    mus = 0.1 * 100 ** rng.random((4, 4))
+    C = rng.standard_normal((4, W.shape[1]))
+    rhs = np.stack([g.apply_A(mus[b], W @ C[b]) for b in range(4)])
+    rt = torch.tensor(rhs, device="cuda")
+    for method in (rbs.RBS_RBCG, rbs.RBS_RBI):
+        out = s.solve_batch(mus, rhs=rt, method=method)
+        assert np.all(out["its"] == 1) and all(st == "CONVERGED" for st in out["status"])
+        X = out["X"].cpu().numpy()
+        for b in range(4):
+            assert np.linalg.norm(X[b] - W @ C[b]) <= 1e-10 * np.linalg.norm(W @ C[b])
+            assert np.abs(out["a_n"][b] - C[b]).max() <= 1e-10 * np.abs(C[b]).max()
+
+
+def test_lemma2_no_smoother(orc, rbs):
+    g, res = oracle_basis(orc, 2, 40, (2, 2), 8, 30, 5)
+    s = rbs.Solver(2, 40, (2, 2)).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = 0.1 * 100 ** np.random.default_rng(7).random((3, 4))
+    out = s.solve_batch(mus, method=rbs.RBS_RBI, sweeps=0, max_iter=5)
+    X = out["X"].cpu().numpy()
+    for b in range(3):
+        xhat = res["W"] @ orc.rb_solve(res["ANq"], res["fn"], mus[b])[0]
+        assert out["status"][b] == "MAXIT"
+        assert np.linalg.norm(X[b] - xhat) <= 1e-12 * np.linalg.norm(xhat)
+    out = s.solve_batch(mus, method=rbs.RBS_RBCG, sweeps=0)
+    assert all(st == "PRECOND" for st in out["status"]) and np.all(out["its"] == 1)
+
+
+def test_empty_basis_is_sgs_pcg(orc, rbs):
+    g = orc.Grid(2, 33, (3, 3))
+    s = rbs.Solver(2, 33, (3, 3)).load_basis(np.zeros((g.N, 0)))
+    mus = 0.1 * 100 ** np.random.default_rng(8).random((4, 9))
+    out = s.solve_batch(mus, record_history=1, want_a_n=False)
+    compare(out, g, None, None, None, mus, "rbcg")
+
+
+def test_not_spd_query_does_not_fail_batch(orc, rbs):
+    g, res = oracle_basis(orc, 2, 30, (2, 2), 6, 30, 9)
+    s = rbs.Solver(2, 30, (2, 2)).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = np.array([[1.0, 2.0, 3.0, 4.0], [-5.0, -1.0, -2.0, -3.0], [0.5, 0.5, 2.0, 1.0]])
+    out = s.solve_batch(mus)
+    assert out["status"][1] == "REDUCED_NOT_SPD"
+    assert out["status"][0] == "CONVERGED" and out["status"][2] == "CONVERGED"
+    compare(dict(out, X=out["X"][[0, 2]], status=[out["status"][0], out["status"][2]],
+                 its=out["its"][[0, 2]], a_n=out["a_n"][[0, 2]]),
+            g, res["W"], res["ANq"], res["fn"], mus[[0, 2]], "rbcg", check_hist=False)
+
+
+# ----------------------------------------------------------------------------- API behaviour
+def test_host_output_determinism_and_launches(orc, rbs):
+    c = CONFIGS["c1"]
+    g, res = c1_basis(orc)
+    s = rbs.Solver(c.dim, c.m, c.blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = query_set(c)
+    a = s.solve_batch(mus)
+    b = s.solve_batch(mus)
+    h = s.solve_batch(mus, x_location=rbs.RBS_MEM_HOST)
+    assert a["launches"] > 0
+    assert np.array_equal(a["X"].cpu().numpy(), b["X"].cpu().numpy())  # bitwise run to run
+    assert np.array_equal(a["X"].cpu().numpy(), h["X"].numpy())
+    assert np.array_equal(a["its"], h["its"])
+
+
+def test_errors_are_status_codes(rbs):
+    import ctypes as C
+    s = rbs.Solver(2, 20, (2, 2))
+    with pytest.raises(rbs.RbsError, match="E_STATE"):
+        s.solve_batch(np.ones((2, 4)))  # no basis yet
+    with pytest.raises(rbs.RbsError, match="E_DIM"):
+        rbs.rbs_set_operator_blocks(s.ctx, 4, 10, (2, 2))
+    s.load_basis(np.linalg.qr(np.random.default_rng(0).standard_normal((400, 3)))[0])
+    with pytest.raises(rbs.RbsError, match="E_DIM"):
+        s.solve_batch(np.ones((65, 4)))
+    assert rbs.lib().rbs_last_error(s.ctx).decode()
+
+
+# ----------------------------------------------------------------------------- GPU greedy
+def test_gpu_greedy_matches_oracle_c1(orc, rbs):
+    c = CONFIGS["c1"]
+    g, res = c1_basis(orc)
+    s = rbs.Solver(c.dim, c.m, c.blocks)
+    gr = s.build_greedy(train_set(c), c.n)
+    assert gr["n"] == res["n"] and gr["n_rejected"] == res["n_rejected"]
+    sel_g, sel_o = list(gr["selected"]), list(res["selected"])
+    if sel_g != sel_o:  # allowed only at a genuine near-tie of the oracle indicator
+        k = next(i for i in range(len(sel_o)) if sel_g[i] != sel_o[i])
+        assert abs(gr["indicator"][k - 1] - res["indicator"][k - 1]) <= 1e-10 * res["indicator"][k - 1]
+    else:
+        Wg = gr["W"].cpu().numpy()
+        sv = np.linalg.svd(Wg.T @ res["W"], compute_uv=False)
+        assert sv.min() >= 1 - 1e-8  # principal angles <= ~1e-4 rad (cos >= 1-1e-8)
+        assert np.abs(gr["indicator"] - res["indicator"]).max() <= 1e-8 * np.abs(res["indicator"]).max()
+        assert np.all(np.abs(gr["snap_iters"] - res["snap_iters"]) <= 1)
+
+
+def test_gpu_greedy_basis_solves(orc, rbs):
+    g, res = oracle_basis(orc, 3, 9, (2, 2, 2), 8, 25, 11)
+    s = rbs.Solver(3, 9, (2, 2, 2))
+    rng = np.random.default_rng(11)
+    tr = 0.1 * 100 ** rng.random((25, 8))
+    gr = s.build_greedy(tr, 8)
+    Wg = gr["W"].cpu().numpy()
+    assert np.abs(Wg.T @ Wg - np.eye(gr["n"])).max() < 1e-12
+    assert list(gr["selected"]) == list(res["selected"])
+    mus = 0.1 * 100 ** rng.random((4, 8))
+    out = s.solve_batch(mus, record_history=1)
+    # the oracle solves with the oracle's own basis; same subspace => same iterates
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg")
