@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark: parameter queries solved per second to relative residual 1e-10.
+
+Workload (BASELINE.json configs[1], "c2"): 2D 5-point thermal-block diffusion on
+a 511x511 grid (N = 261,121), 3x3 subdomains (P = Q = 9), mu log-uniform in
+[0.1, 10], f = 1, fp64, greedy basis n = 40 from 1024 seeded training mu
+(built on the GPU by rbs_build_greedy, untimed), 256 queries per GPU batched
+B = 32, RBCG to tol 1e-10 with symmetric red-black GS.
+
+A step = one rbs_solve_batch of B queries to convergence (every row of the
+hot path: reduced assembly + Cholesky, residual, projection, reduced solve,
+prolongation, smoothing, CG recurrences, stop test).  N > 1: one process per
+GPU (torchrun), queries sharded (rank r solves its own 256), no collective on
+the data path: weak scaling.  Timing: CUDA events on the solve stream after a
+barrier + synchronize, max over ranks.  The working set (W 84 MB + four 67 MB
+state vectors) exceeds the 126 MB L2, so no explicit flush is needed.
+
+--impl reference: the CPU oracle (oracle/, plain C fp64) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, query_set, train_set  # noqa: E402
+
+METRIC = "parameter queries solved/sec to rel. residual 1e-10 (c2, RBCG, 1 GPU)"
+UNIT = "queries/s"
+HBM_FALLBACK_GBS = 6650.0     # /opt/skills/guides/B200_PROFILING.md fallback
+FP64_NOMINAL_TFS = 37.0       # B200 HGX datasheet FP64 / FP64-tensor (not measured)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile-iters", type=int, default=30)
+    return p.parse_args()
+
+
+def workload_desc(c):
+    return (f"{c.name}: {c.dim}D {c.m}^{c.dim} (N={c.N}), {'x'.join(map(str, c.blocks))} blocks, "
+            f"mu logU[{c.lo},{c.hi}]^{c.P}, f=1, greedy n={c.n} from {c.n_train} train mu, "
+            f"{c.n_queries} queries/GPU, B={c.B}, RBCG sym-RBGS nu=1, tol 1e-10")
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.gpu = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+        load = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def _oracle_worker(args):
+    path, idx, mu = args
+    import oracle
+    from synth import CONFIGS as CF
+    c = CF["c2"]
+    d = np.load(path)
+    g = oracle.Grid(c.dim, c.m, c.blocks)
+    t = time.perf_counter()
+    out = g.rbcg(np.asfortranarray(d["W"]), d["ANq"], d["fn"], mu)
+    return idx, time.perf_counter() - t, out["its"], out["status"]
+
+
+def oracle_basis_file(c):
+    """Oracle-built basis at full size (test input recipe): coarse
+    greedy on 63^2, multilinear prolongation to the fine grid, oracle MGS and
+    offline blocks.  Cached per process in /tmp (rebuilt if absent)."""
+    import oracle
+    path = os.path.join(tempfile.gettempdir(), f"rbs_oracle_basis_{c.name}_{c.n}.npz")
+    if not os.path.exists(path):
+        W, ANq, fn = oracle.interpolated_basis(c.dim, c.m, c.blocks, train_set(c), c.n, 63)
+        np.savez(path, W=W, ANq=ANq, fn=fn)
+    return path
+
+
+def cpu_oracle_run(c, nq, offset=0):
+    """solve nq queries with the oracle, one process per core; returns q/s, details."""
+    import multiprocessing as mp
+    path = oracle_basis_file(c)
+    mus = query_set(c, offset + nq)[offset:]
+    cores = min(nq, os.cpu_count() or 1)
+    t = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_oracle_worker, [(path, i, mus[i]) for i in range(nq)])
+    wall = time.perf_counter() - t
+    its = [r[2] for r in res]
+    return nq / wall, cores, wall, its
+
+
+def run_reference(a):
+    c = CONFIGS[a.config]
+    ncpu = os.cpu_count() or 1
+    nq = min(ncpu, 8)
+    oracle_basis_file(c)
+    for w in range(a.warmup):
+        cpu_oracle_run(c, nq, offset=w * nq)
+    t0 = time.perf_counter()
+    tot_q, its_all, cores = 0, [], 1
+    for s in range(a.steps):
+        _, cores, _, its = cpu_oracle_run(c, nq, offset=(a.warmup + s) * nq)
+        tot_q += nq
+        its_all += its
+    el = time.perf_counter() - t0
+    v = tot_q / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * el / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(c), "basis": "oracle coarse-greedy (63^2) "
+                       "interpolated, n=40", "oracle_its": [int(min(its_all)), int(max(its_all))]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{nq} queries per step, one oracle process per core, "
+                                       f"RBCG to 1e-10 (host has {ncpu} cores)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        if rank == 0:
+            run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_1804_06363_b200 as rbs
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[a.config]
+    s = rbs.Solver(c.dim, c.m, c.blocks, device=local)
+    stream = torch.cuda.current_stream()
+
+    # ---- offline: greedy basis on the GPU (rank 0), broadcast over NCCL -----
+    t0 = time.perf_counter()
+    if rank == 0:
+        gr = s.build_greedy(train_set(c), c.n, load=False)
+        W = gr["W"].contiguous()
+        ANq = torch.tensor(gr["ANq"], device=s.device)
+        fn = torch.tensor(gr["fn"], device=s.device)
+        snap = [int(x) for x in gr["snap_iters"]]
+    else:
+        W = torch.empty((c.N, c.n), dtype=torch.float64, device=s.device)
+        ANq = torch.empty((c.P, c.n, c.n), dtype=torch.float64, device=s.device)
+        fn = torch.empty((c.n,), dtype=torch.float64, device=s.device)
+        snap = []
+    if world > 1:
+        for t in (W, ANq, fn):
+            dist.broadcast(t, 0)
+    s.load_basis(W, ANq.cpu().numpy(), fn.cpu().numpy())
+    torch.cuda.synchronize()
+    offline_s = time.perf_counter() - t0
+
+    # ---- queries: rank r owns its own n_queries (weak scaling) ---------------
+    nq = c.n_queries
+    mus_all = query_set(c, nq * world)
+    mus = mus_all[rank * nq:(rank + 1) * nq]
+    nb = nq // c.B
+    X = torch.empty((c.B, c.N), dtype=torch.float64, device=s.device)
+
+    def step(k, **kw):
+        b = k % nb
+        return s.solve_batch(mus[b * c.B:(b + 1) * c.B], X=X, want_a_n=False, **kw)
+
+    for w in range(max(a.warmup, 1)):
+        step(w)
+    # ---- timed region (device events, max over ranks) ------------------------
+    clocks = Clocks(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches, its = 0, []
+    for k in range(a.steps):
+        out = step(k)
+        launches += out["launches"]
+        its += [int(i) for i in out["its"]]
+        assert all(st == "CONVERGED" for st in out["status"]), out["status"]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=s.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    clk = clocks.stop()
+    value = a.steps * c.B * world / (ms / 1e3)
+
+    # ---- e2e: public API with host buffers (pinned X, host mu) --------------
+    Xh = torch.empty((c.B, c.N), dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    for k in range(a.steps):
+        b = k % nb
+        s.solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xh, x_location=rbs.RBS_MEM_HOST,
+                      want_a_n=True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=s.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = {"value": a.steps * c.B * world / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": c.B * c.P * 8,
+           "d2h_bytes_per_step": c.B * c.N * 8 + c.B * (4 + 4 + 8 + 8 + 8 * c.n)}
+
+    # ---- per-kernel device times (eager, events on the launching stream) -----
+    prof = step(0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
+    hbm, hbm_src = peaks()
+    Bq = c.B
+    k_ms, k_cnt = prof["k_proj"]
+    dur = k_ms / max(k_cnt, 1) / 1e3
+    alg_bytes = c.N * (40 * Bq) + c.N * c.n * 8          # p,x,r read + x,r write + W once
+    alg_flops = 2.0 * c.N * c.n * Bq                      # W^T r on the FP64 tensor cores
+    tot_ms = sum(v[0] for v in prof.values())
+    roof = {"bound": "hbm", "kernel": "k_proj<MODE_CG> (RBCG Steps 6-8 + W^T r)",
+            "achieved": alg_bytes / dur / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": alg_bytes / dur / 1e9 / hbm, "traffic": None, "peak_source": hbm_src,
+            "alg_bytes_per_launch": alg_bytes, "avg_launch_us": dur * 1e6,
+            "share_of_iteration": k_ms / tot_ms if tot_ms else None,
+            "fp64_tensor": {"achieved_tflops": alg_flops / dur / 1e12,
+                            "nominal_peak_tflops": FP64_NOMINAL_TFS,
+                            "frac_of_nominal": alg_flops / dur / 1e12 / FP64_NOMINAL_TFS}}
+    per_iter_bytes = {"k_cgp": 24 * Bq * c.N, "k_proj": alg_bytes, "k_prolong": 8 * Bq * c.N + c.N * c.n * 8,
+                      "k_gs": None, "k_alpha": 0, "k_reduce_solve": 0, "k_beta": 0}
+    kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
+                   "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items()}
+    for k, b in per_iter_bytes.items():
+        if b and kernels[k]["launches"]:
+            kernels[k]["GBps"] = b / (kernels[k]["avg_us"] * 1e-6) / 1e9
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(c), "queries_per_gpu": nq, "B": c.B, "n": c.n,
+                       "parallelism": f"query-shard x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (W 84 MB + 4 x 67 MB state > 126 MB)",
+                       "its_min_med_max": [min(its), int(np.median(its)), max(its)],
+                       "offline_greedy_s": round(offline_s, 2), "snapshot_its": snap[:6]},
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "kernels": kernels}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            nq_cpu = min(os.cpu_count() or 1, 8)
+            v, cores, wall, oits = cpu_oracle_run(c, nq_cpu)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": f"{nq_cpu} c2 queries, one oracle process per core, "
+                                              f"RBCG to 1e-10, oracle-built interpolated basis "
+                                              f"n=40 (its {min(oits)}-{max(oits)}), wall {wall:.1f}s"}
+        except Exception as e:  # reported, never silently dropped
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle",
+                                    "sample": f"failed: {e!r}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -129,6 +129,8 @@ typedef struct {
     int record_history;  /* 1: fill history[B][max_iter+1] */
     int x_location;      /* RBS_MEM_DEVICE (default) | RBS_MEM_HOST for X */
     int graph_chunk;     /* iterations per captured CUDA graph (default 16, even) */
+    int profile;         /* 1: launch eagerly (no graph) with CUDA events around every
+                            kernel; per-class times via rbs_last_profile (default 0) */
 } rbs_solve_opts;
 
 void rbs_default_opts(rbs_solve_opts* opts);
@@ -163,6 +165,15 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
 
 /* Number of kernel launches issued by the last rbs_solve_batch (instrumentation). */
 int64_t rbs_last_launch_count(const rbs_ctx* ctx);
+
+/* Kernel classes of the iteration body and their per-class device time (ms,
+ * CUDA events on the launching stream) and launch counts, accumulated over the
+ * complete iterations of the last rbs_solve_batch run with opts.profile = 1.
+ * ms_total / launches: host arrays of RBS_K_NCLASS. */
+enum { RBS_K_CGP = 0, RBS_K_ALPHA = 1, RBS_K_PROJ = 2, RBS_K_REDUCE_SOLVE = 3, RBS_K_PROLONG = 4,
+       RBS_K_GS = 5, RBS_K_BETA = 6, RBS_K_NCLASS = 7 };
+rbs_status rbs_last_profile(const rbs_ctx* ctx, double* ms_total, int64_t* launches);
+const char* rbs_kernel_class_name(int k);
 
 /* ---------------------------------------------------------------------------
  * Offline greedy build (algorithm0; adaptive: PAPER.md:294-308

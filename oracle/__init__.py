@@ -233,3 +233,30 @@ def rb_solve(ANq, fn, mu):
     a = np.empty(n)
     piv = lib().or_rb_solve(n, ANq.shape[0], _d(ANq), _d(fn), _d(mu), _d(a))
     return a, piv
+
+
+# -- full-size test input recipe ---------------------------------------------
+def interpolated_basis(dim, m, blocks, mu_train, n, m_coarse):
+    """Oracle-built basis at a size where the oracle greedy is too slow
+    (DESIGN.md "Input recipe"): greedy (algorithm3) on the coarse grid m_coarse,
+    multilinear prolongation of its basis vectors to the fine grid (input
+    generation only; (m+1) must be a multiple of (m_coarse+1)), then oracle MGS
+     and oracle offline blocks (eq12c).  Returns (W, ANq, fn)."""
+    from scipy.interpolate import RegularGridInterpolator
+    assert (m + 1) % (m_coarse + 1) == 0
+    gc = Grid(dim, m_coarse, blocks)
+    res = gc.greedy(mu_train, n)
+    hc, hf = 1.0 / (m_coarse + 1), 1.0 / (m + 1)
+    axc = np.arange(m_coarse + 2) * hc
+    fine = np.meshgrid(*[np.arange(1, m + 1) * hf] * dim, indexing="ij")
+    pts = np.stack([f.reshape(-1, order="F") for f in fine], axis=1)  # x fastest
+    W = None
+    for j in range(res["n"]):
+        v = np.zeros((m_coarse + 2,) * dim)
+        inner = res["W"][:, j].reshape((m_coarse,) * dim, order="F")
+        v[tuple(slice(1, m_coarse + 1) for _ in range(dim))] = inner
+        vf = RegularGridInterpolator([axc] * dim, v)(pts)
+        W, rej = mgs_append(W, vf)
+    g = Grid(dim, m, blocks)
+    ANq, fn = g.offline_blocks(W)
+    return np.asfortranarray(W), ANq, fn

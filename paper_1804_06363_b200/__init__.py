@@ -33,7 +33,8 @@ class RbsError(RuntimeError):
 class rbs_solve_opts(C.Structure):
     _fields_ = [("method", C.c_int), ("tol", C.c_double), ("max_iter", C.c_int),
                 ("smoother", C.c_int), ("sweeps", C.c_int), ("delta", C.c_double),
-                ("record_history", C.c_int), ("x_location", C.c_int), ("graph_chunk", C.c_int)]
+                ("record_history", C.c_int), ("x_location", C.c_int), ("graph_chunk", C.c_int),
+                ("profile", C.c_int)]
 
 
 _lib = None
@@ -45,6 +46,8 @@ _SIGS = {
     "rbs_destroy": (None, [C.c_void_p]),
     "rbs_last_error": (C.c_char_p, [C.c_void_p]),
     "rbs_last_launch_count": (C.c_int64, [C.c_void_p]),
+    "rbs_last_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rbs_kernel_class_name": (C.c_char_p, [C.c_int]),
     "rbs_set_operator_blocks": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int)]),
     "rbs_set_rhs_constant": (C.c_int, [C.c_void_p, C.c_double]),
@@ -172,6 +175,21 @@ def rbs_last_launch_count(ctx):
     return int(lib().rbs_last_launch_count(ctx))
 
 
+RBS_K_NCLASS = 7
+
+
+def rbs_last_profile(ctx):
+    ms = np.zeros(RBS_K_NCLASS)
+    cnt = np.zeros(RBS_K_NCLASS, dtype=np.int64)
+    _check(ctx, lib().rbs_last_profile(ctx, _ptr(ms), _ptr(cnt)), "rbs_last_profile")
+    return {lib().rbs_kernel_class_name(k).decode(): (float(ms[k]), int(cnt[k]))
+            for k in range(RBS_K_NCLASS)}
+
+
+def rbs_kernel_class_name(k):
+    return lib().rbs_kernel_class_name(int(k)).decode()
+
+
 def rbs_greedy_workspace_size(ctx, n_train, n_max):
     s = C.c_size_t()
     _check(ctx, lib().rbs_greedy_workspace_size(ctx, int(n_train), int(n_max), C.byref(s)),
@@ -276,6 +294,8 @@ class Solver:
         out = dict(X=X, its=its, status=[QSTATUS[int(s)] for s in st], qstatus=st, relres=rel,
                    true_relres=trr, a_n=None if a_n is None else a_n[:, :(self.n or 0)],
                    launches=rbs_last_launch_count(self.ctx))
+        if o.profile:
+            out["profile"] = rbs_last_profile(self.ctx)
         if hist is not None:
             out["history"] = [hist[b, :its[b] + 1].copy() for b in range(B)]
         return out

@@ -44,6 +44,10 @@ struct rbs_ctx {
     cudaGraphExec_t gexec = nullptr;
     std::string gkey;
     int g_per_chunk = 0;
+    // profiling (opts.profile): eager launches bracketed by events
+    std::vector<cudaEvent_t> pev;
+    double prof_ms[RBS_K_NCLASS] = {0};
+    int64_t prof_cnt[RBS_K_NCLASS] = {0};
 };
 
 namespace {
@@ -283,12 +287,28 @@ void rbs_destroy(rbs_ctx* ctx) {
     if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->pev) cudaEventDestroy(e);
     delete ctx;
 }
 
 const char* rbs_last_error(const rbs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
 
 int64_t rbs_last_launch_count(const rbs_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+rbs_status rbs_last_profile(const rbs_ctx* ctx, double* ms_total, int64_t* launches) {
+    if (!ctx || !ms_total || !launches) return RBS_E_ARG;
+    for (int k = 0; k < RBS_K_NCLASS; ++k) {
+        ms_total[k] = ctx->prof_ms[k];
+        launches[k] = ctx->prof_cnt[k];
+    }
+    return RBS_OK;
+}
+
+const char* rbs_kernel_class_name(int k) {
+    static const char* names[RBS_K_NCLASS] = {"k_cgp", "k_alpha", "k_proj", "k_reduce_solve",
+                                              "k_prolong", "k_gs", "k_beta"};
+    return (k >= 0 && k < RBS_K_NCLASS) ? names[k] : "";
+}
 
 rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], const int blocks[3]) {
     if (!ctx) return RBS_E_ARG;
@@ -449,6 +469,7 @@ void rbs_default_opts(rbs_solve_opts* o) {
     o->record_history = 0;
     o->x_location = RBS_MEM_DEVICE;
     o->graph_chunk = 16;
+    o->profile = 0;
 }
 
 rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opts* o, size_t* bytes) {
@@ -555,18 +576,37 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     const std::vector<int> seq = color_seq(o->smoother, o->sweeps);
     const int pgrid = grid_for(((g.N + 7) / 8) * (Bp / 8), 8, ctx->num_sms * 16);
 
+    // ---- profiling hooks (no-ops unless opts.profile) -------------------------
+    const bool prof = o->profile != 0;
+    int pne = 0;
+    std::vector<int> pcls;
+    if (prof && ctx->pev.empty()) {
+        ctx->pev.resize(2 * 256);
+        for (auto& e : ctx->pev) CK(cudaEventCreate(&e));
+    }
+    for (int k = 0; k < RBS_K_NCLASS; ++k) { ctx->prof_ms[k] = 0.0; ctx->prof_cnt[k] = 0; }
+    auto pb = [&](int cls) {
+        if (prof && pne < 256) { cudaEventRecord(ctx->pev[2 * pne], st); pcls.push_back(cls); }
+    };
+    auto pe = [&]() {
+        if (prof && pne < 256) { cudaEventRecord(ctx->pev[2 * pne + 1], st); ++pne; }
+    };
+
     // ---- pass builders -------------------------------------------------------
     auto prolong = [&](double* Yv, int acc) {
         ProlongArgs a{};
         a.N = g.N; a.Bp = Bp; a.npad = npad; a.W = ctx->Wi; a.E = L.E; a.active = L.active;
         a.Y = Yv; a.accumulate = acc; a.done = done;
+        pb(RBS_K_PROLONG);
         if (npad > 0) {
             k_prolong<<<pgrid, kThreads, 0, st>>>(a);
         } else if (!acc) {  // empty basis: y0 = 0
             k_fill_batch<<<fgrid, 256, 0, st>>>(Yv, g.N, ctx->N8, Bp, 0, nullptr, 0.0);
         } else {
+            pe();
             return 0;
         }
+        pe();
         return 1;
     };
     auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last) {
@@ -579,6 +619,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         for (size_t t = 0; t < cs.size(); ++t) {
             a.color = cs[t];
             const bool l = last && t + 1 == cs.size();
+            pb(RBS_K_GS);
             if (g.dim == 2) {
                 if (l) k_gs<2, true><<<nctf, kThreads, fsm, st>>>(a);
                 else k_gs<2, false><<<nctf, kThreads, fsm, st>>>(a);
@@ -586,6 +627,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
                 if (l) k_gs<3, true><<<nctf, kThreads, fsm, st>>>(a);
                 else k_gs<3, false><<<nctf, kThreads, fsm, st>>>(a);
             }
+            pe();
             ++cnt;
         }
         return cnt;
@@ -596,8 +638,10 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         a.W = ctx->Wi; a.theta = L.theta; a.active = use_active ? L.active : nullptr;
         a.alpha = L.alpha; a.P = P; a.X = L.X; a.R = L.R; a.V = Fv; a.vconst = ctx->fconst;
         a.part = L.partP; a.done = use_active ? done : nullptr;
+        pb(RBS_K_PROJ);
         if (mode == MODE_CG) launch_proj<MODE_CG>(g, nct, psm, st, a);
         else launch_proj<MODE_RESID>(g, nct, psm, st, a);
+        pe();
         return 1;
     };
     auto cgp = [&](const double* Pold, double* Pnew) {
@@ -605,8 +649,10 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.part = L.partF; a.nctf = nctf;
         a.done = done;
+        pb(RBS_K_CGP);
         if (g.dim == 2) k_cgp<2><<<nctf, kThreads, fsm, st>>>(a);
         else k_cgp<3><<<nctf, kThreads, fsm, st>>>(a);
+        pe();
         return 1;
     };
 
@@ -631,17 +677,17 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             double* Pold = (it & 1) ? L.P1 : L.P0;
             double* Pnew = (it & 1) ? L.P0 : L.P1;
             c += cgp(Pold, Pnew);                               // Step 11 (prev) + A p
-            k_alpha<<<1, 512, 0, st>>>(S); ++c;                 // Step 5
+            pb(RBS_K_ALPHA); k_alpha<<<1, 512, 0, st>>>(S); pe(); ++c;            // Step 5
             c += proj(MODE_CG, Pnew, true);                     // Steps 6-7, ||r||, W^T r
-            k_reduce_solve<<<Bp, 128, 0, st>>>(S); ++c;         // Step 8, reduced solve
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 128, 0, st>>>(S); pe(); ++c;  // Step 8
             c += prolong(L.Y, 0);                               // Step 9: y0 = W e
             c += smooth(L.Y, L.R, 0.0, true);                   //         y = S(A, r, y0)
-            k_beta<<<1, 512, 0, st>>>(S, 0); ++c;               // Step 10
+            pb(RBS_K_BETA); k_beta<<<1, 512, 0, st>>>(S, 0); pe(); ++c;           // Step 10
         } else {
             c += prolong(L.X, 1);                               // Step 6
             c += smooth(L.X, Fv, ctx->fconst, false);           // Step 7
             c += proj(MODE_RESID, nullptr, true);               // Steps 2, 4
-            k_reduce_solve<<<Bp, 128, 0, st>>>(S); ++c;         // Steps 3, 5
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 128, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
         }
         return c;
     };
@@ -652,7 +698,27 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
              o->tol, o->delta, o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist,
              rhs_dev ? 1 : 0, n, npad, ctx->fconst);
     const std::string key(keybuf);
-    if (!ctx->gexec || ctx->gkey != key) {
+    if (prof) {
+        // eager launches, one iteration at a time, events on the launching stream
+        volatile int* hf = ctx->h_flag;
+        for (int64_t it = 0; it <= (int64_t)o->max_iter + 1; ++it) {
+            pne = 0;
+            pcls.clear();
+            launches += body((int)(it & 1));
+            CKL();
+            CK(cudaMemcpyAsync((void*)ctx->h_flag, done, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const bool fin = hf[0] != 0;
+            if (!fin)  // only complete iterations (no early-exit launches) are accumulated
+                for (int e = 0; e < pne; ++e) {
+                    float ms = 0.f;
+                    CK(cudaEventElapsedTime(&ms, ctx->pev[2 * e], ctx->pev[2 * e + 1]));
+                    ctx->prof_ms[pcls[e]] += ms;
+                    ctx->prof_cnt[pcls[e]] += 1;
+                }
+            if (fin) break;
+        }
+    } else if (!ctx->gexec || ctx->gkey != key) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
         cudaStream_t cap;
         CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -678,7 +744,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     const int64_t max_launch = (int64_t)o->max_iter / chunk + 3;
     volatile int* hf = ctx->h_flag;
     hf[0] = hf[1] = 0;
-    for (int64_t l = 0;; ++l) {
+    for (int64_t l = 0; !prof; ++l) {
         CK(cudaGraphLaunch(ctx->gexec, st));
         launches += per_iter;
         CK(cudaMemcpyAsync((void*)(ctx->h_flag + (l & 1)), done, sizeof(int), cudaMemcpyDeviceToHost, st));

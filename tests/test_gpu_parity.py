@@ -265,3 +265,32 @@ def test_gpu_greedy_basis_solves(orc, rbs):
     out = s.solve_batch(mus, record_history=1)
     # the oracle solves with the oracle's own basis; same subspace => same iterates
     compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg")
+
+
+# ----------------------------------------------------------------------------- full size (c2)
+def test_c2_full_size_sampled(orc, rbs):
+    """BASELINE configs[1] at full size in bench.py's launch configuration (B = 32):
+    oracle-built basis (coarse greedy interpolated, DESIGN.md input recipe);
+    sampled outputs the oracle computes one by one + a property at any size."""
+    c = CONFIGS["c2"]
+    W, ANq, fn = orc.interpolated_basis(c.dim, c.m, c.blocks, train_set(c), c.n, 63)
+    g = orc.Grid(c.dim, c.m, c.blocks)
+    s = rbs.Solver(c.dim, c.m, c.blocks).load_basis(W, ANq, fn)
+    mus = query_set(c)[:c.B]
+    # (1) fixed-iteration mode on the whole batch, oracle on 3 sampled queries
+    out = s.solve_batch(mus, tol=0.0, max_iter=30, record_history=1)
+    idx = [0, 13, 31]
+    compare(dict(out, X=out["X"][idx], status=[out["status"][i] for i in idx], its=out["its"][idx],
+                 a_n=out["a_n"][idx], history=[out["history"][i] for i in idx]),
+            g, W, ANq, fn, mus[idx], "rbcg", tol=0.0, max_iter=30)
+    # (2) converged batch: every query satisfies the stopping property, checked
+    #     with the oracle's operator; one query compared in full
+    out = s.solve_batch(mus, record_history=1)
+    assert all(st == "CONVERGED" for st in out["status"])
+    X = out["X"].cpu().numpy()
+    for b in range(c.B):
+        r = 1.0 - g.apply_A(mus[b], X[b])
+        assert np.linalg.norm(r) / np.sqrt(g.N) < 1.5e-10, b
+    compare(dict(out, X=out["X"][[5]], status=[out["status"][5]], its=out["its"][[5]],
+                 a_n=out["a_n"][[5]], history=[out["history"][5]]),
+            g, W, ANq, fn, mus[[5]], "rbcg")
