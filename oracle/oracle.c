@@ -539,7 +539,7 @@ int or_cg(int dim, int64_t m, const int* blocks, const double* mu, const double*
  * PAPER.md:301); n = 0 is the symmetric-GS-preconditioned CG. */
 static int snapshot(int dim, int64_t m, const int* blocks, int n, const double* W,
                     const double* ANq_ld, int ldA, const double* fn, const double* mu,
-                    double tol, double* x, int* its)
+                    double tol, int max_iter, double* x, int* its)
 {
     int Q = grid_Q(dim, blocks);
     /* compact leading n x n blocks */
@@ -548,7 +548,7 @@ static int snapshot(int dim, int64_t m, const int* blocks, int n, const double* 
         for (int i = 0; i < n; ++i)
             for (int j = 0; j < n; ++j)
                 A[(int64_t)q * n * n + i * n + j] = ANq_ld[(int64_t)q * ldA * ldA + i * ldA + j];
-    or_opts o = {tol, 200000, OR_SMOOTH_SYM_RBGS, 1, 1.0, 1e-12};
+    or_opts o = {tol, max_iter, OR_SMOOTH_SYM_RBGS, 1, 1.0, 1e-12};
     double trr;
     int st = or_rbcg(dim, m, blocks, n, W, A, fn, mu, NULL, &o, x, its, NULL, NULL, &trr);
     free(A);
@@ -569,15 +569,30 @@ static int greedy_core(int dim, int64_t m, const int* blocks, int n_train,
     double* AN = (double*)malloc(sizeof(double) * (size_t)n_max * n_max + 8);
     double* L = (double*)malloc(sizeof(double) * (size_t)n_max * n_max + 8);
     double* a = (double*)malloc(sizeof(double) * (size_t)n_max + 8);
-    int n = 0, rej = 0;
+    int n = 0, rej = 0, its_first = -1;
     /* Step 0/1: mu_1 = Xi_train[0] (AMB-13; Xi_train itself is seeded random) */
     int cand = 0;
     int list_pos = 0;
     while (n < n_max && cand >= 0) {
         const double* mu = mu_train + (int64_t)cand * P;
         /* Step 3: solve the snapshot (adaptive: RBCG with W_{N-1}) */
-        int its = 0;
-        snapshot(dim, m, blocks, adaptive ? n : 0, W, ANq, n_max, fn, mu, snapshot_tol, x, &its);
+        int its = 0, st;
+        if (!adaptive || n == 0) {
+            /* N = 1 (or plain greedy): the "standard solver" of PAPER.md:291 = SGS-PCG */
+            st = snapshot(dim, m, blocks, 0, W, ANq, n_max, fn, mu, snapshot_tol, 200000, x, &its);
+            if (n == 0 && its_first < 0) its_first = its;
+        } else {
+            /* RBCG with W_{N-1}, guarded (AMB-22): if it has not
+             * converged within 2*its_1 + 50 iterations (its_1 = the N = 1 snapshot),
+             * fall back to the standard solver. */
+            st = snapshot(dim, m, blocks, n, W, ANq, n_max, fn, mu, snapshot_tol,
+                          2 * (its_first > 0 ? its_first : 1000) + 50, x, &its);
+            if (st != OR_CONVERGED) {
+                st = snapshot(dim, m, blocks, 0, W, ANq, n_max, fn, mu, snapshot_tol, 200000, x, &its);
+                its = -its;   /* reported negative: fallback used */
+            }
+        }
+        (void)st;
         /* Step 4: W_N = MGS(W_{N-1}, x(mu_N)) */
         int rejected = or_mgs_append(N, n, W, x, drop_tol);
         excluded[cand] = 1;

@@ -86,7 +86,9 @@ int or_cg(int dim, int64_t m, const int* blocks, const double* mu, const double*
 /* Greedy (algorithm0; adaptive=1: algorithm3).
  * W_out: column-major N x n_max.  ANq_out: Q x n_max x n_max (only the leading
  * n_out x n_out block of each q is meaningful, row stride n_max).
- * returns n_out. */
+ * snap_iters[k] < 0: the guarded RBCG snapshot did not converge within
+ * 2*its_1 + 50 iterations and the SGS-PCG fallback took |snap_iters[k]|
+ * iterations (DESIGN.md AMB-22).  returns n_out. */
 int or_greedy(int dim, int64_t m, const int* blocks, int n_train, const double* mu_train,
               int n_max, int adaptive, double snapshot_tol, double drop_tol,
               double* W_out, double* ANq_out, double* fn_out, int* selected,

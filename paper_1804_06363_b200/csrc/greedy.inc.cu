@@ -159,7 +159,7 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
     rbs_default_opts(&so);
     so.tol = snapshot_tol;
     so.max_iter = 200000;
-    int n = 0, rej = 0, cand = 0;
+    int n = 0, rej = 0, cand = 0, its_first = -1;
     auto dot = [&](const double* a, int64_t sa, const double* b, int64_t sb, double* out) {
         k_dot<<<kDotCtas, 256, 0, st>>>(a, sa, b, sb, g.N, L.dpart);
         k_sum_to<<<1, 32, 0, st>>>(L.dpart, kDotCtas, out);
@@ -173,11 +173,26 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
             for (int i = 0; i < ctx->n; ++i)
                 for (int j = 0; j < ctx->n; ++j)
                     ctx->hANq[((size_t)q * ctx->n + i) * ctx->n + j] = hA[((size_t)q * npad + i) * npad + j];
+        // N = 1 (or plain greedy): SGS-PCG, the standard solver of PAPER.md:291.
+        // N >= 2 (adaptive): RBCG with W_{N-1}, guarded (AMB-22): not converged
+        // within 2*its_1 + 50 -> fall back to SGS-PCG; its < 0.
         int its = 0, qs = 0;
+        so.max_iter = (ctx->n == 0) ? 200000 : 2 * (its_first > 0 ? its_first : 1000) + 50;
         rbs_status s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, nullptr, L.x, &its,
                                        &qs, nullptr, nullptr, nullptr, nullptr, L.solve_ws,
                                        L.solve_bytes, stream);
         if (s != RBS_OK) return s;
+        if (ctx->n == 0 && its_first < 0) its_first = its;
+        if (qs != Q_CONVERGED && ctx->n > 0) {
+            ctx->n = 0;
+            ctx->hfn.clear();
+            ctx->hANq.clear();
+            so.max_iter = 200000;
+            s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, nullptr, L.x, &its, &qs,
+                                nullptr, nullptr, nullptr, nullptr, L.solve_ws, L.solve_bytes, stream);
+            if (s != RBS_OK) return s;
+            its = -its;
+        }
         // ---- Step 4: W_N = MGS(W_{N-1}, x) ------------------------------------
         CK(cudaMemcpyAsync(L.w, L.x, (size_t)g.N * 8, cudaMemcpyDeviceToDevice, st));
         dot(L.x, 1, L.x, 1, L.scal + 0);

@@ -396,11 +396,15 @@ __device__ __forceinline__ void last_block_update(SolveState& s, bool bump_k) {
 __global__ void __launch_bounds__(128) k_reduce_solve(SolveState s) {
     if (*(volatile const int*)s.done) return;
     __shared__ double s_rn[kMaxN + 1];
+    __shared__ double s_L[kMaxN * kMaxN];
     __shared__ int s_go;
     const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rows = s.npad + 1;
     const bool act = s.active[b] != 0;
     if (act) {
+        // stage the factor in shared memory while the partial sums stream in
+        const double* Lg = s.L + (int64_t)b * s.npad * s.npad;
+        for (int t = threadIdx.x; t < s.n * s.npad; t += blockDim.x) s_L[t] = Lg[t];
         for (int r = warp; r <= s.n; r += 4) {
             const int j = r < s.n ? r : s.npad;
             const double v = warp_sum_row(s.partP + ((int64_t)b * rows + j) * s.nct, s.nct, lane);
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__(128) k_reduce_solve(SolveState s) {
         }
         __syncthreads();
         if (s_go && s.n > 0 && warp == 0) {
-            const double* L = s.L + (int64_t)b * s.npad * s.npad;
+            const double* L = s_L;
             double z0 = lane < s.n ? s_rn[lane] : 0.0;
             double z1 = lane + 32 < s.n ? s_rn[lane + 32] : 0.0;
             warp_chol_solve(L, s.npad, s.n, &z0, &z1, lane);
