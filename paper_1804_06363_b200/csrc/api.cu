@@ -90,8 +90,8 @@ inline int proj_ctas(const Geo& g) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(c, 296));
 }
 inline int flat_ctas(const Geo& g) {
-    int64_t c = (g.N + 31) / 32;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(c, 1184));
+    int64_t c = (g.N + 63) / 64;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(c, 296));
 }
 inline int grid_for(int64_t work, int per, int cap) {
     int64_t c = (work + per - 1) / per;
@@ -609,10 +609,10 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         pe();
         return 1;
     };
-    auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last) {
+    auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last, int init) {
         GSArgs a{};
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
-        a.Y = Yv; a.Rhs = rhs; a.rconst = rconst; a.part = L.partF; a.nctf = nctf; a.done = done;
+        a.Y = Yv; a.Rhs = rhs; a.rconst = rconst; a.init = init; a.s = S; a.done = done;
         int cnt = 0;
         std::vector<int> cs = seq;
         if (cs.empty() && last) cs.push_back(-1);
@@ -621,11 +621,11 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             const bool l = last && t + 1 == cs.size();
             pb(RBS_K_GS);
             if (g.dim == 2) {
-                if (l) k_gs<2, true><<<nctf, kThreads, fsm, st>>>(a);
-                else k_gs<2, false><<<nctf, kThreads, fsm, st>>>(a);
+                if (l) k_gs<2, true><<<nctf, kFlat, fsm, st>>>(a);
+                else k_gs<2, false><<<nctf, kFlat, fsm, st>>>(a);
             } else {
-                if (l) k_gs<3, true><<<nctf, kThreads, fsm, st>>>(a);
-                else k_gs<3, false><<<nctf, kThreads, fsm, st>>>(a);
+                if (l) k_gs<3, true><<<nctf, kFlat, fsm, st>>>(a);
+                else k_gs<3, false><<<nctf, kFlat, fsm, st>>>(a);
             }
             pe();
             ++cnt;
@@ -647,11 +647,10 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     auto cgp = [&](const double* Pold, double* Pnew) {
         CGPArgs a{};
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
-        a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.part = L.partF; a.nctf = nctf;
-        a.done = done;
+        a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.s = S; a.done = done;
         pb(RBS_K_CGP);
-        if (g.dim == 2) k_cgp<2><<<nctf, kThreads, fsm, st>>>(a);
-        else k_cgp<3><<<nctf, kThreads, fsm, st>>>(a);
+        if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
+        else k_cgp<3><<<nctf, kFlat, fsm, st>>>(a);
         pe();
         return 1;
     };
@@ -659,9 +658,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     // ---- RBCG Step 2-3: y_0 = RBI(A, r_0, W, 1), rho_0 = r_0^T y_0 ------------
     if (cg) {
         launches += prolong(L.Y, 0);
-        launches += smooth(L.Y, L.R, 0.0, true);
-        k_beta<<<1, 512, 0, st>>>(S, 1);
-        ++launches;
+        launches += smooth(L.Y, L.R, 0.0, true, 1);            // + rho_0, PRECOND check
         CKL();
     } else {
         k_update_done<<<1, 1, 0, st>>>(L.active, Bp, done);
@@ -676,18 +673,16 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         if (cg) {
             double* Pold = (it & 1) ? L.P1 : L.P0;
             double* Pnew = (it & 1) ? L.P0 : L.P1;
-            c += cgp(Pold, Pnew);                               // Step 11 (prev) + A p
-            pb(RBS_K_ALPHA); k_alpha<<<1, 512, 0, st>>>(S); pe(); ++c;            // Step 5
-            c += proj(MODE_CG, Pnew, true);                     // Steps 6-7, ||r||, W^T r
-            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 128, 0, st>>>(S); pe(); ++c;  // Step 8
-            c += prolong(L.Y, 0);                               // Step 9: y0 = W e
-            c += smooth(L.Y, L.R, 0.0, true);                   //         y = S(A, r, y0)
-            pb(RBS_K_BETA); k_beta<<<1, 512, 0, st>>>(S, 0); pe(); ++c;           // Step 10
+            c += cgp(Pold, Pnew);             // Step 11 (prev) + A p, Step 5 (alpha) in last CTA
+            c += proj(MODE_CG, Pnew, true);   // Steps 6-7, ||r||, W^T r
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 256, 0, st>>>(S); pe(); ++c;  // Step 8
+            c += prolong(L.Y, 0);             // Step 9: y0 = W e
+            c += smooth(L.Y, L.R, 0.0, true, 0);  // y = S(A, r, y0); Step 10 in last CTA
         } else {
             c += prolong(L.X, 1);                               // Step 6
-            c += smooth(L.X, Fv, ctx->fconst, false);           // Step 7
+            c += smooth(L.X, Fv, ctx->fconst, false, 0);        // Step 7
             c += proj(MODE_RESID, nullptr, true);               // Steps 2, 4
-            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 128, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 256, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
         }
         return c;
     };

@@ -7,6 +7,11 @@
 // (mma.sync m8n8k4 f64 -> SASS DMMA): tcgen05 has no f64 kind on sm_100a.
 // Reductions are deterministic two-stage sums (fixed CTA partition, fixed
 // in-CTA order, fixed stage-2 order): bitwise reproducible run to run.
+// Streaming passes are latency-bound unless each thread keeps several
+// independent loads in flight: loops are unrolled with every load of the
+// unrolled group issued before any arithmetic that consumes it.
+// The tiny scalar steps (alpha, beta, stop tests) are folded into the
+// last CTA of the producing pass (atomic ticket), not separate launches.
 #pragma once
 #include "rbs_internal.cuh"
 
@@ -15,6 +20,122 @@ namespace rbs {
 enum { MODE_CG = 0, MODE_RESID = 1, MODE_PLAIN = 2 };
 enum { Q_CONVERGED = 0, Q_MAXIT = 1, Q_NOT_SPD = 2, Q_CURVATURE = 3, Q_PRECOND = 4,
        Q_NONFINITE = 5 };
+
+constexpr int kFlat = 512;     // threads per CTA of the flat (thread-per-element) passes
+
+// ---------------------------------------------------------------------------
+// Per-solve state shared by the bookkeeping steps.
+// ---------------------------------------------------------------------------
+struct SolveState {
+    int B, Bp, n, npad, nct, nctf, maxit, method;
+    double tol, delta;
+    const double* ANq;        // [Q][npad][npad]
+    int Q;
+    double* theta;            // [Q][Bp]
+    double* fproj;            // [Bp][npad+1]: f_n and ||f||^2
+    double* L;                // [Bp][npad][npad]
+    double* E;                // [npad][Bp]
+    double* a_n;              // [Bp][npad]
+    double* partP;            // [Bp][npad+1][nct]
+    double* partF;            // [Bp][2][nctf]
+    double *alpha, *beta, *rho, *rr, *fnorm, *relres;
+    int *active, *status, *its, *pivot;
+    int* kcount;
+    int* done;
+    unsigned* ticket;
+    double* hist;             // [Bp][maxit+1] or nullptr
+};
+
+__device__ __forceinline__ int ld_flag(const int* p) { return *(volatile const int*)p; }
+
+// deterministic warp sum of p[0..cnt) (4 independent loads in flight per lane)
+__device__ __forceinline__ double warp_sum_row(const double* p, int cnt, int lane) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int c = lane;
+    for (; c + 96 < cnt; c += 128) {
+        s0 += __ldcg(p + c);
+        s1 += __ldcg(p + c + 32);
+        s2 += __ldcg(p + c + 64);
+        s3 += __ldcg(p + c + 96);
+    }
+    for (; c < cnt; c += 32) s0 += __ldcg(p + c);
+    double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// triangular solves L L^T e = rhs by one warp; lane owns rows lane, lane+32.
+__device__ void warp_chol_solve(const double* L, int ld, int n, double* z0, double* z1, int lane) {
+    for (int i = 0; i < n; ++i) {
+        const int own = i & 31, slot = i >> 5;
+        const double mine = slot ? *z1 : *z0;
+        const double zi = __shfl_sync(0xffffffffu, mine, own) / L[i * ld + i];
+        if (lane == own) { if (slot) *z1 = zi; else *z0 = zi; }
+        if (lane > i && lane < n) *z0 -= L[lane * ld + i] * zi;
+        if (lane + 32 > i && lane + 32 < n) *z1 -= L[(lane + 32) * ld + i] * zi;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        const int own = i & 31, slot = i >> 5;
+        const double mine = slot ? *z1 : *z0;
+        const double ei = __shfl_sync(0xffffffffu, mine, own) / L[i * ld + i];
+        if (lane == own) { if (slot) *z1 = ei; else *z0 = ei; }
+        if (lane < i) *z0 -= L[i * ld + lane] * ei;
+        if (lane + 32 < i) *z1 -= L[i * ld + lane + 32] * ei;
+    }
+}
+
+// Atomic ticket: returns true in exactly one thread (threadIdx.x == 0) of the
+// CTA that finishes last; all earlier CTAs' global writes are then visible.
+__device__ __forceinline__ bool cta_is_last(unsigned* ticket, int* s_last) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        *s_last = (t == gridDim.x - 1);
+        if (*s_last) __threadfence();
+    }
+    __syncthreads();
+    return *s_last != 0;
+}
+
+__device__ __forceinline__ void release_ticket(unsigned* ticket) {
+    if (threadIdx.x == 0) {
+        *(volatile unsigned*)ticket = 0u;
+        __threadfence();
+    }
+}
+
+__device__ __forceinline__ void update_done(const SolveState& s) {
+    if (threadIdx.x == 0) {
+        int any = 0;
+        for (int b = 0; b < s.Bp; ++b) any |= ((volatile int*)s.active)[b];
+        *(volatile int*)s.done = any ? 0 : 1;
+    }
+}
+
+// sum over the CTAs' partials part[(b*2+slot)*nctf + c] for every query b;
+// result in s_out[b].  Whole CTA participates (blockDim.x multiple of Bp).
+__device__ void cta_sum_slot(const SolveState& s, int slot, double* s_buf, double* s_out) {
+    const int gsz = blockDim.x / s.Bp;
+    const int b = threadIdx.x / gsz, t = threadIdx.x - b * gsz;
+    double v0 = 0.0, v1 = 0.0;
+    const double* p = s.partF + ((int64_t)b * 2 + slot) * s.nctf;
+    int c = t;
+    for (; c + gsz < s.nctf; c += 2 * gsz) {
+        v0 += __ldcg(p + c);
+        v1 += __ldcg(p + c + gsz);
+    }
+    if (c < s.nctf) v0 += __ldcg(p + c);
+    s_buf[threadIdx.x] = v0 + v1;
+    __syncthreads();
+    if (t == 0) {
+        double a = 0.0;
+        for (int u = 0; u < gsz; ++u) a += s_buf[b * gsz + u];
+        s_out[b] = a;
+    }
+    __syncthreads();
+}
 
 // ---------------------------------------------------------------------------
 // Projection family: per node-query value v (mode-dependent), then
@@ -25,6 +146,7 @@ enum { Q_CONVERGED = 0, Q_MAXIT = 1, Q_NOT_SPD = 2, Q_CURVATURE = 3, Q_PRECOND =
 // MODE_RESID (RBI Step 2): v = b - A x (not stored).
 // MODE_PLAIN: v = V (or the constant vconst).
 // Warp layout = DMMA B-fragment: lane l owns node 4g + (l&3), query 8bt + (l>>2).
+// Two node groups per warp iteration, all loads of both issued first.
 // ---------------------------------------------------------------------------
 struct ProjArgs {
     Geo g;
@@ -44,8 +166,51 @@ struct ProjArgs {
 };
 
 template <int MODE, int DIM>
-__global__ void __launch_bounds__(kThreads) k_proj(ProjArgs a) {
-    if (a.done && *(volatile const int*)a.done) return;
+__device__ __forceinline__ void proj_load(const ProjArgs& a, const double* s_th, int b, int64_t i,
+                                          bool ok, double* nb, double& c0, double& c1, double& c2,
+                                          int& I, int& J, int& K) {
+    if (!ok) return;
+    const int64_t e = i * a.Bp + b;
+    if (MODE == MODE_PLAIN) {
+        c0 = a.V ? __ldg(a.V + e) : a.vconst;
+        return;
+    }
+    node_coords(a.g, (uint32_t)i, I, J, K);
+    if (MODE == MODE_CG) {
+        c0 = __ldg(a.P + e);
+        node_nbrs<DIM>(a.g, a.P, a.Bp, i, b, I, J, K, nb);
+        c1 = a.X[e];
+        c2 = a.R[e];
+    } else {
+        c0 = a.X[e];
+        node_nbrs<DIM>(a.g, a.X, a.Bp, i, b, I, J, K, nb);
+        c1 = a.V ? __ldg(a.V + e) : a.vconst;
+    }
+}
+
+template <int MODE, int DIM>
+__device__ __forceinline__ double proj_value(const ProjArgs& a, const double* s_th, double al,
+                                             int b, int64_t i, bool ok, const double* nb,
+                                             double c0, double c1, double c2, int I, int J, int K) {
+    if (!ok) return 0.0;
+    if (MODE == MODE_PLAIN) return c0;
+    double k[2 * DIM];
+    node_kappa<DIM>(a.g, s_th, a.Bp, b, I, J, K, k);
+    const double q = stencil_apply<DIM>(a.g, k, c0, nb);
+    const int64_t e = i * a.Bp + b;
+    if (MODE == MODE_CG) {
+        const double xv = fma(al, c0, c1);
+        const double rv = fma(-al, q, c2);
+        a.X[e] = xv;
+        a.R[e] = rv;
+        return rv;
+    }
+    return c1 - q;
+}
+
+template <int MODE, int DIM>
+__global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
+    if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
     const int Bp = a.Bp, npad = a.npad, nbt = Bp >> 3, ntile = npad >> 3;
     const int nlc = 8 / nbt;  // node lanes per CTA
@@ -67,6 +232,7 @@ __global__ void __launch_bounds__(kThreads) k_proj(ProjArgs a) {
     const int b = bt * 8 + (lane >> 2);
     const bool wact = nl < nlc;
     const bool qact = s_act[b] != 0;
+    const double al = s_alpha[b];
     const int64_t g0 = (a.ngroups * blockIdx.x) / gridDim.x;
     const int64_t g1 = (a.ngroups * (blockIdx.x + 1)) / gridDim.x;
 
@@ -75,41 +241,34 @@ __global__ void __launch_bounds__(kThreads) k_proj(ProjArgs a) {
     for (int t = 0; t < 16; ++t) acc[t] = 0.0;
     double rr = 0.0;
     if (wact) {
-        for (int64_t gi = g0 + nl; gi < g1; gi += nlc) {
-            const int64_t i = gi * 4 + (lane & 3);
-            double v = 0.0;
-            if (i < a.g.N && qact) {
-                const int64_t e = i * Bp + b;
-                if (MODE == MODE_PLAIN) {
-                    v = a.V ? a.V[e] : a.vconst;
-                } else {
-                    int I, J, K;
-                    node_coords(a.g, (uint32_t)i, I, J, K);
-                    double k[2 * DIM], nb[2 * DIM];
-                    node_kappa<DIM>(a.g, s_th, Bp, b, I, J, K, k);
-                    if (MODE == MODE_CG) {
-                        const double pp = __ldg(a.P + e);
-                        node_nbrs<DIM>(a.g, a.P, Bp, i, b, I, J, K, nb);
-                        const double q = stencil_apply<DIM>(a.g, k, pp, nb);
-                        const double al = s_alpha[b];
-                        const double xv = fma(al, pp, a.X[e]);
-                        const double rv = fma(-al, q, a.R[e]);
-                        a.X[e] = xv;
-                        a.R[e] = rv;
-                        v = rv;
-                    } else {  // MODE_RESID
-                        const double xp = a.X[e];
-                        node_nbrs<DIM>(a.g, a.X, Bp, i, b, I, J, K, nb);
-                        const double q = stencil_apply<DIM>(a.g, k, xp, nb);
-                        v = (a.V ? a.V[e] : a.vconst) - q;
-                    }
-                }
-            }
-            rr = fma(v, v, rr);
-            const double* wrow = a.W + i * npad + (lane >> 2);
+        for (int64_t gi = g0 + nl; gi < g1; gi += 2 * nlc) {
+            const int64_t gB = gi + nlc;
+            const int64_t iA = gi * 4 + (lane & 3), iB = gB * 4 + (lane & 3);
+            const bool okA = iA < a.g.N && qact, okB = gB < g1 && iB < a.g.N && qact;
+            double nbA[2 * DIM], nbB[2 * DIM];
+            double a0 = 0, a1 = 0, a2 = 0, b0 = 0, b1 = 0, b2 = 0;
+            int IA = 1, JA = 1, KA = 1, IB = 1, JB = 1, KB = 1;
+            proj_load<MODE, DIM>(a, s_th, b, iA, okA, nbA, a0, a1, a2, IA, JA, KA);
+            proj_load<MODE, DIM>(a, s_th, b, iB, okB, nbB, b0, b1, b2, IB, JB, KB);
+            double wA[8], wB[8];
+            const double* wrowA = a.W + iA * npad + (lane >> 2);
+            const double* wrowB = a.W + (gB < g1 ? iB : iA) * npad + (lane >> 2);
 #pragma unroll
             for (int jt = 0; jt < 8; ++jt)
-                if (jt < ntile) dmma_8x8x4(acc[2 * jt], acc[2 * jt + 1], __ldg(wrow + jt * 8), v);
+                if (jt < ntile) {
+                    wA[jt] = __ldg(wrowA + jt * 8);
+                    wB[jt] = __ldg(wrowB + jt * 8);
+                }
+            const double vA = proj_value<MODE, DIM>(a, s_th, al, b, iA, okA, nbA, a0, a1, a2, IA, JA, KA);
+            const double vB = proj_value<MODE, DIM>(a, s_th, al, b, iB, okB, nbB, b0, b1, b2, IB, JB, KB);
+            rr = fma(vA, vA, rr);
+            rr = fma(vB, vB, rr);
+#pragma unroll
+            for (int jt = 0; jt < 8; ++jt)
+                if (jt < ntile) {
+                    dmma_8x8x4(acc[2 * jt], acc[2 * jt + 1], wA[jt], vA);
+                    dmma_8x8x4(acc[2 * jt], acc[2 * jt + 1], wB[jt], vB);
+                }
         }
     }
     // rr of query b: lanes sharing l>>2 (fixed order)
@@ -139,7 +298,9 @@ __global__ void __launch_bounds__(kThreads) k_proj(ProjArgs a) {
 
 // ---------------------------------------------------------------------------
 // Prolongation  Y = W E  (or Y += W E), PAPER.md:144-147 (eq7) / 165.
-// DMMA with M = 8 nodes, N = 8 queries, K = 4 basis vectors.
+// DMMA with M = 8 nodes, N = 8 queries, K = 4 basis vectors.  Each warp owns
+// one query tile (its E fragments stay in registers) and runs two node tiles
+// as independent accumulator chains.
 // ---------------------------------------------------------------------------
 struct ProlongArgs {
     int64_t N;
@@ -152,37 +313,68 @@ struct ProlongArgs {
     const int* done;
 };
 
-__global__ void __launch_bounds__(kThreads) k_prolong(ProlongArgs a) {
-    if (a.done && *(volatile const int*)a.done) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-    const int64_t tw = (int64_t)gridDim.x * (kThreads / 32);
-    const int nbt = a.Bp >> 3, nk = a.npad >> 2;
-    const int64_t ntiles = ((a.N + 7) >> 3) * nbt;
-    for (int64_t idx = gw; idx < ntiles; idx += tw) {
-        const int64_t nt = idx / nbt;
-        const int bt = (int)(idx - nt * nbt);
-        const int64_t i0 = nt * 8;
-        double d0 = 0.0, d1 = 0.0;
-        const double* wrow = a.W + (i0 + (lane >> 2)) * a.npad + (lane & 3);
-        const double* ecol = a.E + (lane & 3) * a.Bp + bt * 8 + (lane >> 2);
-#pragma unroll 4
-        for (int kk = 0; kk < nk; ++kk)
-            dmma_8x8x4(d0, d1, __ldg(wrow + kk * 4), __ldg(ecol + (int64_t)kk * 4 * a.Bp));
-        const int64_t i = i0 + (lane >> 2);
-        const int b = bt * 8 + 2 * (lane & 3);
-        if (i < a.N) {
-            double* y = a.Y + i * a.Bp + b;
-            if (a.active[b]) y[0] = a.accumulate ? y[0] + d0 : d0;
-            if (a.active[b + 1]) y[1] = a.accumulate ? y[1] + d1 : d1;
+__device__ __forceinline__ void prolong_store(const ProlongArgs& a, int64_t i, int b, double d0,
+                                              double d1, bool act0, bool act1) {
+    if (i >= a.N) return;
+    double* y = a.Y + i * a.Bp + b;
+    if (act0 && act1) {
+        double2 v = make_double2(d0, d1);
+        if (a.accumulate) {
+            const double2 o = *reinterpret_cast<const double2*>(y);
+            v.x += o.x;
+            v.y += o.y;
         }
+        *reinterpret_cast<double2*>(y) = v;
+    } else {
+        if (act0) y[0] = a.accumulate ? y[0] + d0 : d0;
+        if (act1) y[1] = a.accumulate ? y[1] + d1 : d1;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_prolong(ProlongArgs a) {
+    if (a.done && ld_flag(a.done)) return;
+    const int lane = threadIdx.x & 31;
+    const int nbt = a.Bp >> 3, nk = a.npad >> 2;
+    const int64_t gw = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const int64_t tw = (int64_t)gridDim.x * (kThreads / 32);   // multiple of nbt (nbt | 8)
+    const int bt = (int)(gw % nbt);
+    const int64_t ts = tw / nbt;
+    const int64_t ntile = (a.N + 7) >> 3;
+    double ef[16];
+    const double* ecol = a.E + (lane & 3) * a.Bp + bt * 8 + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) ef[kk] = kk < nk ? __ldg(ecol + (int64_t)kk * 4 * a.Bp) : 0.0;
+    const int b = bt * 8 + 2 * (lane & 3);
+    const bool act0 = a.active[b] != 0, act1 = a.active[b + 1] != 0;
+    for (int64_t nt = gw / nbt; nt < ntile; nt += 2 * ts) {
+        const int64_t nt2 = nt + ts;
+        const bool two = nt2 < ntile;
+        const double* wA = a.W + (nt * 8 + (lane >> 2)) * a.npad + (lane & 3);
+        const double* wB = a.W + ((two ? nt2 : nt) * 8 + (lane >> 2)) * a.npad + (lane & 3);
+        double xa[16], xb[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+            if (kk < nk) {
+                xa[kk] = __ldg(wA + kk * 4);
+                xb[kk] = __ldg(wB + kk * 4);
+            }
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+            if (kk < nk) {
+                dmma_8x8x4(a0, a1, xa[kk], ef[kk]);
+                dmma_8x8x4(b0, b1, xb[kk], ef[kk]);
+            }
+        prolong_store(a, nt * 8 + (lane >> 2), b, a0, a1, act0, act1);
+        if (two) prolong_store(a, nt2 * 8 + (lane >> 2), b, b0, b1, act0, act1);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Red-black Gauss-Seidel half-sweep of `color` (AMB-5; eq8)
-// on A y = rhs, in place.  color < 0: no update.  LAST: also partials of
-// y^T rhs and y^T y per query (RBCG Step 10 / AMB-11).
+// on A y = rhs, in place.  color < 0: no update.  LAST: also y^T rhs and
+// y^T y per query; the last CTA then does RBCG Step 10:
+// rho' = y^T r, PRECOND check (AMB-11), beta = rho'/rho (init: rho_0, beta 0).
 // Flat thread-per-element mapping (e = i*Bp + b), Bp a power of two.
 // ---------------------------------------------------------------------------
 struct GSArgs {
@@ -195,68 +387,114 @@ struct GSArgs {
     const double* Rhs;        // or nullptr -> rconst
     double rconst;
     int color;
-    double* part;             // [Bp][2][nctf]
-    int nctf;
+    int init;                 // LAST: 1 = rho_0 (RBCG Step 2-3)
+    SolveState s;             // LAST: partials + bookkeeping
     const int* done;
 };
 
+constexpr int kGsUnroll = 4;
+
 template <int DIM, bool LAST>
-__global__ void __launch_bounds__(kThreads) k_gs(GSArgs a) {
-    if (a.done && *(volatile const int*)a.done) return;
+__global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
+    if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
     double* s_th = smem;
     int* s_act = (int*)(s_th + a.g.Q * a.Bp);
-    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kThreads) s_th[t] = a.theta[t];
-    for (int t = threadIdx.x; t < a.Bp; t += kThreads) s_act[t] = a.active[t];
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kFlat) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kFlat) s_act[t] = a.active[t];
     __syncthreads();
     double yr = 0.0, yy = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
-    const int b = (int)((blockIdx.x * (int64_t)kThreads + threadIdx.x) & (a.Bp - 1));
-    const bool act = s_act[b] != 0;
-    if (act) {
-        for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < a.NB; e += stride) {
-            const int64_t i = e >> a.lgB;
-            int I, J, K;
-            node_coords(a.g, (uint32_t)i, I, J, K);
-            const int par = (I + J + (DIM == 3 ? K : 0)) & 1;
-            const double rhs = a.Rhs ? a.Rhs[e] : a.rconst;
-            double y;
-            if (par == a.color) {
-                double k[2 * DIM], nb[2 * DIM];
-                node_kappa<DIM>(a.g, s_th, a.Bp, b, I, J, K, k);
-                node_nbrs<DIM>(a.g, a.Y, a.Bp, i, b, I, J, K, nb);
-                y = gs_value<DIM>(a.g, k, rhs, nb);
-                a.Y[e] = y;
-            } else if (LAST) {
-                y = a.Y[e];
+    const int64_t stride = (int64_t)gridDim.x * kFlat;
+    const int b = threadIdx.x & (a.Bp - 1);
+    if (s_act[b]) {
+        for (int64_t e0 = blockIdx.x * (int64_t)kFlat + threadIdx.x; e0 < a.NB;
+             e0 += kGsUnroll * stride) {
+            double nb[kGsUnroll][2 * DIM], rhs[kGsUnroll], yo[kGsUnroll];
+            int I[kGsUnroll], J[kGsUnroll], K[kGsUnroll];
+            bool upd[kGsUnroll], ok[kGsUnroll];
+#pragma unroll
+            for (int u = 0; u < kGsUnroll; ++u) {
+                const int64_t e = e0 + u * stride;
+                ok[u] = e < a.NB;
+                upd[u] = false;
+                rhs[u] = a.rconst;
+                yo[u] = 0.0;
+                if (ok[u]) {
+                    const int64_t i = e >> a.lgB;
+                    node_coords(a.g, (uint32_t)i, I[u], J[u], K[u]);
+                    upd[u] = ((I[u] + J[u] + (DIM == 3 ? K[u] : 0)) & 1) == a.color;
+                    if (a.Rhs && (upd[u] || LAST)) rhs[u] = __ldg(a.Rhs + e);
+                    if (upd[u]) node_nbrs<DIM>(a.g, a.Y, a.Bp, i, b, I[u], J[u], K[u], nb[u]);
+                    else if (LAST) yo[u] = a.Y[e];
+                }
             }
-            if (LAST) {
-                yr = fma(y, rhs, yr);
-                yy = fma(y, y, yy);
+#pragma unroll
+            for (int u = 0; u < kGsUnroll; ++u) {
+                if (upd[u]) {
+                    double k[2 * DIM];
+                    node_kappa<DIM>(a.g, s_th, a.Bp, b, I[u], J[u], K[u], k);
+                    yo[u] = gs_value<DIM>(a.g, k, rhs[u], nb[u]);
+                    a.Y[e0 + u * stride] = yo[u];
+                }
+                if (LAST && ok[u]) {
+                    yr = fma(yo[u], rhs[u], yr);
+                    yy = fma(yo[u], yo[u], yy);
+                }
             }
         }
     }
     if (LAST) {
-        __shared__ double s_yr[kThreads], s_yy[kThreads];
-        s_yr[threadIdx.x] = yr;
-        s_yy[threadIdx.x] = yy;
+        __shared__ double s_a[kFlat], s_b[kFlat];
+        __shared__ double s_yr[kMaxBatch], s_yy[kMaxBatch];
+        __shared__ int s_last;
+        SolveState& s = a.s;
+        s_a[threadIdx.x] = yr;
+        s_b[threadIdx.x] = yy;
         __syncthreads();
         if (threadIdx.x < a.Bp) {
             double sr = 0.0, sy = 0.0;
-            for (int t = threadIdx.x; t < kThreads; t += a.Bp) {
-                sr += s_yr[t];
-                sy += s_yy[t];
+            for (int t = threadIdx.x; t < kFlat; t += a.Bp) {
+                sr += s_a[t];
+                sy += s_b[t];
             }
-            a.part[((int64_t)threadIdx.x * 2 + 0) * a.nctf + blockIdx.x] = sr;
-            a.part[((int64_t)threadIdx.x * 2 + 1) * a.nctf + blockIdx.x] = sy;
+            s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + blockIdx.x] = sr;
+            s.partF[((int64_t)threadIdx.x * 2 + 1) * s.nctf + blockIdx.x] = sy;
+        }
+        if (cta_is_last(s.ticket, &s_last)) {
+            cta_sum_slot(s, 0, s_a, s_yr);
+            cta_sum_slot(s, 1, s_a, s_yy);
+            if (threadIdx.x < s.Bp) {
+                const int bb = threadIdx.x;
+                if (s.active[bb]) {
+                    const double r1 = s_yr[bb], y2 = s_yy[bb];
+                    if (!(r1 > s.delta * sqrt(y2) * sqrt(s.rr[bb]))) {
+                        s.status[bb] = isfinite(r1) ? Q_PRECOND : Q_NONFINITE;
+                        s.active[bb] = 0;
+                        s.beta[bb] = 0.0;
+                    } else {
+                        s.beta[bb] = a.init ? 0.0 : r1 / s.rho[bb];
+                        s.rho[bb] = r1;
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                int any = 0;
+                for (int bb = 0; bb < s.Bp; ++bb) any |= ((volatile int*)s.active)[bb];
+                *(volatile int*)s.done = any ? 0 : 1;
+                if (!a.init) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
+            }
+            release_ticket(s.ticket);
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// RBCG Step 11 + Step 5 numerator:
+// RBCG Step 11 + Step 5:
 //   p_new = y + beta p_old (recomputed on the halo), q = A p_new,
-//   part[b][0][cta] = sum p_new q.   p is double-buffered.
+//   sigma partial = p_new^T q; the last CTA computes alpha = rho / sigma with
+//   the MAXIT / CURVATURE checks.  p is double-buffered.
 // ---------------------------------------------------------------------------
 struct CGPArgs {
     Geo g;
@@ -268,144 +506,117 @@ struct CGPArgs {
     const double* Y;
     const double* Pold;
     double* Pnew;
-    double* part;             // [Bp][2][nctf] (slot 0)
-    int nctf;
+    SolveState s;
     const int* done;
 };
 
+constexpr int kCgpUnroll = 2;
+
 template <int DIM>
-__global__ void __launch_bounds__(kThreads) k_cgp(CGPArgs a) {
-    if (a.done && *(volatile const int*)a.done) return;
+__global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
+    if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
     double* s_th = smem;
     int* s_act = (int*)(s_th + a.g.Q * a.Bp);
-    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kThreads) s_th[t] = a.theta[t];
-    for (int t = threadIdx.x; t < a.Bp; t += kThreads) s_act[t] = a.active[t];
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kFlat) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kFlat) s_act[t] = a.active[t];
     __syncthreads();
     double sig = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
-    const int b = (int)((blockIdx.x * (int64_t)kThreads + threadIdx.x) & (a.Bp - 1));
+    const int64_t stride = (int64_t)gridDim.x * kFlat;
+    const int b = threadIdx.x & (a.Bp - 1);
     if (s_act[b]) {
         const double bet = a.beta[b];
         const int64_t sy = (int64_t)a.g.m * a.Bp, sz = sy * a.g.m;
-        for (int64_t e = blockIdx.x * (int64_t)kThreads + threadIdx.x; e < a.NB; e += stride) {
-            const int64_t i = e >> a.lgB;
-            int I, J, K;
-            node_coords(a.g, (uint32_t)i, I, J, K);
-            double k[2 * DIM], nb[2 * DIM];
-            node_kappa<DIM>(a.g, s_th, a.Bp, b, I, J, K, k);
-            const double pp = fma(bet, __ldg(a.Pold + e), __ldg(a.Y + e));
-#define PNB(off) fma(bet, __ldg(a.Pold + e + (off)), __ldg(a.Y + e + (off)))
-            nb[0] = I > 1 ? PNB(-a.Bp) : 0.0;
-            nb[1] = I < a.g.m ? PNB(a.Bp) : 0.0;
-            nb[2] = J > 1 ? PNB(-sy) : 0.0;
-            nb[3] = J < a.g.m ? PNB(sy) : 0.0;
-            if (DIM == 3) {
-                nb[4] = K > 1 ? PNB(-sz) : 0.0;
-                nb[5] = K < a.g.m ? PNB(sz) : 0.0;
+        for (int64_t e0 = blockIdx.x * (int64_t)kFlat + threadIdx.x; e0 < a.NB;
+             e0 += kCgpUnroll * stride) {
+            double yv[kCgpUnroll][2 * DIM + 1], pv[kCgpUnroll][2 * DIM + 1];
+            int I[kCgpUnroll], J[kCgpUnroll], K[kCgpUnroll];
+            bool ok[kCgpUnroll];
+#pragma unroll
+            for (int u = 0; u < kCgpUnroll; ++u) {
+                const int64_t e = e0 + u * stride;
+                ok[u] = e < a.NB;
+                if (ok[u]) {
+                    const int64_t i = e >> a.lgB;
+                    node_coords(a.g, (uint32_t)i, I[u], J[u], K[u]);
+                    const int64_t off[6] = {-a.Bp, a.Bp, -sy, sy, -sz, sz};
+                    const bool in[6] = {I[u] > 1, I[u] < a.g.m, J[u] > 1, J[u] < a.g.m,
+                                        K[u] > 1, K[u] < a.g.m};
+                    yv[u][0] = __ldg(a.Y + e);
+                    pv[u][0] = __ldg(a.Pold + e);
+#pragma unroll
+                    for (int d = 0; d < 2 * DIM; ++d) {
+                        yv[u][d + 1] = in[d] ? __ldg(a.Y + e + off[d]) : 0.0;
+                        pv[u][d + 1] = in[d] ? __ldg(a.Pold + e + off[d]) : 0.0;
+                    }
+                }
             }
-#undef PNB
-            const double q = stencil_apply<DIM>(a.g, k, pp, nb);
-            a.Pnew[e] = pp;
-            sig = fma(pp, q, sig);
+#pragma unroll
+            for (int u = 0; u < kCgpUnroll; ++u)
+                if (ok[u]) {
+                    double k[2 * DIM], nb[2 * DIM];
+                    node_kappa<DIM>(a.g, s_th, a.Bp, b, I[u], J[u], K[u], k);
+                    const double pp = fma(bet, pv[u][0], yv[u][0]);
+#pragma unroll
+                    for (int d = 0; d < 2 * DIM; ++d) nb[d] = fma(bet, pv[u][d + 1], yv[u][d + 1]);
+                    const double q = stencil_apply<DIM>(a.g, k, pp, nb);
+                    a.Pnew[e0 + u * stride] = pp;
+                    sig = fma(pp, q, sig);
+                }
         }
     }
-    __shared__ double s_sig[kThreads];
-    s_sig[threadIdx.x] = sig;
+    __shared__ double s_a[kFlat];
+    __shared__ double s_sig[kMaxBatch];
+    __shared__ int s_last;
+    SolveState& s = a.s;
+    s_a[threadIdx.x] = sig;
     __syncthreads();
     if (threadIdx.x < a.Bp) {
-        double s = 0.0;
-        for (int t = threadIdx.x; t < kThreads; t += a.Bp) s += s_sig[t];
-        a.part[((int64_t)threadIdx.x * 2 + 0) * a.nctf + blockIdx.x] = s;
+        double t0 = 0.0;
+        for (int t = threadIdx.x; t < kFlat; t += a.Bp) t0 += s_a[t];
+        s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + blockIdx.x] = t0;
     }
-}
-
-// ---------------------------------------------------------------------------
-// Per-solve state shared by the bookkeeping kernels.
-// ---------------------------------------------------------------------------
-struct SolveState {
-    int B, Bp, n, npad, nct, nctf, maxit, method;
-    double tol, delta;
-    const double* ANq;        // [Q][npad][npad]
-    int Q;
-    double* theta;            // [Q][Bp]
-    double* fproj;            // [Bp][npad+1]: f_n and ||f||^2
-    double* L;                // [Bp][npad][npad]
-    double* E;                // [npad][Bp]
-    double* a_n;              // [Bp][npad]
-    double* partP;            // [Bp][npad+1][nct]
-    double* partF;            // [Bp][2][nctf]
-    double *alpha, *beta, *rho, *rr, *fnorm, *relres;
-    int *active, *status, *its, *pivot;
-    int* kcount;
-    int* done;
-    unsigned* ticket;
-    double* hist;             // [Bp][maxit+1] or nullptr
-};
-
-// deterministic warp sum of part[row][0..cnt)
-__device__ __forceinline__ double warp_sum_row(const double* p, int cnt, int lane) {
-    double s = 0.0;
-    for (int c = lane; c < cnt; c += 32) s += p[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
-}
-
-// triangular solves L L^T e = rhs by one warp; lane owns rows lane, lane+32.
-__device__ void warp_chol_solve(const double* L, int ld, int n, double* z0, double* z1, int lane) {
-    for (int i = 0; i < n; ++i) {
-        const int own = i & 31, slot = i >> 5;
-        const double mine = slot ? *z1 : *z0;
-        const double zi = __shfl_sync(0xffffffffu, mine, own) / L[i * ld + i];
-        if (lane == own) { if (slot) *z1 = zi; else *z0 = zi; }
-        if (lane > i && lane < n) *z0 -= L[lane * ld + i] * zi;
-        if (lane + 32 > i && lane + 32 < n) *z1 -= L[(lane + 32) * ld + i] * zi;
-    }
-    for (int i = n - 1; i >= 0; --i) {
-        const int own = i & 31, slot = i >> 5;
-        const double mine = slot ? *z1 : *z0;
-        const double ei = __shfl_sync(0xffffffffu, mine, own) / L[i * ld + i];
-        if (lane == own) { if (slot) *z1 = ei; else *z0 = ei; }
-        if (lane < i) *z0 -= L[i * ld + lane] * ei;
-        if (lane + 32 < i) *z1 -= L[i * ld + lane + 32] * ei;
-    }
-}
-
-__device__ __forceinline__ void last_block_update(SolveState& s, bool bump_k) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned t = atomicAdd(s.ticket, 1u);
-        if (t == gridDim.x - 1) {
-            __threadfence();
-            int any = 0;
-            for (int b = 0; b < s.Bp; ++b) any |= ((volatile int*)s.active)[b];
-            *(volatile int*)s.done = any ? 0 : 1;
-            if (bump_k) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
-            *(volatile unsigned*)s.ticket = 0u;
-            __threadfence();
+    if (cta_is_last(s.ticket, &s_last)) {
+        cta_sum_slot(s, 0, s_a, s_sig);
+        const int k = ld_flag(s.kcount);
+        if (threadIdx.x < s.Bp) {
+            const int bb = threadIdx.x;
+            double al = 0.0;
+            if (s.active[bb]) {
+                const double sg = s_sig[bb];
+                if (k >= s.maxit) { s.status[bb] = Q_MAXIT; s.its[bb] = k; s.active[bb] = 0; }
+                else if (!(sg > 0.0)) {
+                    s.status[bb] = isfinite(sg) ? Q_CURVATURE : Q_NONFINITE;
+                    s.its[bb] = k;
+                    s.active[bb] = 0;
+                } else al = s.rho[bb] / sg;
+            }
+            s.alpha[bb] = al;
         }
+        __syncthreads();
+        if (threadIdx.x == 0) __threadfence();
+        update_done(s);
+        release_ticket(s.ticket);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Stage 2 of W^T r / ||r||^2 + stop test + reduced solve (RBCG Steps 7-9,
-// RBI Steps 2-5).  One CTA per query.
+// RBI Steps 2-5).  One CTA per query; the factor is staged in shared memory.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_reduce_solve(SolveState s) {
-    if (*(volatile const int*)s.done) return;
+__global__ void __launch_bounds__(256) k_reduce_solve(SolveState s) {
+    if (ld_flag(s.done)) return;
     __shared__ double s_rn[kMaxN + 1];
     __shared__ double s_L[kMaxN * kMaxN];
-    __shared__ int s_go;
+    __shared__ int s_go, s_last;
     const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
     const int rows = s.npad + 1;
     const bool act = s.active[b] != 0;
     if (act) {
-        // stage the factor in shared memory while the partial sums stream in
         const double* Lg = s.L + (int64_t)b * s.npad * s.npad;
         for (int t = threadIdx.x; t < s.n * s.npad; t += blockDim.x) s_L[t] = Lg[t];
-        for (int r = warp; r <= s.n; r += 4) {
+        for (int r = warp; r <= s.n; r += nw) {
             const int j = r < s.n ? r : s.npad;
             const double v = warp_sum_row(s.partP + ((int64_t)b * rows + j) * s.nct, s.nct, lane);
             if (lane == 0) s_rn[j] = v;
@@ -414,7 +625,7 @@ __global__ void __launch_bounds__(128) k_reduce_solve(SolveState s) {
         if (threadIdx.x == 0) {
             const double rr2 = s_rn[s.npad];
             const double h = sqrt(rr2) / s.fnorm[b];
-            const int it = *(volatile int*)s.kcount + 1;
+            const int it = ld_flag(s.kcount) + 1;
             if (s.hist) s.hist[(int64_t)b * (s.maxit + 1) + it] = h;
             s.its[b] = it;
             s.relres[b] = h;
@@ -428,15 +639,22 @@ __global__ void __launch_bounds__(128) k_reduce_solve(SolveState s) {
         }
         __syncthreads();
         if (s_go && s.n > 0 && warp == 0) {
-            const double* L = s_L;
             double z0 = lane < s.n ? s_rn[lane] : 0.0;
             double z1 = lane + 32 < s.n ? s_rn[lane + 32] : 0.0;
-            warp_chol_solve(L, s.npad, s.n, &z0, &z1, lane);
+            warp_chol_solve(s_L, s.npad, s.n, &z0, &z1, lane);
             if (lane < s.n) s.E[lane * s.Bp + b] = z0;
             if (lane + 32 < s.n) s.E[(lane + 32) * s.Bp + b] = z1;
         }
     }
-    last_block_update(s, s.method == 0);
+    if (cta_is_last(s.ticket, &s_last)) {
+        if (threadIdx.x == 0) {
+            int any = 0;
+            for (int bb = 0; bb < s.Bp; ++bb) any |= ((volatile int*)s.active)[bb];
+            *(volatile int*)s.done = any ? 0 : 1;
+            if (s.method == 0) *(volatile int*)s.kcount = ld_flag(s.kcount) + 1;
+        }
+        release_ticket(s.ticket);
+    }
 }
 
 // generic stage 2: out[b][j] = sum_c part[b][j][c], j < rows (one CTA per b)
@@ -446,80 +664,6 @@ __global__ void __launch_bounds__(128) k_reduce_rows(const double* part, int row
     for (int j = warp; j < rows; j += 4) {
         const double v = warp_sum_row(part + ((int64_t)b * rows + j) * nct, nct, lane);
         if (lane == 0) out[(int64_t)b * rows + j] = v;
-    }
-}
-
-// 1-CTA sum of partF slot `slot` for every query; result in s_out[b]
-__device__ void block_sum_slot(const SolveState& s, int slot, double* s_buf, double* s_out) {
-    const int gsz = blockDim.x / s.Bp;
-    const int b = threadIdx.x / gsz, t = threadIdx.x - b * gsz;
-    double v = 0.0;
-    if (b < s.Bp)
-        for (int c = t; c < s.nctf; c += gsz) v += s.partF[((int64_t)b * 2 + slot) * s.nctf + c];
-    s_buf[threadIdx.x] = v;
-    __syncthreads();
-    if (t == 0 && b < s.Bp) {
-        double a = 0.0;
-        for (int u = 0; u < gsz; ++u) a += s_buf[b * gsz + u];
-        s_out[b] = a;
-    }
-    __syncthreads();
-}
-
-// RBCG Step 5: alpha = rho / p^T A p, MAXIT / CURVATURE checks.
-__global__ void __launch_bounds__(512) k_alpha(SolveState s) {
-    if (*(volatile const int*)s.done) return;
-    __shared__ double s_buf[512], s_sig[kMaxBatch];
-    block_sum_slot(s, 0, s_buf, s_sig);
-    const int k = *(volatile int*)s.kcount;
-    if (threadIdx.x < s.Bp) {
-        const int b = threadIdx.x;
-        double al = 0.0;
-        if (s.active[b]) {
-            const double sig = s_sig[b];
-            if (k >= s.maxit) { s.status[b] = Q_MAXIT; s.its[b] = k; s.active[b] = 0; }
-            else if (!(sig > 0.0)) {
-                s.status[b] = isfinite(sig) ? Q_CURVATURE : Q_NONFINITE;
-                s.its[b] = k;
-                s.active[b] = 0;
-            } else al = s.rho[b] / sig;
-        }
-        s.alpha[b] = al;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int any = 0;
-        for (int b = 0; b < s.Bp; ++b) any |= s.active[b];
-        *s.done = any ? 0 : 1;
-    }
-}
-
-// RBCG Step 10: beta = y^T r (new) / y^T r (old); PRECOND check.
-__global__ void __launch_bounds__(512) k_beta(SolveState s, int init) {
-    if (*(volatile const int*)s.done) return;
-    __shared__ double s_buf[512], s_yr[kMaxBatch], s_yy[kMaxBatch];
-    block_sum_slot(s, 0, s_buf, s_yr);
-    block_sum_slot(s, 1, s_buf, s_yy);
-    if (threadIdx.x < s.Bp) {
-        const int b = threadIdx.x;
-        if (s.active[b]) {
-            const double yr = s_yr[b], yy = s_yy[b];
-            if (!(yr > s.delta * sqrt(yy) * sqrt(s.rr[b]))) {
-                s.status[b] = isfinite(yr) ? Q_PRECOND : Q_NONFINITE;
-                s.active[b] = 0;
-                s.beta[b] = 0.0;
-            } else {
-                s.beta[b] = init ? 0.0 : yr / s.rho[b];
-                s.rho[b] = yr;
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int any = 0;
-        for (int b = 0; b < s.Bp; ++b) any |= s.active[b];
-        *s.done = any ? 0 : 1;
-        if (!init) *s.kcount = *s.kcount + 1;
     }
 }
 
