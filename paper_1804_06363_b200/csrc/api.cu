@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/rbs.h"
-#include "kernels.cuh"
+#include "march.cuh"
 
 using namespace rbs;
 
@@ -93,6 +93,21 @@ inline int flat_ctas(const Geo& g) {
     int64_t c = (g.N + 63) / 64;
     return (int)std::max<int64_t>(1, std::min<int64_t>(c, 296));
 }
+// strip partition of the 2D row-marching passes (march.cuh): ~one CTA per SM
+inline int march_tx(int Bp) { return Bp <= 32 ? 32 : 16; }
+inline MarchPart march_part(const Geo& g, int TX, int sms = 148) {
+    MarchPart p;
+    p.nsx = (g.m + TX - 1) / TX;
+    int nsy = std::max(1, sms / p.nsx);
+    p.rows_per_seg = std::max(8, (g.m + nsy - 1) / nsy);
+    p.nsy = (g.m + p.rows_per_seg - 1) / p.rows_per_seg;
+    return p;
+}
+// columns of the per-CTA partial buffers of the flat / march passes
+inline int part_ctas(const Geo& g) {
+    const MarchPart a = march_part(g, 32), b = march_part(g, 16);
+    return std::max(flat_ctas(g), std::max(a.nsx * a.nsy, b.nsx * b.nsy));
+}
 inline int grid_for(int64_t work, int per, int cap) {
     int64_t c = (work + per - 1) / per;
     return (int)std::max<int64_t>(1, std::min<int64_t>(c, cap));
@@ -139,6 +154,9 @@ void set_attrs() {
     cudaFuncSetAttribute(k_gs<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_gs<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_cgp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    // 227 KB per CTA in total: leave room for the kernels' static shared memory
+    cudaFuncSetAttribute(k_smooth_march<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(k_smooth_march<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_cgp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     g_attr_done = true;
 }
@@ -163,8 +181,8 @@ BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
 
 // solve workspace
 struct SolveLayout {
-    double *X, *R, *P0, *P1, *Y, *F, *Xout;
-    double *theta, *fproj, *L, *E, *a_n, *partP, *partF;
+    double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout;
+    double *theta, *fproj, *L, *Ainv, *E, *a_n, *partP, *partF;
     double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist;
     int *active, *status, *its, *pivot, *ints;
     size_t bytes;
@@ -172,11 +190,12 @@ struct SolveLayout {
 SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool rhs, void* base) {
     const int Bp = pow2_batch(B), npad = c->npad;
     const size_t vec = (size_t)c->N8 * Bp;
-    const int nct = proj_ctas(c->g), nctf = flat_ctas(c->g);
+    const int nct = proj_ctas(c->g), nctf = part_ctas(c->g);
     Carve cv(base);
     SolveLayout L{};
     const bool cg = o->method == RBS_RBCG;
     L.X = cv.take<double>(vec);
+    L.X2 = (!cg && c->g.dim == 2) ? cv.take<double>(vec) : nullptr;   // RBI ping-pong (march)
     L.R = cg ? cv.take<double>(vec) : nullptr;
     L.P0 = cg ? cv.take<double>(vec) : nullptr;
     L.P1 = cg ? cv.take<double>(vec) : nullptr;
@@ -186,6 +205,7 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.theta = cv.take<double>((size_t)c->g.Q * Bp);
     L.fproj = cv.take<double>((size_t)Bp * (npad + 1));
     L.L = cv.take<double>((size_t)Bp * npad * npad + 8);
+    L.Ainv = cv.take<double>((size_t)Bp * npad * npad + 8);
     L.E = cv.take<double>((size_t)std::max(npad, 8) * Bp);
     L.a_n = cv.take<double>((size_t)Bp * npad + 8);
     L.partP = cv.take<double>((size_t)Bp * (npad + 1) * nct);
@@ -552,6 +572,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         CK(cudaMemcpyAsync(L.fproj, fp.data(), fp.size() * 8, cudaMemcpyHostToDevice, st));
     }
     CK(cudaMemsetAsync(L.X, 0, vecN * 8, st));
+    if (L.X2) CK(cudaMemsetAsync(L.X2, 0, vecN * 8, st));
     if (cg) {
         CK(cudaMemsetAsync(L.P0, 0, vecN * 8, st));
         CK(cudaMemsetAsync(L.P1, 0, vecN * 8, st));
@@ -563,7 +584,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     SolveState S{};
     S.B = B; S.Bp = Bp; S.n = n; S.npad = npad; S.nct = nct; S.nctf = nctf;
     S.maxit = o->max_iter; S.method = cg ? 1 : 0; S.tol = o->tol; S.delta = o->delta;
-    S.ANq = ctx->dANq; S.Q = Q; S.theta = L.theta; S.fproj = L.fproj; S.L = L.L; S.E = L.E;
+    S.ANq = ctx->dANq; S.Q = Q; S.theta = L.theta; S.fproj = L.fproj; S.L = L.L; S.Ainv = L.Ainv; S.E = L.E;
     S.a_n = L.a_n; S.partP = L.partP; S.partF = L.partF; S.alpha = L.alpha; S.beta = L.beta;
     S.rho = L.rho; S.rr = L.rr; S.fnorm = L.fnorm; S.relres = L.relres; S.active = L.active;
     S.status = L.status; S.its = L.its; S.pivot = L.pivot; S.kcount = kcount; S.done = done;
@@ -632,11 +653,11 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         }
         return cnt;
     };
-    auto proj = [&](int mode, const double* P, bool use_active) {
+    auto proj = [&](int mode, const double* P, bool use_active, double* Xv = nullptr) {
         ProjArgs a{};
         a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
         a.W = ctx->Wi; a.theta = L.theta; a.active = use_active ? L.active : nullptr;
-        a.alpha = L.alpha; a.P = P; a.X = L.X; a.R = L.R; a.V = Fv; a.vconst = ctx->fconst;
+        a.alpha = L.alpha; a.P = P; a.X = Xv ? Xv : L.X; a.R = L.R; a.V = Fv; a.vconst = ctx->fconst;
         a.part = L.partP; a.done = use_active ? done : nullptr;
         pb(RBS_K_PROJ);
         if (mode == MODE_CG) launch_proj<MODE_CG>(g, nct, psm, st, a);
@@ -655,10 +676,37 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         return 1;
     };
 
+    // 2D: prolongation + all half-sweeps (+ y^T r) in one row-marching pass
+    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps;
+    auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
+                     int init) {
+        SmoothMarchArgs a{};
+        const int TX = march_tx(Bp);
+        a.g = g; a.Bp = Bp; a.npad = npad; a.part = march_part(g, TX, ctx->num_sms);
+        a.W = ctx->Wi; a.E = L.E; a.Xold = Xold; a.Rhs = rhs; a.rconst = rconst; a.Y = Yv;
+        a.theta = L.theta; a.active = L.active; a.S = (int)seq.size();
+        for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
+        a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
+        const int grid = a.part.nsx * a.part.nsy;
+        pb(RBS_K_GS);
+        if (TX == 32) {
+            SmoothSmem<32> sl(Bp, npad, Q, a.S, rhs != nullptr, Xold != nullptr);
+            k_smooth_march<32><<<grid, kMarchThreads, sl.total, st>>>(a);
+        } else {
+            SmoothSmem<16> sl(Bp, npad, Q, a.S, rhs != nullptr, Xold != nullptr);
+            k_smooth_march<16><<<grid, kMarchThreads, sl.total, st>>>(a);
+        }
+        pe();
+        return 1;
+    };
+
     // ---- RBCG Step 2-3: y_0 = RBI(A, r_0, W, 1), rho_0 = r_0^T y_0 ------------
     if (cg) {
-        launches += prolong(L.Y, 0);
-        launches += smooth(L.Y, L.R, 0.0, true, 1);            // + rho_0, PRECOND check
+        if (use_march) launches += march(nullptr, L.Y, L.R, 0.0, true, 1);   // + rho_0, PRECOND
+        else {
+            launches += prolong(L.Y, 0);
+            launches += smooth(L.Y, L.R, 0.0, true, 1);
+        }
         CKL();
     } else {
         k_update_done<<<1, 1, 0, st>>>(L.active, Bp, done);
@@ -675,14 +723,24 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             double* Pnew = (it & 1) ? L.P0 : L.P1;
             c += cgp(Pold, Pnew);             // Step 11 (prev) + A p, Step 5 (alpha) in last CTA
             c += proj(MODE_CG, Pnew, true);   // Steps 6-7, ||r||, W^T r
-            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 256, 0, st>>>(S); pe(); ++c;  // Step 8
-            c += prolong(L.Y, 0);             // Step 9: y0 = W e
-            c += smooth(L.Y, L.R, 0.0, true, 0);  // y = S(A, r, y0); Step 10 in last CTA
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Step 8
+            if (use_march) {
+                c += march(nullptr, L.Y, L.R, 0.0, true, 0);   // Step 9 + Step 10 (last CTA)
+            } else {
+                c += prolong(L.Y, 0);             // Step 9: y0 = W e
+                c += smooth(L.Y, L.R, 0.0, true, 0);  // y = S(A, r, y0); Step 10 in last CTA
+            }
+        } else if (use_march) {
+            double* Xi = (it & 1) ? L.X2 : L.X;     // ping-pong: the march reads halos of x_old
+            double* Xo = (it & 1) ? L.X : L.X2;
+            c += march(Xi, Xo, Fv, ctx->fconst, false, 0);      // Steps 6-7
+            c += proj(MODE_RESID, nullptr, true, Xo);           // Steps 2, 4
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
         } else {
             c += prolong(L.X, 1);                               // Step 6
             c += smooth(L.X, Fv, ctx->fconst, false, 0);        // Step 7
             c += proj(MODE_RESID, nullptr, true);               // Steps 2, 4
-            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, 256, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
+            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
         }
         return c;
     };
@@ -778,7 +836,14 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     }
     // X: [N8][Bp] -> [B][N]
     double* xdst = o->x_location == RBS_MEM_HOST ? L.Xout : X;
-    k_transpose_out<<<(unsigned)((g.N + 31) / 32), 256, 0, st>>>(L.X, g.N, Bp, B, xdst);
+    const double* Xfin = L.X;
+    if (L.X2) {  // RBI ping-pong: corrections applied so far decide the buffer
+        int kc = 0;
+        CK(cudaMemcpyAsync(&kc, kcount, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        Xfin = (kc & 1) ? L.X2 : L.X;
+    }
+    k_transpose_out<<<(unsigned)((g.N + 31) / 32), 256, 0, st>>>(Xfin, g.N, Bp, B, xdst);
     ++launches;
     CKL();
     if (o->x_location == RBS_MEM_HOST)

@@ -34,6 +34,7 @@ struct SolveState {
     double* theta;            // [Q][Bp]
     double* fproj;            // [Bp][npad+1]: f_n and ||f||^2
     double* L;                // [Bp][npad][npad]
+    double* Ainv;             // [Bp][npad][npad]: A_n(mu)^{-1} ("invert the RB matrix")
     double* E;                // [npad][Bp]
     double* a_n;              // [Bp][npad]
     double* partP;            // [Bp][npad+1][nct]
@@ -106,27 +107,32 @@ __device__ __forceinline__ void release_ticket(unsigned* ticket) {
     }
 }
 
+// any query still active?  (whole CTA; one load per thread, no serial chain)
+__device__ __forceinline__ int cta_any_active(const SolveState& s) {
+    const int v = (int)threadIdx.x < s.Bp ? __ldcg(s.active + threadIdx.x) : 0;
+    return __syncthreads_or(v);
+}
+
 __device__ __forceinline__ void update_done(const SolveState& s) {
-    if (threadIdx.x == 0) {
-        int any = 0;
-        for (int b = 0; b < s.Bp; ++b) any |= ((volatile int*)s.active)[b];
-        *(volatile int*)s.done = any ? 0 : 1;
-    }
+    const int any = cta_any_active(s);
+    if (threadIdx.x == 0) *(volatile int*)s.done = any ? 0 : 1;
 }
 
 // sum over the CTAs' partials part[(b*2+slot)*nctf + c] for every query b;
 // result in s_out[b].  Whole CTA participates (blockDim.x multiple of Bp).
+// (the producing kernel's own CTAs: gridDim.x columns, row stride s.nctf)
 __device__ void cta_sum_slot(const SolveState& s, int slot, double* s_buf, double* s_out) {
     const int gsz = blockDim.x / s.Bp;
     const int b = threadIdx.x / gsz, t = threadIdx.x - b * gsz;
+    const int cnt = gridDim.x;
     double v0 = 0.0, v1 = 0.0;
     const double* p = s.partF + ((int64_t)b * 2 + slot) * s.nctf;
     int c = t;
-    for (; c + gsz < s.nctf; c += 2 * gsz) {
+    for (; c + gsz < cnt; c += 2 * gsz) {
         v0 += __ldcg(p + c);
         v1 += __ldcg(p + c + gsz);
     }
-    if (c < s.nctf) v0 += __ldcg(p + c);
+    if (c < cnt) v0 += __ldcg(p + c);
     s_buf[threadIdx.x] = v0 + v1;
     __syncthreads();
     if (t == 0) {
@@ -477,11 +483,9 @@ __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
                     }
                 }
             }
-            __syncthreads();
+            __threadfence();
+            const int any = cta_any_active(s);
             if (threadIdx.x == 0) {
-                __threadfence();
-                int any = 0;
-                for (int bb = 0; bb < s.Bp; ++bb) any |= ((volatile int*)s.active)[bb];
                 *(volatile int*)s.done = any ? 0 : 1;
                 if (!a.init) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
             }
@@ -593,8 +597,7 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
             }
             s.alpha[bb] = al;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) __threadfence();
+        __threadfence();
         update_done(s);
         release_ticket(s.ticket);
     }
@@ -602,27 +605,49 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
 
 // ---------------------------------------------------------------------------
 // Stage 2 of W^T r / ||r||^2 + stop test + reduced solve (RBCG Steps 7-9,
-// RBI Steps 2-5).  One CTA per query; the factor is staged in shared memory.
+// RBI Steps 2-5).  One CTA per query.  All partial loads are issued at once
+// (each thread sums a fixed chunk of one row, then the chunks are combined in
+// a fixed order); the reduced solve e = A_n(mu)^{-1} r_n is a matvec with the
+// inverse formed once per query at setup.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_reduce_solve(SolveState s) {
+constexpr int kRsThreads = 512;
+constexpr int kRsChunks = 8;      // chunks per row (rows <= 65 -> 520 > 512 handled by loop)
+
+__global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
     if (ld_flag(s.done)) return;
     __shared__ double s_rn[kMaxN + 1];
-    __shared__ double s_L[kMaxN * kMaxN];
+    __shared__ double s_chunk[(kMaxN + 1) * kRsChunks];
+    __shared__ double s_e[kMaxN * 8];
     __shared__ int s_go, s_last;
-    const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    const int rows = s.npad + 1;
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int rows = s.npad + 1, nr = s.n + 1;     // rows 0..n-1 and the rr row (npad)
     const bool act = s.active[b] != 0;
     if (act) {
-        const double* Lg = s.L + (int64_t)b * s.npad * s.npad;
-        for (int t = threadIdx.x; t < s.n * s.npad; t += blockDim.x) s_L[t] = Lg[t];
-        for (int r = warp; r <= s.n; r += nw) {
+        const int per = (s.nct + kRsChunks - 1) / kRsChunks;
+        for (int t = tid; t < nr * kRsChunks; t += kRsThreads) {
+            const int r = t / kRsChunks, c = t - r * kRsChunks;
             const int j = r < s.n ? r : s.npad;
-            const double v = warp_sum_row(s.partP + ((int64_t)b * rows + j) * s.nct, s.nct, lane);
-            if (lane == 0) s_rn[j] = v;
+            const double* p = s.partP + ((int64_t)b * rows + j) * s.nct;
+            const int c0 = c * per, c1 = min(s.nct, c0 + per);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int k = c0;
+            for (; k + 3 < c1; k += 4) {
+                a0 += __ldcg(p + k);
+                a1 += __ldcg(p + k + 1);
+                a2 += __ldcg(p + k + 2);
+                a3 += __ldcg(p + k + 3);
+            }
+            for (; k < c1; ++k) a0 += __ldcg(p + k);
+            s_chunk[r * kRsChunks + c] = (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid < nr) {
+            double v = 0.0;
+            for (int c = 0; c < kRsChunks; ++c) v += s_chunk[tid * kRsChunks + c];
+            s_rn[tid < s.n ? tid : s.npad] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
             const double rr2 = s_rn[s.npad];
             const double h = sqrt(rr2) / s.fnorm[b];
             const int it = ld_flag(s.kcount) + 1;
@@ -638,18 +663,25 @@ __global__ void __launch_bounds__(256) k_reduce_solve(SolveState s) {
             s_go = go;
         }
         __syncthreads();
-        if (s_go && s.n > 0 && warp == 0) {
-            double z0 = lane < s.n ? s_rn[lane] : 0.0;
-            double z1 = lane + 32 < s.n ? s_rn[lane + 32] : 0.0;
-            warp_chol_solve(s_L, s.npad, s.n, &z0, &z1, lane);
-            if (lane < s.n) s.E[lane * s.Bp + b] = z0;
-            if (lane + 32 < s.n) s.E[(lane + 32) * s.Bp + b] = z1;
+        // e = A_n^{-1} r_n: row i by 8 threads (fixed order), frozen lanes get e = 0
+        const double* Ai = s.Ainv + (int64_t)b * s.npad * s.npad;
+        for (int t = tid; t < s.n * 8; t += kRsThreads) {
+            const int i = t >> 3, l = t & 7;
+            double v = 0.0;
+            if (s_go)
+                for (int j = l; j < s.n; j += 8) v = fma(Ai[i * s.npad + j], s_rn[j], v);
+            s_e[t] = v;
+        }
+        __syncthreads();
+        if (tid < s.n) {
+            double v = 0.0;
+            for (int l = 0; l < 8; ++l) v += s_e[tid * 8 + l];
+            s.E[tid * s.Bp + b] = v;
         }
     }
     if (cta_is_last(s.ticket, &s_last)) {
+        const int any = cta_any_active(s);
         if (threadIdx.x == 0) {
-            int any = 0;
-            for (int bb = 0; bb < s.Bp; ++bb) any |= ((volatile int*)s.active)[bb];
             *(volatile int*)s.done = any ? 0 : 1;
             if (s.method == 0) *(volatile int*)s.kcount = ld_flag(s.kcount) + 1;
         }
@@ -735,6 +767,27 @@ __global__ void __launch_bounds__(128) k_setup_reduced(SolveState s, int rbi) {
         s.status[b] = st;
     }
     __syncthreads();
+    // A_n^{-1} = L^{-T} L^{-1}: thread j solves column j (L z = e_j, L^T x = z)
+    if (s_fail < 0 && s.Ainv) {
+        double* Ai = s.Ainv + (int64_t)b * ld * ld;
+        for (int j = tid; j < ld; j += blockDim.x) {
+            if (j >= n) {
+                for (int i = 0; i < ld; ++i) Ai[i * ld + j] = 0.0;
+                continue;
+            }
+            for (int i = 0; i < n; ++i) {
+                double v = (i == j) ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) v -= sA[i * ld + k] * Ai[k * ld + j];
+                Ai[i * ld + j] = i < j ? 0.0 : v / sA[i * ld + i];
+            }
+            for (int i = n - 1; i >= 0; --i) {
+                double v = Ai[i * ld + j];
+                for (int k = i + 1; k < n; ++k) v -= sA[k * ld + i] * Ai[k * ld + j];
+                Ai[i * ld + j] = v / sA[i * ld + i];
+            }
+            for (int i = n; i < ld; ++i) Ai[i * ld + j] = 0.0;
+        }
+    }
     if (s_fail < 0 && n > 0 && tid < 32) {
         // sA holds the factor in its lower triangle (only that part is read)
         const double* fn = s.fproj + (int64_t)b * (ld + 1);

@@ -78,6 +78,20 @@ __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int l
                                            int I, int J, int K, double* k) {
     const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
     const int by0 = axis_block(g, J - 1, g.py) * g.px, by1 = axis_block(g, J, g.py) * g.px;
+    int bz0 = 0, bz1 = 0;
+    if (DIM == 3) {
+        const int pxy = g.px * g.py;
+        bz0 = axis_block(g, K - 1, g.pz) * pxy;
+        bz1 = axis_block(g, K, g.pz) * pxy;
+    }
+    if (bx0 == bx1 && by0 == by1 && bz0 == bz1) {
+        // all cells around the node in one block: 0.5*(c+c) = 0.25*((c+c)+(c+c)) = c
+        // exactly, so this is bitwise the general formula with one load
+        const double c = th[(bx0 + by0 + bz0) * ldb + b];
+#pragma unroll
+        for (int e = 0; e < 2 * DIM; ++e) k[e] = c;
+        return;
+    }
     if (DIM == 2) {
         const double c00 = th[(bx0 + by0) * ldb + b], c10 = th[(bx1 + by0) * ldb + b];
         const double c01 = th[(bx0 + by1) * ldb + b], c11 = th[(bx1 + by1) * ldb + b];
@@ -86,8 +100,6 @@ __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int l
         k[2] = 0.5 * (c00 + c10);
         k[3] = 0.5 * (c01 + c11);
     } else {
-        const int pxy = g.px * g.py;
-        const int bz0 = axis_block(g, K - 1, g.pz) * pxy, bz1 = axis_block(g, K, g.pz) * pxy;
         // c[dx][dy][dz] = theta of cell (I-1+dx, J-1+dy, K-1+dz)
         const double c000 = th[(bx0 + by0 + bz0) * ldb + b], c100 = th[(bx1 + by0 + bz0) * ldb + b];
         const double c010 = th[(bx0 + by1 + bz0) * ldb + b], c110 = th[(bx1 + by1 + bz0) * ldb + b];
