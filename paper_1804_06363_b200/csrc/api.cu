@@ -31,8 +31,8 @@ struct rbs_ctx {
     double fconst = 1.0;
     // basis
     bool has_basis = false;
-    int n = 0, npad = 0;
-    double* Wi = nullptr;    // [N8][npad]
+    int n = 0, npad = 0, ldw = 4;   // ldw = npad + 4: row stride of the packed W
+    double* Wi = nullptr;    // [N8][ldw]
     double* dANq = nullptr;  // [Q][npad][npad]
     double* scratch = nullptr;
     std::vector<double> hANq, hfn;  // Q*n*n, n (fn = W^T 1)
@@ -72,6 +72,9 @@ rbs_status fail(rbs_ctx* c, rbs_status s, const std::string& msg) {
     } while (0)
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+// packed W row stride: npad + 4 doubles = 2(npad+4) words = 8 or 24 mod 32, so the
+// 4-row DMMA fragment reads of a half-warp hit distinct shared-memory banks
+inline int w_ld(int npad) { return npad + 4; }
 inline int pow2_batch(int B) {
     int p = 8;
     while (p < B) p <<= 1;
@@ -157,6 +160,8 @@ void set_attrs() {
     // 227 KB per CTA in total: leave room for the kernels' static shared memory
     cudaFuncSetAttribute(k_smooth_march<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_smooth_march<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(k_resid_march<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(k_resid_march<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_cgp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     g_attr_done = true;
 }
@@ -170,7 +175,7 @@ BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
     const int npad = (int)round_up(n, 8);
     Carve cv(base);
     BasisLayout L;
-    L.Wi = cv.take<double>((size_t)c->N8 * std::max(npad, 8));
+    L.Wi = cv.take<double>((size_t)c->N8 * w_ld(npad));
     L.ANq = cv.take<double>((size_t)c->g.Q * npad * npad + 8);
     L.Z = cv.take<double>((size_t)c->N8 * 8);
     L.part = cv.take<double>((size_t)8 * (npad + 1) * proj_ctas(c->g));
@@ -208,7 +213,8 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.Ainv = cv.take<double>((size_t)Bp * npad * npad + 8);
     L.E = cv.take<double>((size_t)std::max(npad, 8) * Bp);
     L.a_n = cv.take<double>((size_t)Bp * npad + 8);
-    L.partP = cv.take<double>((size_t)Bp * (npad + 1) * nct);
+    const MarchPart rp = march_part(c->g, kRmTX);
+    L.partP = cv.take<double>((size_t)Bp * (npad + 1) * std::max(nct, rp.nsx * rp.nsy));
     L.partF = cv.take<double>((size_t)Bp * 2 * nctf);
     L.alpha = cv.take<double>(Bp);
     L.beta = cv.take<double>(Bp);
@@ -397,14 +403,15 @@ rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
     ctx->has_basis = false;
     ctx->n = n;
     ctx->npad = npad;
+    ctx->ldw = w_ld(npad);
     ctx->Wi = L.Wi;
     ctx->dANq = L.ANq;
     ctx->scratch = L.Z;
     if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
     const int Q = g.Q;
     if (n > 0) {
-        k_pack_W<<<grid_for(ctx->N8 * npad, 256, 4 * ctx->num_sms * 8), 256, 0, st>>>(
-            W_dev, ldw, g.N, ctx->N8, n, npad, L.Wi);
+        k_pack_W<<<grid_for(ctx->N8 * ctx->ldw, 256, 4 * ctx->num_sms * 8), 256, 0, st>>>(
+            W_dev, ldw, g.N, ctx->N8, n, ctx->ldw, L.Wi);
         CKL();
     }
     ctx->hANq.assign((size_t)Q * n * n, 0.0);
@@ -419,11 +426,11 @@ rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
         for (int q = 0; q < Q; ++q)
             for (int j0 = 0; j0 < npad; j0 += 8) {
                 const int grid = grid_for(g.N * 8, kThreads, ctx->num_sms * 8);
-                if (g.dim == 2) k_apply_Aq<2><<<grid, kThreads, 0, st>>>(g, q, L.Wi, npad, j0, L.Z);
-                else k_apply_Aq<3><<<grid, kThreads, 0, st>>>(g, q, L.Wi, npad, j0, L.Z);
+                if (g.dim == 2) k_apply_Aq<2><<<grid, kThreads, 0, st>>>(g, q, L.Wi, ctx->ldw, j0, L.Z);
+                else k_apply_Aq<3><<<grid, kThreads, 0, st>>>(g, q, L.Wi, ctx->ldw, j0, L.Z);
                 CKL();
                 ProjArgs a{};
-                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ctx->ldw;
                 a.W = L.Wi; a.V = L.Z; a.part = L.part;
                 launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
                 CKL();
@@ -446,7 +453,7 @@ rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
     } else if (n > 0) {
         const int nct = proj_ctas(g);
         ProjArgs a{};
-        a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+        a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ctx->ldw;
         a.W = L.Wi; a.V = nullptr; a.vconst = 1.0; a.part = L.part;
         launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
         CKL();
@@ -522,8 +529,12 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     cudaStream_t st = (cudaStream_t)stream;
     const Geo& g = ctx->g;
     const int Bp = pow2_batch(B), lgB = ilog2(Bp), n = ctx->n, npad = ctx->npad, Q = g.Q;
-    const int nct = proj_ctas(g), nctf = flat_ctas(g);
     const bool cg = o->method == RBS_RBCG;
+    // 2D, B_pad <= 32: the projection pass is the row march (k_resid_march)
+    const bool use_rmarch = g.dim == 2 && Bp <= 32;
+    const MarchPart rpart = march_part(g, kRmTX, ctx->num_sms);
+    const int nct = use_rmarch ? rpart.nsx * rpart.nsy : proj_ctas(g), nctf = part_ctas(g);
+    const int nct_plain = proj_ctas(g);
     const int64_t vecN = ctx->N8 * Bp;
     const size_t psm = proj_smem(g, Bp, npad), fsm = flat_smem(g, Bp);
     int64_t launches = 0;
@@ -556,11 +567,11 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         ++launches;
         Fv = L.F;
         ProjArgs a{};
-        a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+        a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct_plain; a.ngroups = (g.N + 3) / 4; a.ldw = ctx->ldw;
         a.W = ctx->Wi; a.theta = L.theta; a.V = L.F; a.part = L.partP;
-        launch_proj<MODE_PLAIN>(g, nct, psm, st, a);
+        launch_proj<MODE_PLAIN>(g, nct_plain, psm, st, a);
         CKL();
-        k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct, L.fproj);
+        k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct_plain, L.fproj);
         CKL();
         launches += 2;
     } else {
@@ -616,7 +627,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     // ---- pass builders -------------------------------------------------------
     auto prolong = [&](double* Yv, int acc) {
         ProlongArgs a{};
-        a.N = g.N; a.Bp = Bp; a.npad = npad; a.W = ctx->Wi; a.E = L.E; a.active = L.active;
+        a.N = g.N; a.Bp = Bp; a.npad = npad; a.ldw = ctx->ldw; a.W = ctx->Wi; a.E = L.E; a.active = L.active;
         a.Y = Yv; a.accumulate = acc; a.done = done;
         pb(RBS_K_PROLONG);
         if (npad > 0) {
@@ -654,14 +665,28 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         return cnt;
     };
     auto proj = [&](int mode, const double* P, bool use_active, double* Xv = nullptr) {
+        if (use_rmarch && use_active) {
+            ResidMarchArgs r{};
+            r.g = g; r.Bp = Bp; r.npad = npad; r.ldw = ctx->ldw; r.mp = rpart; r.W = ctx->Wi;
+            r.theta = L.theta; r.active = L.active; r.alpha = L.alpha; r.P = P;
+            r.X = Xv ? Xv : L.X; r.R = L.R; r.V = Fv; r.vconst = ctx->fconst;
+            r.part = L.partP; r.nct = nct; r.done = done;
+            ResidSmem rs(Bp, ctx->ldw, Q, mode == MODE_CG ? 0 : 1, Fv != nullptr);
+            pb(RBS_K_PROJ);
+            if (mode == MODE_CG) k_resid_march<0><<<nct, kMarchThreads, rs.total, st>>>(r);
+            else k_resid_march<1><<<nct, kMarchThreads, rs.total, st>>>(r);
+            pe();
+            return 1;
+        }
         ProjArgs a{};
-        a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+        a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ctx->ldw;
         a.W = ctx->Wi; a.theta = L.theta; a.active = use_active ? L.active : nullptr;
         a.alpha = L.alpha; a.P = P; a.X = Xv ? Xv : L.X; a.R = L.R; a.V = Fv; a.vconst = ctx->fconst;
         a.part = L.partP; a.done = use_active ? done : nullptr;
+        a.nct = use_active ? nct : nct_plain;
         pb(RBS_K_PROJ);
-        if (mode == MODE_CG) launch_proj<MODE_CG>(g, nct, psm, st, a);
-        else launch_proj<MODE_RESID>(g, nct, psm, st, a);
+        if (mode == MODE_CG) launch_proj<MODE_CG>(g, a.nct, psm, st, a);
+        else launch_proj<MODE_RESID>(g, a.nct, psm, st, a);
         pe();
         return 1;
     };
@@ -682,7 +707,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
                      int init) {
         SmoothMarchArgs a{};
         const int TX = march_tx(Bp);
-        a.g = g; a.Bp = Bp; a.npad = npad; a.part = march_part(g, TX, ctx->num_sms);
+        a.g = g; a.Bp = Bp; a.npad = npad; a.ldw = ctx->ldw; a.part = march_part(g, TX, ctx->num_sms);
         a.W = ctx->Wi; a.E = L.E; a.Xold = Xold; a.Rhs = rhs; a.rconst = rconst; a.Y = Yv;
         a.theta = L.theta; a.active = L.active; a.S = (int)seq.size();
         for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
@@ -690,10 +715,10 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         const int grid = a.part.nsx * a.part.nsy;
         pb(RBS_K_GS);
         if (TX == 32) {
-            SmoothSmem<32> sl(Bp, npad, Q, a.S, rhs != nullptr, Xold != nullptr);
+            SmoothSmem<32> sl(Bp, npad, ctx->ldw, Q, a.S, rhs != nullptr, Xold != nullptr);
             k_smooth_march<32><<<grid, kMarchThreads, sl.total, st>>>(a);
         } else {
-            SmoothSmem<16> sl(Bp, npad, Q, a.S, rhs != nullptr, Xold != nullptr);
+            SmoothSmem<16> sl(Bp, npad, ctx->ldw, Q, a.S, rhs != nullptr, Xold != nullptr);
             k_smooth_march<16><<<grid, kMarchThreads, sl.total, st>>>(a);
         }
         pe();
@@ -823,7 +848,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         proj(MODE_RESID, nullptr, false);
         ++launches;
         // reuse npad rows: the rr row of the partials is row npad
-        k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct, L.fproj);
+        k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct_plain, L.fproj);
         ++launches;
         CKL();
         std::vector<double> rows((size_t)Bp * (npad + 1));

@@ -71,7 +71,7 @@ GreedyLayout greedy_layout(rbs_ctx* c, int nt, int n_max, void* base) {
     const int npad = (int)round_up(n_max, 8);
     Carve cv(base);
     GreedyLayout L{};
-    L.Wi = cv.take<double>((size_t)c->N8 * npad);
+    L.Wi = cv.take<double>((size_t)c->N8 * w_ld(npad));
     L.ANq = cv.take<double>((size_t)c->g.Q * npad * npad + 8);
     L.Z = cv.take<double>((size_t)c->N8 * 8);
     L.part = cv.take<double>((size_t)8 * (npad + 1) * proj_ctas(c->g));
@@ -90,6 +90,7 @@ GreedyLayout greedy_layout(rbs_ctx* c, int nt, int n_max, void* base) {
     // solve workspace for B = 1 RBCG snapshots with the full padded width
     rbs_ctx tmp = *c;
     tmp.npad = npad;
+    tmp.ldw = w_ld(npad);
     rbs_solve_opts o;
     rbs_default_opts(&o);
     L.solve_bytes = solve_layout(&tmp, 1, &o, false, nullptr).bytes;
@@ -127,11 +128,11 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
     const Geo& g = ctx->g;
-    const int Q = g.Q, P = Q, npad = (int)round_up(n_max, 8), nt = n_train;
+    const int Q = g.Q, P = Q, npad = (int)round_up(n_max, 8), nt = n_train, ldw = w_ld(npad);
     const int nct = proj_ctas(g);
     const int vgrid = grid_for(g.N, 256, ctx->num_sms * 8);
 
-    CK(cudaMemsetAsync(L.Wi, 0, (size_t)ctx->N8 * npad * 8, st));
+    CK(cudaMemsetAsync(L.Wi, 0, (size_t)ctx->N8 * ldw * 8, st));
     CK(cudaMemsetAsync(L.ANq, 0, ((size_t)Q * npad * npad + 8) * 8, st));
     CK(cudaMemsetAsync(L.x, 0, (size_t)ctx->N8 * 8, st));
     CK(cudaMemsetAsync(L.w, 0, (size_t)ctx->N8 * 8, st));
@@ -140,6 +141,7 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
     ctx->Wi = L.Wi;
     ctx->dANq = L.ANq;
     ctx->npad = npad;
+    ctx->ldw = ldw;
     ctx->n = 0;
     ctx->hANq.assign(0, 0.0);
     ctx->hfn.assign(0, 0.0);
@@ -198,8 +200,8 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
         dot(L.x, 1, L.x, 1, L.scal + 0);
         for (int pass = 0; pass < 2; ++pass)
             for (int j = 0; j < n; ++j) {
-                dot(L.Wi + j, npad, L.w, 1, L.scal + 2);
-                k_mgs_axpy<<<vgrid, 256, 0, st>>>(L.w, L.Wi + j, npad, L.scal + 2, g.N);
+                dot(L.Wi + j, ldw, L.w, 1, L.scal + 2);
+                k_mgs_axpy<<<vgrid, 256, 0, st>>>(L.w, L.Wi + j, ldw, L.scal + 2, g.N);
             }
         dot(L.w, 1, L.w, 1, L.scal + 1);
         CKL();
@@ -212,16 +214,16 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
         if (rejected) {
             ++rej;
         } else {
-            k_store_col<<<vgrid, 256, 0, st>>>(L.w, wn, L.Wi, npad, n, g.N);
+            k_store_col<<<vgrid, 256, 0, st>>>(L.w, wn, L.Wi, ldw, n, g.N);
             CKL();
             // ---- offline column n: (A_{N,q})_{i n} = w_i^T A_q w_n, i <= n --------
             const int j0 = (n / 8) * 8, jj = n - j0;
             for (int q = 0; q < Q; ++q) {
                 const int grid = grid_for(g.N * 8, kThreads, ctx->num_sms * 8);
-                if (g.dim == 2) k_apply_Aq<2><<<grid, kThreads, 0, st>>>(g, q, L.Wi, npad, j0, L.Z);
-                else k_apply_Aq<3><<<grid, kThreads, 0, st>>>(g, q, L.Wi, npad, j0, L.Z);
+                if (g.dim == 2) k_apply_Aq<2><<<grid, kThreads, 0, st>>>(g, q, L.Wi, ldw, j0, L.Z);
+                else k_apply_Aq<3><<<grid, kThreads, 0, st>>>(g, q, L.Wi, ldw, j0, L.Z);
                 ProjArgs a{};
-                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ldw;
                 a.W = L.Wi; a.V = L.Z; a.part = L.part;
                 launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
                 k_reduce_rows<<<8, 128, 0, st>>>(L.part, npad + 1, nct, L.rows);
@@ -237,7 +239,7 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
             }
             {   // f_{N,1}[n] = w_n^T 1
                 ProjArgs a{};
-                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+                a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ldw;
                 a.W = L.Wi; a.V = nullptr; a.vconst = 1.0; a.part = L.part;
                 launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
                 k_reduce_rows<<<1, 128, 0, st>>>(L.part, npad + 1, nct, L.rows);
@@ -294,7 +296,7 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
     *n_out = n;
     if (n_rejected) *n_rejected = rej;
     if (n > 0) {
-        k_unpack_W<<<grid_for(g.N * n, 256, ctx->num_sms * 8), 256, 0, st>>>(L.Wi, g.N, n, npad, W_out);
+        k_unpack_W<<<grid_for(g.N * n, 256, ctx->num_sms * 8), 256, 0, st>>>(L.Wi, g.N, n, ldw, W_out);
         CKL();
     }
     if (ANq_out)

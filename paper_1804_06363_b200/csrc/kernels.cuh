@@ -157,6 +157,7 @@ __device__ void cta_sum_slot(const SolveState& s, int slot, double* s_buf, doubl
 struct ProjArgs {
     Geo g;
     int Bp, npad, nct;
+    int ldw;                  // row stride of W (npad + 4: conflict-free DMMA fragments)
     int64_t ngroups;          // ceil(N/4)
     const double* W;          // [N8][npad]
     const double* theta;      // [Q][Bp]
@@ -257,8 +258,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
             proj_load<MODE, DIM>(a, s_th, b, iA, okA, nbA, a0, a1, a2, IA, JA, KA);
             proj_load<MODE, DIM>(a, s_th, b, iB, okB, nbB, b0, b1, b2, IB, JB, KB);
             double wA[8], wB[8];
-            const double* wrowA = a.W + iA * npad + (lane >> 2);
-            const double* wrowB = a.W + (gB < g1 ? iB : iA) * npad + (lane >> 2);
+            const double* wrowA = a.W + iA * a.ldw + (lane >> 2);
+            const double* wrowB = a.W + (gB < g1 ? iB : iA) * a.ldw + (lane >> 2);
 #pragma unroll
             for (int jt = 0; jt < 8; ++jt)
                 if (jt < ntile) {
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
 // ---------------------------------------------------------------------------
 struct ProlongArgs {
     int64_t N;
-    int Bp, npad;
+    int Bp, npad, ldw;
     const double* W;      // [N8][npad]
     const double* E;      // [npad][Bp]
     const int* active;    // [Bp]
@@ -355,8 +356,8 @@ __global__ void __launch_bounds__(kThreads) k_prolong(ProlongArgs a) {
     for (int64_t nt = gw / nbt; nt < ntile; nt += 2 * ts) {
         const int64_t nt2 = nt + ts;
         const bool two = nt2 < ntile;
-        const double* wA = a.W + (nt * 8 + (lane >> 2)) * a.npad + (lane & 3);
-        const double* wB = a.W + ((two ? nt2 : nt) * 8 + (lane >> 2)) * a.npad + (lane & 3);
+        const double* wA = a.W + (nt * 8 + (lane >> 2)) * a.ldw + (lane & 3);
+        const double* wB = a.W + ((two ? nt2 : nt) * 8 + (lane >> 2)) * a.ldw + (lane & 3);
         double xa[16], xb[16];
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
@@ -801,26 +802,26 @@ __global__ void __launch_bounds__(128) k_setup_reduced(SolveState s, int rbi) {
 // ---------------------------------------------------------------------------
 // layout / init helpers
 // ---------------------------------------------------------------------------
-// W column-major (ldw) -> node-major [N8][npad], zero padded
+// W column-major (ldw) -> node-major [N8][ldwi], zero padded
 __global__ void k_pack_W(const double* __restrict__ W, int64_t ldw, int64_t N, int64_t N8, int n,
-                         int npad, double* __restrict__ Wi) {
-    const int64_t tot = N8 * npad;
+                         int ldwi, double* __restrict__ Wi) {
+    const int64_t tot = N8 * ldwi;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / npad;
-        const int j = (int)(t - i * npad);
+        const int64_t i = t / ldwi;
+        const int j = (int)(t - i * ldwi);
         Wi[t] = (i < N && j < n) ? W[(int64_t)j * ldw + i] : 0.0;
     }
 }
 
-// node-major [N8][npad] -> column-major N x n
-__global__ void k_unpack_W(const double* __restrict__ Wi, int64_t N, int n, int npad,
+// node-major [N8][ldwi] -> column-major N x n
+__global__ void k_unpack_W(const double* __restrict__ Wi, int64_t N, int n, int ldwi,
                            double* __restrict__ W) {
     const int64_t tot = N * n;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = t / N, i = t - j * N;
-        W[t] = Wi[i * npad + j];
+        W[t] = Wi[i * ldwi + j];
     }
 }
 

@@ -71,7 +71,7 @@ struct MarchPart {
 
 struct SmoothMarchArgs {
     Geo g;
-    int Bp, npad;
+    int Bp, npad, ldw;
     MarchPart part;
     const double* W;          // [N8][npad]
     const double* E;          // [npad][Bp]
@@ -96,8 +96,8 @@ constexpr int kRows = 2;
 template <int TX>
 struct SmoothSmem {
     int TW, RY, RR, RW, tiles;
-    size_t yring, rring, wring, xring, es, th, bars, total;
-    __host__ __device__ SmoothSmem(int Bp, int npad, int Q, int S, bool has_rhs, bool acc) {
+    size_t yring, rring, wring, xring, es, cb, th, bars, total;
+    __host__ __device__ SmoothSmem(int Bp, int npad, int ldw, int Q, int S, bool has_rhs, bool acc) {
         TW = TX + 2 * S;
         tiles = (TW + 7) / 8;
         RY = kRows + S + 1;
@@ -107,9 +107,10 @@ struct SmoothSmem {
         auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 127) & ~size_t(127); return o; };
         yring = take((size_t)RY * TW * Bp * 8);
         rring = take(has_rhs ? (size_t)RR * TW * Bp * 8 : 0);
-        wring = take((size_t)RW * tiles * 8 * npad * 8);
+        wring = take((size_t)RW * tiles * 8 * ldw * 8);
         xring = take(acc ? (size_t)RW * TW * Bp * 8 : 0);
-        es = take((size_t)npad * Bp * 8);
+        es = take((size_t)npad * (Bp + 4) * 8);      // row stride Bp + 4: conflict-free B fragments
+        cb = take((size_t)2 * (TW + 2) * 4);
         th = take((size_t)Q * Bp * 8);
         bars = take(8 * 2 + 64);
         total = off;
@@ -125,13 +126,15 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
     extern __shared__ __align__(128) unsigned char sm[];
     const int Bp = a.Bp, npad = a.npad, S = a.S, m = a.g.m;
     const bool has_rhs = a.Rhs != nullptr, acc = a.Xold != nullptr;
-    SmoothSmem<TX> L(Bp, npad, a.g.Q, S, has_rhs, acc);
+    SmoothSmem<TX> L(Bp, npad, a.ldw, a.g.Q, S, has_rhs, acc);
+    const int ldw = a.ldw, Bpe = Bp + 4;
     double* yring = (double*)(sm + L.yring);
     double* rring = (double*)(sm + L.rring);
     double* wring = (double*)(sm + L.wring);
     double* xring = (double*)(sm + L.xring);
     double* Es = (double*)(sm + L.es);
     double* th = (double*)(sm + L.th);
+    int* cbx = (int*)(sm + L.cb);      // [col][2]: x-blocks of cells I-1, I of window column col
     uint64_t* bars = (uint64_t*)(sm + L.bars);
     __shared__ int s_act[kMaxBatch];
     __shared__ double s_a[kMarchThreads], s_b[kMarchThreads];
@@ -150,7 +153,15 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
 
     // ---- init: zero the rings (invalid halo columns stay zero), stage E, theta
     for (size_t t = tid; t < (L.es - L.yring) / 8; t += kMarchThreads) ((double*)(sm + L.yring))[t] = 0.0;
-    for (int t = tid; t < npad * Bp; t += kMarchThreads) Es[t] = a.has_e ? a.E[t] : 0.0;
+    for (int t = tid; t < npad * Bp; t += kMarchThreads) {
+        const int j = t / Bp, bb = t - j * Bp;
+        Es[j * Bpe + bb] = a.has_e ? a.E[t] : 0.0;
+    }
+    for (int col = tid; col < L.TW; col += kMarchThreads) {
+        const int I = min(max(xlo + col, 1), m);
+        cbx[2 * col] = axis_block(a.g, I - 1, a.g.px);
+        cbx[2 * col + 1] = axis_block(a.g, I, a.g.px);
+    }
     for (int t = tid; t < a.g.Q * Bp; t += kMarchThreads) th[t] = a.theta[t];
     for (int t = tid; t < Bp; t += kMarchThreads) s_act[t] = a.active[t];
     if (tid == 0) {
@@ -162,9 +173,9 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
 
     const int Jfirst = y0 - H, Jlast = y1 - 1 + H;   // rows whose y0 is formed
     const int nsteps = (Jlast - Jfirst + kRows) / kRows;
-    const size_t wrow = (size_t)L.tiles * 8 * npad;   // doubles per W slot
+    const size_t wrow = (size_t)L.tiles * 8 * ldw;    // doubles per W slot
     const size_t vrow = (size_t)TW * Bp;              // doubles per vector slot
-    const uint32_t wb = a.has_e ? (uint32_t)ncopy * npad * 8 : 0u;
+    const uint32_t wb = a.has_e ? (uint32_t)ncopy * ldw * 8 : 0u;
     const uint32_t vb = (uint32_t)ncopy * Bp * 8;
     // loads of step t: rows Jfirst + t*R + k, k < R (thread 0 only)
     auto issue = [&](int t) {
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
             const int ws = (t & 1) * kRows + k;            // W / x slot
             const int u = t * kRows + k;                   // row index relative to Jfirst
             const int rs = u % RR;                         // r slot (once per row, thread 0)
-            if (a.has_e) bulk_g2s(wring + ws * wrow + (size_t)coff * npad, a.W + n0 * npad, wb, bar);
+            if (a.has_e) bulk_g2s(wring + ws * wrow + (size_t)coff * ldw, a.W + n0 * ldw, wb, bar);
             if (has_rhs) bulk_g2s(rring + rs * vrow + (size_t)coff * Bp, a.Rhs + n0 * Bp, vb, bar);
             if (acc) bulk_g2s(xring + ws * vrow + (size_t)coff * Bp, a.Xold + n0 * Bp, vb, bar);
         }
@@ -224,14 +235,14 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
                 {
                     const int bt = pr & (nbt - 1), tile = pr >> lgnbt;
                     double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-                    const double* wr = Ws + (size_t)(tile * 8 + (lane >> 2)) * npad + (lane & 3);
-                    const double* ec = Es + (lane & 3) * Bp + bt * 8 + (lane >> 2);
+                    const double* wr = Ws + (size_t)(tile * 8 + (lane >> 2)) * ldw + (lane & 3);
+                    const double* ec = Es + (lane & 3) * Bpe + bt * 8 + (lane >> 2);
                     int kk = 0;
                     for (; kk + 1 < nk; kk += 2) {
-                        dmma_8x8x4(d0, d1, wr[kk * 4], ec[kk * 4 * Bp]);
-                        dmma_8x8x4(e0, e1, wr[kk * 4 + 4], ec[(kk + 1) * 4 * Bp]);
+                        dmma_8x8x4(d0, d1, wr[kk * 4], ec[kk * 4 * Bpe]);
+                        dmma_8x8x4(e0, e1, wr[kk * 4 + 4], ec[(kk + 1) * 4 * Bpe]);
                     }
-                    if (kk < nk) dmma_8x8x4(d0, d1, wr[kk * 4], ec[kk * 4 * Bp]);
+                    if (kk < nk) dmma_8x8x4(d0, d1, wr[kk * 4], ec[kk * 4 * Bpe]);
                     d0 += e0;
                     d1 += e1;
                     const int col = tile * 8 + (lane >> 2);
@@ -263,10 +274,11 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
                     const double* yup = yring + (size_t)wrapn(sl + 1, RY) * vrow;
                     const double* rs = rring + (size_t)wrapn(rsb - 1 - s + k, RR) * vrow;
                     const int cs = c0 + ((color - (xlo + c0 + J)) & 1);   // first column of `color`
+                    const int by0 = axis_block(a.g, J - 1, a.g.py) * a.g.px;
+                    const int by1 = axis_block(a.g, J, a.g.py) * a.g.px;
                     for (int col = cs + 2 * cfirst; col <= c1; col += 2 * cstride) {
-                        const int I = xlo + col;
                         double kap[4], nb[4];
-                        node_kappa<2>(a.g, th, Bp, b, I, J, 1, kap);
+                        kappa2_blocks(th, Bp, b, cbx[2 * col], cbx[2 * col + 1], by0, by1, kap);
                         const size_t e = (size_t)col * Bp + b;
                         nb[0] = yc[e - Bp];
                         nb[1] = yc[e + Bp];
@@ -342,6 +354,247 @@ __global__ void __launch_bounds__(kMarchThreads, 1) k_smooth_march(SmoothMarchAr
             if (!a.init) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
         }
         release_ticket(s.ticket);
+    }
+}
+
+}  // namespace rbs
+
+namespace rbs {
+
+// ---------------------------------------------------------------------------
+// k_resid_march: the projection pass as a row march (2D).
+//   MODE_CG    (RBCG Steps 6-8): q = A p, x += alpha p,
+//              r -= alpha q (x, r stored), v = r
+//   MODE_RESID (RBI Step 2): v = f - A x (not stored)
+// Per step (row J): stage A forms v on row J (stencil from the p / x ring,
+// halo 1) and parks it in shared memory; stage B contracts row J-1 with W on
+// the FP64 tensor cores (D[j][b] += W[node][j] v[node][b], W^T v, eq5).  The
+// stages touch different rows, so one barrier per row suffices.  Each warp
+// owns fixed (j-tile, b-tile) accumulators for the whole march, so the
+// per-CTA partials need no combination: deterministic.
+// ---------------------------------------------------------------------------
+constexpr int kRmTX = 32;
+constexpr int kRmPF = 2;
+
+struct ResidMarchArgs {
+    Geo g;
+    int Bp, npad, ldw;
+    MarchPart mp;
+    const double* W;          // [N8][ldw]
+    const double* theta;      // [Q][Bp]
+    const int* active;        // [Bp] or nullptr
+    const double* alpha;      // MODE_CG
+    const double* P;          // MODE_CG stencil input
+    double* X;                // MODE_CG rw / MODE_RESID stencil input
+    double* R;                // MODE_CG rw
+    const double* V;          // MODE_RESID rhs rows or nullptr -> vconst
+    double vconst;
+    double* part;             // [Bp][npad+1][nct]
+    int nct;
+    const int* done;
+};
+
+struct ResidSmem {
+    size_t sring, xring, rring, vring, wring, th, bars, total;
+    __host__ __device__ ResidSmem(int Bp, int ldw, int Q, int mode, bool has_v) {
+        size_t off = 0;
+        auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 127) & ~size_t(127); return o; };
+        const size_t row1 = (size_t)(kRmTX + 2) * Bp * 8, row0 = (size_t)kRmTX * Bp * 8;
+        sring = take((3 + kRmPF) * row1);                                 // stencil input, halo 1
+        xring = take(mode == 0 ? (2 + kRmPF) * row0 : 0);                 // x (CG)
+        rring = take(mode == 0 ? (2 + kRmPF) * row0 : 0);                 // r (CG)
+        vring = take(mode == 1 && has_v ? (2 + kRmPF) * row0 : 0);        // rhs rows (RESID)
+        wring = take((size_t)(3 + kRmPF) * kRmTX * ldw * 8);
+        th = take((size_t)Q * Bp * 8 + 2 * (size_t)kRmTX * (Bp + 4) * 8);  // theta + new-v rows
+        bars = take(8 * (kRmPF + 1) + 64);
+        total = off;
+    }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kMarchThreads, 1) k_resid_march(ResidMarchArgs a) {
+    if (a.done && ld_flag(a.done)) return;
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int Bp = a.Bp, npad = a.npad, ldw = a.ldw, m = a.g.m, Bpv = Bp + 4;
+    const bool has_v = a.V != nullptr;
+    ResidSmem L(Bp, ldw, a.g.Q, MODE, has_v);
+    double* sring = (double*)(sm + L.sring);
+    double* xring = (double*)(sm + L.xring);
+    double* rring = (double*)(sm + L.rring);
+    double* vring = (double*)(sm + L.vring);
+    double* wring = (double*)(sm + L.wring);
+    double* th = (double*)(sm + L.th);
+    double* vnew = th + a.g.Q * Bp;            // 2 rows of [kRmTX][Bp+4]
+    uint64_t* bars = (uint64_t*)(sm + L.bars);
+    __shared__ int s_act[kMaxBatch];
+    __shared__ double s_alpha[kMaxBatch];
+    __shared__ int s_cbx[2 * (kRmTX + 2)];
+    __shared__ double s_rr[kMarchThreads];
+
+    const int tid = threadIdx.x;
+    const int sx = blockIdx.x % a.mp.nsx, sy = blockIdx.x / a.mp.nsx;
+    const int x0 = 1 + sx * kRmTX;
+    const int y0 = 1 + sy * a.mp.rows_per_seg;
+    const int y1 = min(m + 1, y0 + a.mp.rows_per_seg);
+    const int xlo = x0 - 1;                        // window column 0 = node x0-1
+    const int Imin = max(1, xlo), Imax = min(m, x0 + kRmTX);   // stencil input range
+    const int nc = min(kRmTX, m - x0 + 1);                       // owned nodes
+    const int ncs = Imax - Imin + 1, coffs = Imin - xlo;
+    const size_t row1 = (size_t)(kRmTX + 2) * Bp, row0 = (size_t)kRmTX * Bp, wrowd = (size_t)kRmTX * ldw;
+
+    for (size_t t = tid; t < (L.th - L.sring) / 8; t += kMarchThreads) ((double*)(sm + L.sring))[t] = 0.0;
+    for (int t = tid; t < a.g.Q * Bp; t += kMarchThreads) th[t] = a.theta[t];
+    for (int t = tid; t < 2 * kRmTX * Bpv; t += kMarchThreads) vnew[t] = 0.0;
+    for (int t = tid; t < Bp; t += kMarchThreads) {
+        s_act[t] = a.active ? a.active[t] : 1;
+        s_alpha[t] = MODE == 0 ? a.alpha[t] : 0.0;
+    }
+    for (int col = tid; col < kRmTX + 2; col += kMarchThreads) {
+        const int I = min(max(xlo + col, 1), m);
+        s_cbx[2 * col] = axis_block(a.g, I - 1, a.g.px);
+        s_cbx[2 * col + 1] = axis_block(a.g, I, a.g.px);
+    }
+    if (tid == 0) {
+        for (int k = 0; k <= kRmPF; ++k) mbar_init(&bars[k], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    const double* Sin = MODE == 0 ? a.P : a.X;      // stencil input
+    // step t handles stage A on row J = y0 - 1 + t (t = 0 loads row y0-1 only) and
+    // stage B on row J - 1; the ring row index of row J is u = J - (y0 - 1).
+    const int Jbase = y0 - 1;
+    const int nsteps = (y1 - y0) + 2;                // J = y0-1 .. y1 = ring rows 0 .. nsteps-1
+    auto issue = [&](int u) {                        // loads of ring row u (row Jbase + u)
+        const int J = Jbase + u;
+        uint64_t* bar = &bars[u % (kRmPF + 1)];
+        const bool srow = J >= 1 && J <= m;                  // stencil row (halo rows too)
+        const bool crow = J >= y0 && J < y1;                 // owned row: centre data + W
+        uint32_t bytes = 0;
+        const uint32_t sb = (uint32_t)ncs * Bp * 8, cb = (uint32_t)nc * Bp * 8, wb = (uint32_t)nc * ldw * 8;
+        if (srow) bytes += sb;
+        if (crow) bytes += wb + (MODE == 0 ? 2 * cb : (has_v ? cb : 0u));
+        fence_async_smem();
+        mbar_expect_tx(bar, bytes);
+        if (srow) {
+            const int64_t n0 = (int64_t)(J - 1) * m + (Imin - 1);
+            bulk_g2s(sring + (u % (3 + kRmPF)) * row1 + (size_t)coffs * Bp, Sin + n0 * Bp, sb, bar);
+        }
+        if (crow) {
+            const int64_t n0 = (int64_t)(J - 1) * m + (x0 - 1);
+            const int cs = u % (2 + kRmPF);
+            bulk_g2s(wring + (u % (3 + kRmPF)) * wrowd, a.W + n0 * ldw, wb, bar);
+            if (MODE == 0) {
+                bulk_g2s(xring + cs * row0, a.X + n0 * Bp, cb, bar);
+                bulk_g2s(rring + cs * row0, a.R + n0 * Bp, cb, bar);
+            } else if (has_v) {
+                bulk_g2s(vring + cs * row0, a.V + n0 * Bp, cb, bar);
+            }
+        }
+    };
+    // ring row u holds row Jbase + u; stage A on row J needs rows J-1..J+1 -> u+1 must be loaded
+    if (tid == 0)
+        for (int u = 0; u <= kRmPF && u < nsteps; ++u) issue(u);
+
+    const int warp = tid >> 5, lane = tid & 31;
+    const int lgB = 31 - __clz(Bp), nbt = Bp >> 3, lgnbt = 31 - __clz(nbt);
+    const int b = tid & (Bp - 1), cfirst = tid >> lgB, cstride = kMarchThreads >> lgB;
+    const bool qact = s_act[b] != 0;
+    const double al = s_alpha[b];
+    const int npairs = (npad >> 3) * nbt;
+    double acc[4][2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][1] = 0.0;
+    double rr = 0.0;
+
+    for (int t = 0; t < nsteps; ++t) {
+        const int J = Jbase + t;                 // stage A row (u = t); ring row t+1 = J+1
+        // row t+PF+1 re-arms the barrier of row t: that phase must have completed
+        // (waited here at t = 0, at step t-1 otherwise) before thread 0 re-arms it
+        if (t == 0) mbar_wait(&bars[0], 0u);
+        if (tid == 0 && t + kRmPF + 1 < nsteps) issue(t + kRmPF + 1);
+        if (t + 1 < nsteps) mbar_wait(&bars[(t + 1) % (kRmPF + 1)], (uint32_t)(((t + 1) / (kRmPF + 1)) & 1));
+        // zero stencil rows outside the domain (no copy was issued for them)
+        if (t + 1 < nsteps && (J + 1 < 1 || J + 1 > m)) {
+            double* z = sring + ((t + 1) % (3 + kRmPF)) * row1;
+            for (size_t e = tid; e < row1; e += kMarchThreads) z[e] = 0.0;
+            __syncthreads();
+        }
+        // ---- stage A: row J (owned rows only)
+        double* vA = vnew + (size_t)(t & 1) * kRmTX * Bpv;
+        if (J >= y0 && J < y1 && qact) {
+            const double* sc = sring + (t % (3 + kRmPF)) * row1;
+            const double* sd = sring + ((t + 3 + kRmPF - 1) % (3 + kRmPF)) * row1;
+            const double* su = sring + ((t + 1) % (3 + kRmPF)) * row1;
+            const int cs = t % (2 + kRmPF);
+            const double* xs = xring + cs * row0;
+            const double* rs = rring + cs * row0;
+            const double* vs = vring + cs * row0;
+            const int by0 = axis_block(a.g, J - 1, a.g.py) * a.g.px, by1 = axis_block(a.g, J, a.g.py) * a.g.px;
+            double* xg = a.X + ((int64_t)(J - 1) * m + (x0 - 1)) * Bp;
+            double* rg = a.R + ((int64_t)(J - 1) * m + (x0 - 1)) * Bp;
+            for (int c = cfirst; c < nc; c += cstride) {
+                const size_t e = (size_t)(c + 1) * Bp + b;     // stencil window index
+                double kap[4], nb[4];
+                kappa2_blocks(th, Bp, b, s_cbx[2 * (c + 1)], s_cbx[2 * (c + 1) + 1], by0, by1, kap);
+                nb[0] = sc[e - Bp];
+                nb[1] = sc[e + Bp];
+                nb[2] = sd[e];
+                nb[3] = su[e];
+                const double q = stencil_apply<2>(a.g, kap, sc[e], nb);
+                const size_t o = (size_t)c * Bp + b;
+                double v;
+                if (MODE == 0) {
+                    const double xv = fma(al, sc[e], xs[o]);
+                    v = fma(-al, q, rs[o]);
+                    xg[o] = xv;
+                    rg[o] = v;
+                } else {
+                    v = (has_v ? vs[o] : a.vconst) - q;
+                }
+                vA[c * Bpv + b] = v;
+                rr = fma(v, v, rr);
+            }
+        } else if (J >= y0 && J < y1) {
+            for (int c = cfirst; c < nc; c += cstride) vA[c * Bpv + b] = 0.0;
+        }
+        // ---- stage B: W^T v on row J-1 (DMMA, K = 4 nodes per step)
+        const int JB = J - 1;
+        if (JB >= y0 && JB < y1) {
+            const double* vB = vnew + (size_t)((t + 1) & 1) * kRmTX * Bpv;
+            const double* Ws = wring + ((t - 1 + 3 + kRmPF) % (3 + kRmPF)) * wrowd;
+            const int nks = (nc + 3) >> 2;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int pr = warp + k * (kMarchThreads / 32);
+                if (pr < npairs) {
+                    const int bt = pr & (nbt - 1), jt = pr >> lgnbt;
+                    const double* wa = Ws + (size_t)(lane & 3) * ldw + jt * 8 + (lane >> 2);
+                    const double* vb = vB + (size_t)(lane & 3) * Bpv + bt * 8 + (lane >> 2);
+                    for (int ks = 0; ks < nks; ++ks)
+                        dmma_8x8x4(acc[k][0], acc[k][1], wa[(size_t)ks * 4 * ldw], vb[(size_t)ks * 4 * Bpv]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // ---- per-CTA partials: (j, b) owned by exactly one warp-task
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int pr = warp + k * (kMarchThreads / 32);
+        if (pr < npairs) {
+            const int bt = pr & (nbt - 1), jt = pr >> lgnbt;
+            const int j = jt * 8 + (lane >> 2), bb = bt * 8 + 2 * (lane & 3);
+            a.part[((int64_t)bb * (npad + 1) + j) * a.nct + blockIdx.x] = acc[k][0];
+            a.part[((int64_t)(bb + 1) * (npad + 1) + j) * a.nct + blockIdx.x] = acc[k][1];
+        }
+    }
+    s_rr[tid] = rr;
+    __syncthreads();
+    if (tid < Bp) {
+        double v = 0.0;
+        for (int u = tid; u < kMarchThreads; u += Bp) v += s_rr[u];
+        a.part[((int64_t)tid * (npad + 1) + npad) * a.nct + blockIdx.x] = v;
     }
 }
 

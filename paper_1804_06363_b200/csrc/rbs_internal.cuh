@@ -114,6 +114,23 @@ __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int l
     }
 }
 
+// 2D edge coefficients from precomputed cell blocks (bx of cells I-1, I; by*px of
+// cells J-1, J): bitwise the same values as node_kappa<2>.
+__device__ __forceinline__ void kappa2_blocks(const double* th, int ldb, int b, int bx0, int bx1,
+                                              int by0, int by1, double* k) {
+    if (bx0 == bx1 && by0 == by1) {
+        const double c = th[(bx0 + by0) * ldb + b];
+        k[0] = k[1] = k[2] = k[3] = c;
+        return;
+    }
+    const double c00 = th[(bx0 + by0) * ldb + b], c10 = th[(bx1 + by0) * ldb + b];
+    const double c01 = th[(bx0 + by1) * ldb + b], c11 = th[(bx1 + by1) * ldb + b];
+    k[0] = 0.5 * (c00 + c01);
+    k[1] = 0.5 * (c10 + c11);
+    k[2] = 0.5 * (c00 + c10);
+    k[3] = 0.5 * (c01 + c11);
+}
+
 // neighbour values (order -x,+x,-y,+y(,-z,+z); 0 outside) of element (i,b)
 // of a node-major batch vector v[N][ldb].
 template <int DIM>
