@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/rbs.h"
-#include "march.cuh"
+#include "march2.cuh"
 
 using namespace rbs;
 
@@ -142,6 +142,28 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
+template <int BP>
+void set_attrs_v2() {
+    const int mx = 214 * 1024;
+    cudaFuncSetAttribute(k_smooth2<BP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_resid2<BP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_resid2<BP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+template <int BP>
+void launch_smooth2(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+    switch (S) {
+        case 0: k_smooth2<BP, 0><<<grid, kMT, smem, st>>>(a); break;
+        case 1: k_smooth2<BP, 1><<<grid, kMT, smem, st>>>(a); break;
+        case 2: k_smooth2<BP, 2><<<grid, kMT, smem, st>>>(a); break;
+        default: k_smooth2<BP, 3><<<grid, kMT, smem, st>>>(a); break;
+    }
+}
+
 bool g_attr_done = false;
 void set_attrs() {
     if (g_attr_done) return;
@@ -163,6 +185,9 @@ void set_attrs() {
     cudaFuncSetAttribute(k_resid_march<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_resid_march<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_cgp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    set_attrs_v2<8>();
+    set_attrs_v2<16>();
+    set_attrs_v2<32>();
     g_attr_done = true;
 }
 
@@ -529,6 +554,9 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     cudaStream_t st = (cudaStream_t)stream;
     const Geo& g = ctx->g;
     const int Bp = pow2_batch(B), lgB = ilog2(Bp), n = ctx->n, npad = ctx->npad, Q = g.Q;
+    // RBS_DISABLE_V2 (debug / A-B): bit 0 smoother, bit 1 p-update, bit 2 projection v2 kernels
+    const char* dv2 = getenv("RBS_DISABLE_V2");
+    const int v2off = dv2 ? atoi(dv2) : 0;
     const bool cg = o->method == RBS_RBCG;
     // 2D, B_pad <= 32: the projection pass is the row march (k_resid_march)
     const bool use_rmarch = g.dim == 2 && Bp <= 32;
@@ -671,10 +699,16 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             r.theta = L.theta; r.active = L.active; r.alpha = L.alpha; r.P = P;
             r.X = Xv ? Xv : L.X; r.R = L.R; r.V = Fv; r.vconst = ctx->fconst;
             r.part = L.partP; r.nct = nct; r.done = done;
-            ResidSmem rs(Bp, ctx->ldw, Q, mode == MODE_CG ? 0 : 1, Fv != nullptr);
+            const size_t rsm = resid2_smem_bytes(Bp, ctx->ldw, Q);
             pb(RBS_K_PROJ);
-            if (mode == MODE_CG) k_resid_march<0><<<nct, kMarchThreads, rs.total, st>>>(r);
-            else k_resid_march<1><<<nct, kMarchThreads, rs.total, st>>>(r);
+            const int md = mode == MODE_CG ? 0 : 1;
+            if (v2off & 4) {
+                const ResidSmem rs1(Bp, ctx->ldw, Q, md, Fv != nullptr);
+                if (md == 0) k_resid_march<0><<<nct, kMarchThreads, rs1.total, st>>>(r);
+                else k_resid_march<1><<<nct, kMarchThreads, rs1.total, st>>>(r);
+            } else if (Bp == 8) { if (md == 0) k_resid2<8, 0><<<nct, kMT, rsm, st>>>(r); else k_resid2<8, 1><<<nct, kMT, rsm, st>>>(r); }
+            else if (Bp == 16) { if (md == 0) k_resid2<16, 0><<<nct, kMT, rsm, st>>>(r); else k_resid2<16, 1><<<nct, kMT, rsm, st>>>(r); }
+            else { if (md == 0) k_resid2<32, 0><<<nct, kMT, rsm, st>>>(r); else k_resid2<32, 1><<<nct, kMT, rsm, st>>>(r); }
             pe();
             return 1;
         }
@@ -695,7 +729,18 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.s = S; a.done = done;
         pb(RBS_K_CGP);
-        if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
+        if (!(v2off & 2) && g.dim == 2 && Bp <= 32) {
+            CGP2Args c2{};
+            c2.g = g; c2.Bp = Bp; c2.theta = L.theta;
+            c2.part = march_part(g, kC2TX, 2 * ctx->num_sms);   // 2 CTAs per SM
+            c2.active = L.active; c2.beta = L.beta; c2.Y = L.Y; c2.Pold = Pold; c2.Pnew = Pnew;
+            c2.s = S; c2.done = done;
+            const size_t csm = cgp2_smem_bytes(Bp, Q);
+            const int gr = c2.part.nsx * c2.part.nsy;
+            if (Bp == 8) k_cgp2<8><<<gr, kMT, csm, st>>>(c2);
+            else if (Bp == 16) k_cgp2<16><<<gr, kMT, csm, st>>>(c2);
+            else k_cgp2<32><<<gr, kMT, csm, st>>>(c2);
+        } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
         else k_cgp<3><<<nctf, kFlat, fsm, st>>>(a);
         pe();
         return 1;
@@ -712,8 +757,20 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         a.theta = L.theta; a.active = L.active; a.S = (int)seq.size();
         for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
         a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
-        const int grid = a.part.nsx * a.part.nsy;
         pb(RBS_K_GS);
+        const Smooth2Smem sl2(a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad);
+        if (!(v2off & 1) && Bp <= 32 && a.S <= 3 && sl2.total <= (size_t)214 * 1024) {
+            // v2: lagged one-barrier-per-row pipeline (march2.cuh), 32-column strips
+            a.part = march_part(g, kS2TX, ctx->num_sms);
+            const int grid2 = a.part.nsx * a.part.nsy;
+            const Smooth2Smem& sl = sl2;
+            if (Bp == 8) launch_smooth2<8>(a.S, grid2, sl.total, st, a);
+            else if (Bp == 16) launch_smooth2<16>(a.S, grid2, sl.total, st, a);
+            else launch_smooth2<32>(a.S, grid2, sl.total, st, a);
+            pe();
+            return 1;
+        }
+        const int grid = a.part.nsx * a.part.nsy;
         if (TX == 32) {
             SmoothSmem<32> sl(Bp, npad, ctx->ldw, Q, a.S, rhs != nullptr, Xold != nullptr);
             k_smooth_march<32><<<grid, kMarchThreads, sl.total, st>>>(a);
