@@ -38,7 +38,9 @@ from synth import CONFIGS, query_set, train_set  # noqa: E402
 METRIC = "parameter queries solved/sec to rel. residual 1e-10 (c2, RBCG, 1 GPU)"
 UNIT = "queries/s"
 HBM_FALLBACK_GBS = 6650.0     # /opt/skills/guides/B200_PROFILING.md fallback
-FP64_NOMINAL_TFS = 37.0       # B200 HGX datasheet FP64 / FP64-tensor (not measured)
+# FP64 tensor (DMMA m8n8k4) peak measured on this pool's B200 with tools/fp64_peak.cu
+# (148 SMs x 1 DMMA / 4 cycles at 1965 MHz; DFMA 36.7 TF/s); not in MEASURED_PEAKS.json
+FP64_TENSOR_MEASURED_TFS = 37.2
 
 
 def parse():
@@ -237,6 +239,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include "timed/" profiles only this
     ev0.record(stream)
     launches, its = 0, []
     for k in range(a.steps):
@@ -245,6 +248,7 @@ def main():
         its += [int(i) for i in out["its"]]
         assert all(st == "CONVERGED" for st in out["status"]), out["status"]
     ev1.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
@@ -278,27 +282,36 @@ def main():
     # ---- per-kernel device times (eager, events on the launching stream) -----
     prof = step(0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
     hbm, hbm_src = peaks()
-    Bq = c.B
-    k_ms, k_cnt = prof["k_proj"]
-    dur = k_ms / max(k_cnt, 1) / 1e3
-    alg_bytes = c.N * (40 * Bq) + c.N * c.n * 8          # p,x,r read + x,r write + W once
-    alg_flops = 2.0 * c.N * c.n * Bq                      # W^T r on the FP64 tensor cores
+    Bq, N, n = c.B, c.N, c.n
+    # algorithmic bytes per launch (each vector once, W once per batch)
+    alg = {"k_cgp": 24 * Bq * N,                    # y, p_old read; p_new written
+           "k_proj": 40 * Bq * N + 8 * N * n,       # p, x, r read; x, r written; W
+           "k_gs": 16 * Bq * N + 8 * N * n}         # r read, y written; W
+    flops = {"k_proj": 2.0 * N * n * Bq, "k_gs": 2.0 * N * n * Bq}   # W^T r / W e on DMMA
     tot_ms = sum(v[0] for v in prof.values())
-    roof = {"bound": "hbm", "kernel": "k_proj<MODE_CG> (RBCG Steps 6-8 + W^T r)",
-            "achieved": alg_bytes / dur / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": alg_bytes / dur / 1e9 / hbm, "traffic": None, "peak_source": hbm_src,
-            "alg_bytes_per_launch": alg_bytes, "avg_launch_us": dur * 1e6,
-            "share_of_iteration": k_ms / tot_ms if tot_ms else None,
-            "fp64_tensor": {"achieved_tflops": alg_flops / dur / 1e12,
-                            "nominal_peak_tflops": FP64_NOMINAL_TFS,
-                            "frac_of_nominal": alg_flops / dur / 1e12 / FP64_NOMINAL_TFS}}
-    per_iter_bytes = {"k_cgp": 24 * Bq * c.N, "k_proj": alg_bytes, "k_prolong": 8 * Bq * c.N + c.N * c.n * 8,
-                      "k_gs": None, "k_alpha": 0, "k_reduce_solve": 0, "k_beta": 0}
     kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
-                   "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items()}
-    for k, b in per_iter_bytes.items():
-        if b and kernels[k]["launches"]:
-            kernels[k]["GBps"] = b / (kernels[k]["avg_us"] * 1e-6) / 1e9
+                   "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
+    for k, kb in alg.items():
+        if k in kernels:
+            d = kernels[k]["avg_us"] * 1e-6
+            kernels[k]["alg_bytes"] = kb
+            kernels[k]["GBps"] = kb / d / 1e9
+            kernels[k]["hbm_frac"] = kb / d / 1e9 / hbm
+            if k in flops:
+                kernels[k]["fp64_tensor_TFs"] = flops[k] / d / 1e12
+    top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
+    kt = kernels[top]
+    iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)
+    iter_bytes = sum(alg.values())
+    roof = {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
+            "frac": kt["GBps"] / hbm, "traffic": None, "peak_source": hbm_src,
+            "alg_bytes_per_launch": kt["alg_bytes"], "avg_launch_us": kt["avg_us"],
+            "share_of_iteration": kt["share"],
+            "iteration": {"us": iter_us, "alg_bytes": iter_bytes,
+                          "GBps": iter_bytes / (iter_us * 1e-6) / 1e9,
+                          "frac": iter_bytes / (iter_us * 1e-6) / 1e9 / hbm},
+            "fp64_tensor_peak_tflops": FP64_TENSOR_MEASURED_TFS,
+            "fp64_tensor_peak_source": "measured, tools/fp64_peak.cu (DMMA m8n8k4, all SMs)"}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,

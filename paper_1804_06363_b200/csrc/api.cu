@@ -142,26 +142,37 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
+template <int BP, bool R>
+void set_attrs_smooth2() {
+    const int mx = 214 * 1024;
+    cudaFuncSetAttribute(k_smooth2<BP, 0, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 1, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 2, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 3, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
 template <int BP>
 void set_attrs_v2() {
     const int mx = 214 * 1024;
-    cudaFuncSetAttribute(k_smooth2<BP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    set_attrs_smooth2<BP, false>();
+    set_attrs_smooth2<BP, true>();
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_resid2<BP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
+template <int BP, bool R>
+void launch_smooth2r(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+    switch (S) {
+        case 0: k_smooth2<BP, 0, R><<<grid, kMT, smem, st>>>(a); break;
+        case 1: k_smooth2<BP, 1, R><<<grid, kMT, smem, st>>>(a); break;
+        case 2: k_smooth2<BP, 2, R><<<grid, kMT, smem, st>>>(a); break;
+        default: k_smooth2<BP, 3, R><<<grid, kMT, smem, st>>>(a); break;
+    }
+}
 template <int BP>
 void launch_smooth2(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
-    switch (S) {
-        case 0: k_smooth2<BP, 0><<<grid, kMT, smem, st>>>(a); break;
-        case 1: k_smooth2<BP, 1><<<grid, kMT, smem, st>>>(a); break;
-        case 2: k_smooth2<BP, 2><<<grid, kMT, smem, st>>>(a); break;
-        default: k_smooth2<BP, 3><<<grid, kMT, smem, st>>>(a); break;
-    }
+    if (a.Rhs) launch_smooth2r<BP, true>(S, grid, smem, st, a);
+    else launch_smooth2r<BP, false>(S, grid, smem, st, a);
 }
 
 bool g_attr_done = false;

@@ -31,6 +31,21 @@ struct LgB {
     static constexpr int v = BP == 8 ? 3 : BP == 16 ? 4 : BP == 32 ? 5 : 6;
 };
 
+// explicit 32-bit shared-memory accesses: the hot loops keep one u32 base per
+// ring row in a register instead of letting the compiler rematerialise the
+// shared window base for every access (ncu: ~25 extra instructions per element)
+__device__ __forceinline__ double ldsd(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void stsd(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void stsd2(uint32_t a, double v0, double v1) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v0), "d"(v1) : "memory");
+}
+
 // (A p)_P for a node whose 4 cells are in one block: scale*theta*(4 p - sum nb)
 __device__ __forceinline__ double stencil_uniform(double st, double c, double n0, double n1, double n2,
                                                   double n3) {
@@ -99,7 +114,7 @@ struct Smooth2Smem {
 // half-sweep s (one column of every column pair has the sweep's colour), and
 // all 12 share the output row.  Every shared-memory load of a step is issued
 // before any update of that step.
-template <int BP, int S>
+template <int BP, int S, bool HAS_RHS>
 __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
@@ -120,7 +135,9 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     __shared__ double s_yr[kMaxBatch], s_yy[kMaxBatch];
     __shared__ int s_last;
     const int m = a.g.m, ldw = a.ldw, npad = a.npad;
-    const bool has_rhs = a.Rhs != nullptr, acc = a.Xold != nullptr;
+    constexpr bool has_rhs = HAS_RHS;
+    const bool acc = a.Xold != nullptr;
+    const uint32_t sbase = smem_u32(smd);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int sx = blockIdx.x % a.part.nsx, sy = blockIdx.x / a.part.nsx;
     const int x0 = 1 + sx * kS2TX;
@@ -231,28 +248,29 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
                 } else {
                     // all tiles of this warp at once: TPW independent accumulator chains,
                     // the E fragment of each k-step shared by the tiles
-                    const int wsb = WO + ws * WROW + (tile0 * 8 + (lane >> 2)) * ldw + (lane & 3);
+                    const uint32_t wsb = sbase + 8u * (WO + ws * WROW + (tile0 * 8 + (lane >> 2)) * ldw + (lane & 3));
+                    const uint32_t tstr = 8u * TSTEP * 8 * ldw;
+                    uint32_t ea = sbase + 8u * eoff;
                     double d0[TPW], d1[TPW];
 #pragma unroll
                     for (int i = 0; i < TPW; ++i) d0[i] = d1[i] = 0.0;
 #pragma unroll 1
-                    for (int kk = 0; kk < nk; kk += 2) {
-                        const double ea = smd[eoff + kk * 4 * (BP + 4)];
-                        const double eb = smd[eoff + (kk + 1) * 4 * (BP + 4)];
+                    for (int kk = 0; kk < nk; kk += 2, ea += 8u * 8 * (BP + 4)) {
+                        const double e0 = ldsd(ea), e1 = ldsd(ea + 8u * 4 * (BP + 4));
                         double wa[TPW], wb2[TPW];
 #pragma unroll
                         for (int i = 0; i < TPW; ++i) {
                             const bool tv = TPW * TSTEP == TILES || tile0 + i * TSTEP < TILES;
-                            const int w = wsb + (tv ? i : 0) * TSTEP * 8 * ldw + kk * 4;
-                            wa[i] = smd[w];
-                            wb2[i] = smd[w + 4];
+                            const uint32_t w = wsb + (tv ? i : 0) * tstr + 32u * kk;
+                            wa[i] = ldsd(w);
+                            wb2[i] = ldsd(w + 32u);
                         }
 #pragma unroll
                         for (int i = 0; i < TPW; ++i)
-                            if (TPW * TSTEP == TILES || tile0 + i * TSTEP < TILES) dmma_8x8x4(d0[i], d1[i], wa[i], ea);
+                            if (TPW * TSTEP == TILES || tile0 + i * TSTEP < TILES) dmma_8x8x4(d0[i], d1[i], wa[i], e0);
 #pragma unroll
                         for (int i = 0; i < TPW; ++i)
-                            if (TPW * TSTEP == TILES || tile0 + i * TSTEP < TILES) dmma_8x8x4(d0[i], d1[i], wb2[i], eb);
+                            if (TPW * TSTEP == TILES || tile0 + i * TSTEP < TILES) dmma_8x8x4(d0[i], d1[i], wb2[i], e1);
                     }
 #pragma unroll
                     for (int i = 0; i < TPW; ++i) {
@@ -279,48 +297,50 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
             if (S > 0 && R >= rlog && R <= rhig && qact) {
                 const int par = (colg - R) & 1;
                 const int sl = (t - 2 * (sgi + 1)) & (kS2YR - 1);
-                const int yc = YR + sl * VROW + b;
-                const int ydn = YR + ((sl - 1) & (kS2YR - 1)) * VROW + b;
-                const int yup = YR + ((sl + 1) & (kS2YR - 1)) * VROW + b;
-                const int rrw = RR + ((t - 2 * (sgi + 1)) & (kS2RR - 1)) * VROW + b;
+                const uint32_t yc = sbase + 8u * (YR + sl * VROW + b);
+                const uint32_t ydn = sbase + 8u * (YR + ((sl - 1) & (kS2YR - 1)) * VROW + b);
+                const uint32_t yup = sbase + 8u * (YR + ((sl + 1) & (kS2YR - 1)) * VROW + b);
+                const uint32_t rrw = sbase + 8u * (RR + ((t - 2 * (sgi + 1)) & (kS2RR - 1)) * VROW + b);
                 const int by0 = axis_block(a.g, R - 1, a.g.py) * a.g.px;
                 const int by1 = axis_block(a.g, R, a.g.py) * a.g.px;
                 const bool rowu = by0 == by1;
-                const int chb = CHO + by0 * BP + b;
+                const uint32_t chb = sbase + 8u * (CHO + by0 * BP + b);
+                const uint32_t cub = smem_u32(s_cu);
 #pragma unroll 1
                 for (int p = p0; p < NPAIRS; p += PPI) {
                     const int col = 2 * p + par;
                     if (col < c0g || col > c1g) continue;
-                    const int o = col * BP;
-                    const double n0 = smd[yc + o - BP], n1 = smd[yc + o + BP];
-                    const double n2 = smd[ydn + o], n3 = smd[yup + o];
-                    const double rh = has_rhs ? smd[rrw + o] : rconst;
-                    const int cu = s_cu[col];
+                    const uint32_t o = 8u * col * BP;
+                    const double n0 = ldsd(yc + o - 8 * BP), n1 = ldsd(yc + o + 8 * BP);
+                    const double n2 = ldsd(ydn + o), n3 = ldsd(yup + o);
+                    const double rh = HAS_RHS ? ldsd(rrw + o) : rconst;
+                    int cu;
+                    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(cu) : "r"(cub + 4u * col) : "memory");
                     double v;
                     if (rowu && cu >= 0) {
-                        v = fma(smd[chb + cu * BP], rh, 0.25 * ((n0 + n1) + (n2 + n3)));
+                        v = fma(ldsd(chb + 8u * cu * BP), rh, 0.25 * ((n0 + n1) + (n2 + n3)));
                     } else {
                         const int ci = s_ci[col];
                         double kap[4], nb[4] = {n0, n1, n2, n3};
                         kappa2_blocks(smd + THO, BP, b, ci & 0xff, ci >> 8, by0, by1, kap);
                         v = gs_value<2>(a.g, kap, rh, nb);
                     }
-                    smd[yc + o] = v;
+                    stsd(yc + o, v);
                 }
             }
             // ---- output row Ro = Jb - (2S+1): stores + y^T r, y^T y -----------------
             const int Ro = Jb - (2 * S + 1);
             if (Ro >= y0 && Ro < y1) {
-                const int yo = YR + ((t - (2 * S + 1)) & (kS2YR - 1)) * VROW + S * BP;
-                const int ro = RR + ((t - (2 * S + 1)) & (kS2RR - 1)) * VROW + S * BP;
+                const uint32_t yo = sbase + 8u * (YR + ((t - (2 * S + 1)) & (kS2YR - 1)) * VROW + S * BP);
+                const uint32_t ro = sbase + 8u * (RR + ((t - (2 * S + 1)) & (kS2RR - 1)) * VROW + S * BP);
 #pragma unroll
                 for (int j = 0; j < JO; ++j) {
                     const int e = vtid + j * kS2NVT;
                     if ((e >> LGB) >= nco) break;
-                    const double v = smd[yo + e];
+                    const double v = ldsd(yo + 8u * e);
                     yg[e] = v;
                     if (a.last) {
-                        const double rv = has_rhs ? smd[ro + e] : rconst;
+                        const double rv = HAS_RHS ? ldsd(ro + 8u * e) : rconst;
                         yr = fma(v, rv, yr);
                         yy = fma(v, v, yy);
                     }
@@ -482,6 +502,7 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
         cub[j] = s_cu[col];
         cib[j] = s_ci[col];
     }
+    const uint32_t sbase = smem_u32(smd);
     double sig = 0.0;
     double* pg = a.Pnew + ((int64_t)(Jfirst - 1) * m + (xlo - 1)) * BP;
     for (int t = 0; t < nsteps; ++t, pg += (int64_t)m * BP) {
@@ -494,30 +515,33 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
         const int na = NR + (t & (kC2P - 1)) * VROW;
         // ---- loads: stage A (row Jb) and stage B (rows Jb-3 .. Jb-1) ---------
         double yv[JA], pv[JA];
+        const uint32_t yA = sbase + 8u * ya, pA = sbase + 8u * pa, nA = sbase + 8u * na;
 #pragma unroll
         for (int j = 0; j < JA; ++j) {
-            yv[j] = smd[ya + oa[j]];
-            pv[j] = smd[pa + oa[j]];
+            yv[j] = ldsd(yA + 8u * oa[j]);
+            pv[j] = ldsd(pA + 8u * oa[j]);
         }
         const int R = Jb - 2;
         const bool brow = R >= y0 && R < y1;
         const int nc_ = NR + ((t - 2) & (kC2P - 1)) * VROW, nd_ = NR + ((t - 3) & (kC2P - 1)) * VROW;
         const int nu_ = NR + ((t - 1) & (kC2P - 1)) * VROW;
         double qc[JB], q0[JB], q1[JB], q2[JB], q3[JB];
+        const uint32_t cA = sbase + 8u * nc_, dA = sbase + 8u * nd_, uA = sbase + 8u * nu_;
 #pragma unroll
         for (int j = 0; j < JB; ++j) {
-            qc[j] = smd[nc_ + ob[j]];
-            q0[j] = smd[nc_ + ob[j] - BP];
-            q1[j] = smd[nc_ + ob[j] + BP];
-            q2[j] = smd[nd_ + ob[j]];
-            q3[j] = smd[nu_ + ob[j]];
+            const uint32_t o = 8u * ob[j];
+            qc[j] = ldsd(cA + o);
+            q0[j] = ldsd(cA + o - 8 * BP);
+            q1[j] = ldsd(cA + o + 8 * BP);
+            q2[j] = ldsd(dA + o);
+            q3[j] = ldsd(uA + o);
         }
         // ---- stage A: p_new = y + beta p_old -----------------------------------
         if (ain) {
 #pragma unroll
             for (int j = 0; j < JA; ++j) {
                 const double v = fma(bet, pv[j], yv[j]);
-                if (va[j]) smd[na + oa[j]] = v;
+                if (va[j]) stsd(nA + 8u * oa[j], v);
                 if (wa[j]) pg[oa[j]] = v;
             }
         } else if (arow) {
@@ -532,7 +556,8 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
                 if (!vbq[j]) continue;
                 double q;
                 if (rowu && cub[j] >= 0) {
-                    q = stencil_uniform(smd[ST + (cub[j] + by0) * BP + b], qc[j], q0[j], q1[j], q2[j], q3[j]);
+                    q = stencil_uniform(ldsd(sbase + 8u * (ST + (cub[j] + by0) * BP + b)), qc[j], q0[j], q1[j], q2[j],
+                                        q3[j]);
                 } else {
                     double kap[4], nb[4] = {q0[j], q1[j], q2[j], q3[j]};
                     kappa2_blocks(a.theta, BP, b, cib[j] & 0xff, cib[j] >> 8, by0, by1, kap);
@@ -707,6 +732,7 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
         ocu[j] = s_cu[oc[j] + 1];
         oci[j] = s_ci[oc[j] + 1];
     }
+    const uint32_t sbase = smem_u32(smd);
     double rr = 0.0;
     int sl_c = 0, sl_n = 1, sl_d = kR2NS - 1;    // ring slots of rows J, J+1, J-1 (mod NS)
     int sl_x = 0;                                // ring slot of row J (mod NC)
@@ -729,19 +755,21 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
         const int su = SR + sl_n * ROW1 + BP + b;
         const int xs = XR + sl_x * ROW0 + b, rs = RRg + sl_x * ROW0 + b;
         double pc[JA], q0[JA], q1[JA], q2[JA], q3[JA], xa[JA], ra[JA];
+        const uint32_t scA = sbase + 8u * sc, sdA = sbase + 8u * sd, suA = sbase + 8u * su;
+        const uint32_t xsA = sbase + 8u * xs, rsA = sbase + 8u * rs;
 #pragma unroll
         for (int j = 0; j < JA; ++j) {
-            const int o = oc[j] * BP;
-            pc[j] = smd[sc + o];
-            q0[j] = smd[sc + o - BP];
-            q1[j] = smd[sc + o + BP];
-            q2[j] = smd[sd + o];
-            q3[j] = smd[su + o];
+            const uint32_t o = 8u * oc[j] * BP;
+            pc[j] = ldsd(scA + o);
+            q0[j] = ldsd(scA + o - 8 * BP);
+            q1[j] = ldsd(scA + o + 8 * BP);
+            q2[j] = ldsd(sdA + o);
+            q3[j] = ldsd(suA + o);
             if (MODE == 0) {
-                xa[j] = smd[xs + o];
-                ra[j] = smd[rs + o];
+                xa[j] = ldsd(xsA + o);
+                ra[j] = ldsd(rsA + o);
             } else {
-                ra[j] = has_v ? smd[rs + o] : vconst;
+                ra[j] = has_v ? ldsd(rsA + o) : vconst;
             }
         }
         // ---- stage B: W^T v on row J-1 (DMMA) -----------------------------------
@@ -749,12 +777,14 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
         if (JB >= y0 && JB < y1) {
             const int vB = ((t + 1) & 1) * kRmTX * BPV;
             const int Ws = WR + sl_d * WROWD;
+            const uint32_t WsA = sbase + 8u * Ws, vBA = sbase + 8u * vB;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 if (k >= myn) break;
-                const int wa = Ws + wofs[k], vb = vB + vofs[k];
-                dmma_8x8x4(acc[k][0], acc[k][1], smd[wa], smd[vb]);
-                dmma_8x8x4(acc[k][0], acc[k][1], smd[wa + 4 * ldw], smd[vb + 4 * BPV]);
+                const uint32_t wa = WsA + 8u * wofs[k], vb = vBA + 8u * vofs[k];
+                const double a0 = ldsd(wa), b0 = ldsd(vb), a1 = ldsd(wa + 32u * ldw), b1 = ldsd(vb + 32u * BPV);
+                dmma_8x8x4(acc[k][0], acc[k][1], a0, b0);
+                dmma_8x8x4(acc[k][0], acc[k][1], a1, b1);
             }
         }
         // ---- stage A compute / stores -------------------------------------------
@@ -770,7 +800,8 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
                 if (qact) {
                     double q;
                     if (rowu && ocu[j] >= 0) {
-                        q = stencil_uniform(smd[STo + (ocu[j] + by0) * BP + b], pc[j], q0[j], q1[j], q2[j], q3[j]);
+                        q = stencil_uniform(ldsd(sbase + 8u * (STo + (ocu[j] + by0) * BP + b)), pc[j], q0[j], q1[j],
+                                            q2[j], q3[j]);
                     } else {
                         double kap[4], nb[4] = {q0[j], q1[j], q2[j], q3[j]};
                         kappa2_blocks(a.theta, BP, b, oci[j] & 0xff, oci[j] >> 8, by0, by1, kap);
@@ -786,7 +817,7 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
                     }
                     rr = fma(v, v, rr);
                 }
-                smd[vA + oc[j] * BPV] = v;
+                stsd(sbase + 8u * (vA + oc[j] * BPV), v);
             }
         }
         __syncthreads();
