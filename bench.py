@@ -191,6 +191,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1804_06363_b200 as rbs
+    from paper_1804_06363_b200.dist import broadcast_basis, gather_counts
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -213,8 +214,7 @@ def main():
         fn = torch.empty((c.n,), dtype=torch.float64, device=s.device)
         snap = []
     if world > 1:
-        for t in (W, ANq, fn):
-            dist.broadcast(t, 0)
+        broadcast_basis(W, ANq, fn, src=0)        # NCCL over NVLink, once, off the hot path
     s.load_basis(W, ANq.cpu().numpy(), fn.cpu().numpy())
     torch.cuda.synchronize()
     offline_s = time.perf_counter() - t0
@@ -258,6 +258,10 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     value = a.steps * c.B * world / (ms / 1e3)
+    if world > 1:   # per-query iteration counts of every rank, for the its statistics
+        t_its = torch.tensor(its, dtype=torch.int32, device=s.device)
+        all_its, _ = gather_counts(t_its, torch.zeros_like(t_its))
+        its = [int(v) for v in all_its.cpu()]
 
     # ---- e2e: public API with host buffers (pinned X, host mu) --------------
     Xh = torch.empty((c.B, c.N), dtype=torch.float64, pin_memory=True)
