@@ -108,8 +108,10 @@ inline MarchPart march_part(const Geo& g, int TX, int sms = 148) {
 }
 // columns of the per-CTA partial buffers of the flat / march passes
 inline int part_ctas(const Geo& g) {
-    const MarchPart a = march_part(g, 32), b = march_part(g, 16);
-    return std::max(flat_ctas(g), std::max(a.nsx * a.nsy, b.nsx * b.nsy));
+    const MarchPart a = march_part(g, 32), b = march_part(g, 16), c = march_part(g, 24);
+    const MarchPart d = march_part(g, 32, 2 * 148);    // k_cgp2: 2 CTAs per SM
+    return std::max(std::max(flat_ctas(g), c.nsx * c.nsy),
+                    std::max(std::max(a.nsx * a.nsy, b.nsx * b.nsy), d.nsx * d.nsy));
 }
 inline int grid_for(int64_t work, int per, int cap) {
     int64_t c = (work + per - 1) / per;
@@ -142,37 +144,51 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
-template <int BP, bool R>
+template <int BP, bool R, int TX>
 void set_attrs_smooth2() {
     const int mx = 214 * 1024;
-    cudaFuncSetAttribute(k_smooth2<BP, 0, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 1, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 2, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 3, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 0, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 1, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 2, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 3, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 template <int BP>
 void set_attrs_v2() {
     const int mx = 214 * 1024;
-    set_attrs_smooth2<BP, false>();
-    set_attrs_smooth2<BP, true>();
+    set_attrs_smooth2<BP, false, 32>();
+    set_attrs_smooth2<BP, true, 32>();
+    set_attrs_smooth2<BP, false, 24>();
+    set_attrs_smooth2<BP, true, 24>();
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(k_resid2<BP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_resid2<BP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_resid2<BP, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_resid2<BP, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_resid2<BP, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_resid2<BP, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
-template <int BP, bool R>
-void launch_smooth2r(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+template <int BP, bool R, int TX>
+void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
     switch (S) {
-        case 0: k_smooth2<BP, 0, R><<<grid, kMT, smem, st>>>(a); break;
-        case 1: k_smooth2<BP, 1, R><<<grid, kMT, smem, st>>>(a); break;
-        case 2: k_smooth2<BP, 2, R><<<grid, kMT, smem, st>>>(a); break;
-        default: k_smooth2<BP, 3, R><<<grid, kMT, smem, st>>>(a); break;
+        case 0: k_smooth2<BP, 0, R, TX><<<grid, kMT, smem, st>>>(a); break;
+        case 1: k_smooth2<BP, 1, R, TX><<<grid, kMT, smem, st>>>(a); break;
+        case 2: k_smooth2<BP, 2, R, TX><<<grid, kMT, smem, st>>>(a); break;
+        default: k_smooth2<BP, 3, R, TX><<<grid, kMT, smem, st>>>(a); break;
     }
 }
 template <int BP>
-void launch_smooth2(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
-    if (a.Rhs) launch_smooth2r<BP, true>(S, grid, smem, st, a);
-    else launch_smooth2r<BP, false>(S, grid, smem, st, a);
+void launch_smooth2(int TX, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+    if (TX == 32) {
+        if (a.Rhs) launch_smooth2t<BP, true, 32>(S, grid, smem, st, a);
+        else launch_smooth2t<BP, false, 32>(S, grid, smem, st, a);
+    } else {
+        if (a.Rhs) launch_smooth2t<BP, true, 24>(S, grid, smem, st, a);
+        else launch_smooth2t<BP, false, 24>(S, grid, smem, st, a);
+    }
+}
+template <int BP, int PF>
+void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r) {
+    if (md == 0) k_resid2<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
+    else k_resid2<BP, 1, PF><<<grid, kMT, smem, st>>>(r);
 }
 
 bool g_attr_done = false;
@@ -546,10 +562,10 @@ rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opt
     return RBS_OK;
 }
 
-rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* o,
-                           const double* rhs_dev, double* X, int* iters, int* qstatus,
-                           double* relres, double* true_relres, double* a_n, double* history,
-                           void* workspace_dev, size_t workspace_bytes, void* stream) {
+static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* o,
+                                   const double* rhs_dev, double* X, int* iters, int* qstatus,
+                                   double* relres, double* true_relres, double* a_n, double* history,
+                                   void* workspace_dev, size_t workspace_bytes, void* stream) {
     if (!ctx) return RBS_E_ARG;
     ctx->err.clear();
     ctx->launches = 0;
@@ -710,16 +726,21 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             r.theta = L.theta; r.active = L.active; r.alpha = L.alpha; r.P = P;
             r.X = Xv ? Xv : L.X; r.R = L.R; r.V = Fv; r.vconst = ctx->fconst;
             r.part = L.partP; r.nct = nct; r.done = done;
-            const size_t rsm = resid2_smem_bytes(Bp, ctx->ldw, Q);
+            const int PF = resid2_smem_bytes(2, Bp, ctx->ldw, Q) <= (size_t)214 * 1024 ? 2 : 1;
+            const size_t rsm = resid2_smem_bytes(PF, Bp, ctx->ldw, Q);
             pb(RBS_K_PROJ);
             const int md = mode == MODE_CG ? 0 : 1;
             if (v2off & 4) {
                 const ResidSmem rs1(Bp, ctx->ldw, Q, md, Fv != nullptr);
                 if (md == 0) k_resid_march<0><<<nct, kMarchThreads, rs1.total, st>>>(r);
                 else k_resid_march<1><<<nct, kMarchThreads, rs1.total, st>>>(r);
-            } else if (Bp == 8) { if (md == 0) k_resid2<8, 0><<<nct, kMT, rsm, st>>>(r); else k_resid2<8, 1><<<nct, kMT, rsm, st>>>(r); }
-            else if (Bp == 16) { if (md == 0) k_resid2<16, 0><<<nct, kMT, rsm, st>>>(r); else k_resid2<16, 1><<<nct, kMT, rsm, st>>>(r); }
-            else { if (md == 0) k_resid2<32, 0><<<nct, kMT, rsm, st>>>(r); else k_resid2<32, 1><<<nct, kMT, rsm, st>>>(r); }
+            } else if (Bp == 8) {
+                if (PF == 2) launch_resid2<8, 2>(md, nct, rsm, st, r); else launch_resid2<8, 1>(md, nct, rsm, st, r);
+            } else if (Bp == 16) {
+                if (PF == 2) launch_resid2<16, 2>(md, nct, rsm, st, r); else launch_resid2<16, 1>(md, nct, rsm, st, r);
+            } else {
+                if (PF == 2) launch_resid2<32, 2>(md, nct, rsm, st, r); else launch_resid2<32, 1>(md, nct, rsm, st, r);
+            }
             pe();
             return 1;
         }
@@ -769,15 +790,20 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
         for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
         a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
         pb(RBS_K_GS);
-        const Smooth2Smem sl2(a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad);
-        if (!(v2off & 1) && Bp <= 32 && a.S <= 3 && sl2.total <= (size_t)214 * 1024) {
-            // v2: lagged one-barrier-per-row pipeline (march2.cuh), 32-column strips
-            a.part = march_part(g, kS2TX, ctx->num_sms);
+        const size_t kMaxDyn = (size_t)214 * 1024;
+        int TX2 = 32;
+        size_t sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad).total;
+        if (sm2 > kMaxDyn) {
+            TX2 = 24;
+            sm2 = Smooth2Smem(24, a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad).total;
+        }
+        if (!(v2off & 1) && Bp <= 32 && a.S <= 3 && sm2 <= kMaxDyn) {
+            // v2: lagged one-barrier-per-row pipeline (march2.cuh)
+            a.part = march_part(g, TX2, ctx->num_sms);
             const int grid2 = a.part.nsx * a.part.nsy;
-            const Smooth2Smem& sl = sl2;
-            if (Bp == 8) launch_smooth2<8>(a.S, grid2, sl.total, st, a);
-            else if (Bp == 16) launch_smooth2<16>(a.S, grid2, sl.total, st, a);
-            else launch_smooth2<32>(a.S, grid2, sl.total, st, a);
+            if (Bp == 8) launch_smooth2<8>(TX2, a.S, grid2, sm2, st, a);
+            else if (Bp == 16) launch_smooth2<16>(TX2, a.S, grid2, sm2, st, a);
+            else launch_smooth2<32>(TX2, a.S, grid2, sm2, st, a);
             pe();
             return 1;
         }
@@ -965,6 +991,36 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             break;
         }
     ctx->launches = launches;
+    return RBS_OK;
+}
+
+
+// Public entry.  2D grids run the row-march kernels with at most 32 queries per
+// pass (their shared-memory rings hold 32-query rows); a larger batch is solved
+// as independent sub-batches of 32 -- every query's iteration is independent of
+// the others (per-query alpha, beta, stop test), so the results are the same.
+rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* o,
+                           const double* rhs_dev, double* X, int* iters, int* qstatus,
+                           double* relres, double* true_relres, double* a_n, double* history,
+                           void* workspace_dev, size_t workspace_bytes, void* stream) {
+    if (!ctx || !ctx->has_op || ctx->g.dim != 2 || B <= 32 || B > RBS_MAX_BATCH || !mu_host || !X || !o)
+        return solve_batch_impl(ctx, B, mu_host, o, rhs_dev, X, iters, qstatus, relres, true_relres, a_n,
+                                history, workspace_dev, workspace_bytes, stream);
+    const int64_t N = ctx->g.N;
+    const int P = ctx->g.Q, nb = ctx->n, hl = o->max_iter + 1;
+    int64_t total = 0;
+    for (int c0 = 0; c0 < B; c0 += 32) {
+        const int b = std::min(32, B - c0);
+        rbs_status s = solve_batch_impl(
+            ctx, b, mu_host + (size_t)c0 * P, o, rhs_dev ? rhs_dev + (size_t)c0 * N : nullptr,
+            X + (size_t)c0 * N, iters ? iters + c0 : nullptr, qstatus ? qstatus + c0 : nullptr,
+            relres ? relres + c0 : nullptr, true_relres ? true_relres + c0 : nullptr,
+            a_n ? a_n + (size_t)c0 * nb : nullptr, history ? history + (size_t)c0 * hl : nullptr,
+            workspace_dev, workspace_bytes, stream);
+        total += ctx->launches;
+        if (s != RBS_OK) return s;
+    }
+    ctx->launches = total;
     return RBS_OK;
 }
 

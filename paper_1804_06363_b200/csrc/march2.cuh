@@ -81,7 +81,7 @@ __device__ __forceinline__ void fill_rowinfo(const Geo& g, int Jfirst, int nr, i
 // written by s+1 (two rows down, a later step): no two stages of a step touch
 // the same row, so the red-black order is exact with one barrier per row.
 // ===========================================================================
-constexpr int kS2TX = 32;
+constexpr int kS2TX = 32;       // strip width (24 when the rings of 32 do not fit)
 constexpr int kS2YR = 8;         // y ring rows (lags 0 .. 2S+1 <= 7)
 constexpr int kS2RR = 8;         // r ring rows (issued at lag 0, last read at lag 2S+1)
 constexpr int kS2WR = 3;         // W / x_old ring rows (prefetch distance 2)
@@ -95,8 +95,8 @@ constexpr int kS2NVT = kMT - 32 * kS2NTW; // vector threads (384)
 struct Smooth2Smem {
     int vrow, xo, eo, wo, tho, cho, wrow;
     size_t total;
-    __host__ __device__ Smooth2Smem(int S, int Bp, int ldw, int Q, bool has_rhs, bool acc, int npad) {
-        const int TW = kS2TX + 2 * S, tiles = (TW + 7) / 8;
+    __host__ __device__ Smooth2Smem(int TX, int S, int Bp, int ldw, int Q, bool has_rhs, bool acc, int npad) {
+        const int TW = TX + 2 * S, tiles = (TW + 7) / 8;
         vrow = TW * Bp;
         wrow = tiles * 8 * ldw;
         xo = (kS2YR + (has_rhs ? kS2RR : 0)) * vrow;
@@ -114,11 +114,11 @@ struct Smooth2Smem {
 // half-sweep s (one column of every column pair has the sweep's colour), and
 // all 12 share the output row.  Every shared-memory load of a step is issued
 // before any update of that step.
-template <int BP, int S, bool HAS_RHS>
+template <int BP, int S, bool HAS_RHS, int TX>
 __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
-    constexpr int TW = kS2TX + 2 * S;
+    constexpr int TW = TX + 2 * S;
     constexpr int VROW = TW * BP;
     constexpr int TILES = (TW + 7) / 8;
     constexpr int NBT = BP / 8;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     constexpr int GW = S > 0 ? (kS2NVT / 32) / S : 1;        // warps per sweep group
     constexpr int GT = GW * 32;                              // threads per sweep group
     constexpr int PPI = GT >> LGB;                           // pairs per slot round
-    constexpr int JO = (kS2TX * BP + kS2NVT - 1) / kS2NVT;   // output slots per thread
+    constexpr int JO = (TX * BP + kS2NVT - 1) / kS2NVT;   // output slots per thread
     constexpr int YR = 0, RR = kS2YR * VROW;
     extern __shared__ __align__(128) double smd[];
     __shared__ int s_ci[TW], s_cu[TW];
@@ -140,17 +140,17 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     const uint32_t sbase = smem_u32(smd);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int sx = blockIdx.x % a.part.nsx, sy = blockIdx.x / a.part.nsx;
-    const int x0 = 1 + sx * kS2TX;
+    const int x0 = 1 + sx * TX;
     const int y0 = 1 + sy * a.part.rows_per_seg;
     const int y1 = min(m + 1, y0 + a.part.rows_per_seg);   // exclusive
     const int xlo = x0 - S;                                  // node of window column 0
-    const int Imin = max(1, xlo), Imax = min(m, x0 + kS2TX - 1 + S);
+    const int Imin = max(1, xlo), Imax = min(m, x0 + TX - 1 + S);
     const int ncopy = Imax - Imin + 1, coff = Imin - xlo;
     const int cmin = Imin - xlo, cmax = Imax - xlo;          // valid window columns
     const int Jfirst = y0 - S;                               // row of step 0
     const int JlastP = y1 - 1 + S;                           // last prolongated row
     const int nsteps = (y1 - y0) + 3 * S + 1;                // last output row y1-1 at lag 2S+1
-    const Smooth2Smem L(S, BP, ldw, a.g.Q, has_rhs, acc, npad);
+    const Smooth2Smem L(TX, S, BP, ldw, a.g.Q, has_rhs, acc, npad);
     const int XO = L.xo, EO = L.eo, WO = L.wo, THO = L.tho, CHO = L.cho, WROW = L.wrow;
 
     // ---- init: zero the rings (Dirichlet columns/rows stay zero), tables ------
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     const int hwg = S - 1 - sgi;
     const int rlog = max(1, y0 - hwg), rhig = min(m, y1 - 1 + hwg);
     const int colg = a.seq[sgi] - xlo;                       // colour term of this group's sweep
-    const int nco = min(S + kS2TX - 1, cmax) - S + 1;        // owned output columns
+    const int nco = min(S + TX - 1, cmax) - S + 1;        // owned output columns
     double* yg = a.Y + ((int64_t)(Jfirst - (2 * S + 1) - 1) * m + (x0 - 1)) * BP;
 
     for (int t = 0; t < nsteps; ++t, yg += (int64_t)m * BP) {
@@ -610,20 +610,20 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
 // eq5), split into (j-tile, b-tile, k-quarter) tasks so the 16 warps carry
 // equal DMMA loads; the quarters are combined in a fixed order at the end.
 // ===========================================================================
-constexpr int kR2PF = 2;
-constexpr int kR2NS = 3 + kR2PF;     // stencil-input / W ring rows
-constexpr int kR2NC = 2 + kR2PF;     // x / r / f ring rows
-
+// prefetch distance PF (rows): 2, or 1 when the rings of 2 do not fit (large n)
 // dynamic shared memory (doubles): stencil ring | x ring | r (or f) ring |
 //   parked v (2 rows, stride Bp+4) | W ring (ldw) | scale*theta
-__host__ __device__ inline size_t resid2_smem_bytes(int Bp, int ldw, int Q) {
-    const size_t fixed = (size_t)kR2NS * (kRmTX + 2) * Bp + 2 * (size_t)kR2NC * kRmTX * Bp +
+__host__ __device__ inline size_t resid2_smem_bytes(int PF, int Bp, int ldw, int Q) {
+    const int NS = 3 + PF, NC = 2 + PF;
+    const size_t fixed = (size_t)NS * (kRmTX + 2) * Bp + 2 * (size_t)NC * kRmTX * Bp +
                          2 * (size_t)kRmTX * (Bp + 4);
-    return (fixed + (size_t)kR2NS * kRmTX * ldw + (size_t)Q * Bp) * 8;
+    return (fixed + (size_t)NS * kRmTX * ldw + (size_t)Q * Bp) * 8;
 }
 
-template <int BP, int MODE>
+template <int BP, int MODE, int kR2PF>
 __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
+    constexpr int kR2NS = 3 + kR2PF;     // stencil-input / W ring rows
+    constexpr int kR2NC = 2 + kR2PF;     // x / r / f ring rows
     if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
     constexpr int BPV = BP + 4;
