@@ -286,7 +286,8 @@ def main():
     # ---- per-kernel device times (eager, events on the launching stream) -----
     prof = step(0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
     hbm, hbm_src = peaks()
-    Bq, N, n = c.B, c.N, c.n
+    # queries per pass: 2D batches above 32 run as 32-query sub-batches
+    Bq, N, n = (min(c.B, 32) if c.dim == 2 else c.B), c.N, c.n
     # algorithmic bytes per launch (each vector once, W once per batch)
     alg = {"k_cgp": 24 * Bq * N,                    # y, p_old read; p_new written
            "k_proj": 40 * Bq * N + 8 * N * n,       # p, x, r read; x, r written; W
@@ -305,7 +306,7 @@ def main():
                 kernels[k]["fp64_tensor_TFs"] = flops[k] / d / 1e12
     top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
     kt = kernels[top]
-    iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)
+    iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bq queries
     iter_bytes = sum(alg.values())
     roof = {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": kt["GBps"] / hbm, "traffic": None, "peak_source": hbm_src,

@@ -163,6 +163,22 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
                            double* relres, double* true_relres, double* a_n, double* history,
                            void* workspace_dev, size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Mesh-slab partition of one 3D system.
+ * rbs_set_virtual_slabs: split the z-planes 1..m into G slabs (sizes balanced
+ *   to within one; slab s owns planes [z0, z1) as paper_1804_06363_b200/dist.py
+ *   slab_partition) and run every following rbs_solve_batch slab by slab in
+ *   this process: each slab keeps its own batch vectors over its owned planes
+ *   plus H ghost planes per side (H = half-sweeps of the smoother), the per-CTA
+ *   partial sums of all slabs are combined in a fixed order, and the ghost
+ *   planes are refreshed by device copies (r: H planes after the residual pass,
+ *   y: 1 plane after the smoother).  G = 1 switches it off.  RBCG only; results
+ *   agree with the unpartitioned solve to rounding (the sum order differs).
+ *   Errors: RBS_E_STATE (no operator), RBS_E_UNSUPPORTED (2D), RBS_E_DIM (a slab
+ *   with fewer than 4 planes).  Invalidates the captured iteration graph.
+ */
+rbs_status rbs_set_virtual_slabs(rbs_ctx* ctx, int G);
+
 /* Number of kernel launches issued by the last rbs_solve_batch (instrumentation). */
 int64_t rbs_last_launch_count(const rbs_ctx* ctx);
 

@@ -51,6 +51,7 @@ _SIGS = {
     "rbs_set_operator_blocks": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int)]),
     "rbs_set_rhs_constant": (C.c_int, [C.c_void_p, C.c_double]),
+    "rbs_set_virtual_slabs": (C.c_int, [C.c_void_p, C.c_int]),
     "rbs_basis_storage_size": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_size_t)]),
     "rbs_load_basis": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
@@ -126,6 +127,10 @@ def rbs_set_operator_blocks(ctx, dim, m, blocks):
 
 def rbs_set_rhs_constant(ctx, value):
     _check(ctx, lib().rbs_set_rhs_constant(ctx, float(value)), "rbs_set_rhs_constant")
+
+
+def rbs_set_virtual_slabs(ctx, G):
+    _check(ctx, lib().rbs_set_virtual_slabs(ctx, int(G)), "rbs_set_virtual_slabs")
 
 
 def rbs_basis_storage_size(ctx, n):
@@ -245,6 +250,12 @@ class Solver:
 
     def _bytes(self, nbytes):
         return self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.device)
+
+    def set_slabs(self, G):
+        """Mesh-slab mode (3D, RBCG): solve slab by slab with G z-slabs (1 = off)."""
+        rbs_set_virtual_slabs(self.ctx, G)
+        self._ws.clear()
+        return self
 
     def load_basis(self, W, ANq=None, fn=None, stream=None):
         """W: (N, n) array (numpy or torch); stored column-major on the device."""

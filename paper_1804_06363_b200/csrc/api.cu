@@ -36,6 +36,8 @@ struct rbs_ctx {
     double* dANq = nullptr;  // [Q][npad][npad]
     double* scratch = nullptr;
     std::vector<double> hANq, hfn;  // Q*n*n, n (fn = W^T 1)
+    // mesh slabs (virtual, one process): 1 = off
+    int nslab = 1;
     // instrumentation / polling
     int64_t launches = 0;
     int* h_flag = nullptr;
@@ -314,6 +316,8 @@ std::vector<int> color_seq(int smoother, int sweeps) {
 
 }  // namespace
 
+#include "slab.inc.cu"
+
 // ============================================================================
 extern "C" {
 
@@ -413,6 +417,10 @@ rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], co
     g.f2m1 = make_fastdiv((uint32_t)(2 * (g.m + 1)));
     g.scale = (double)(g.m + 1) * (double)(g.m + 1);
     g.h2 = 1.0 / g.scale;
+    g.kofs = 0;
+    g.mz = g.m;
+    g.own_lo = 0;
+    g.own_hi = g.m;
     ctx->g = g;
     ctx->N8 = round_up(N, 8);
     ctx->has_op = true;
@@ -559,6 +567,7 @@ rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opt
     rbs_status s = check_opts(ctx, o);
     if (s != RBS_OK) return s;
     *bytes = solve_layout(ctx, B, o, true, nullptr).bytes;
+    if (ctx->nslab > 1) *bytes = std::max(*bytes, slab_plan(ctx, B, o, nullptr).bytes);
     return RBS_OK;
 }
 
@@ -574,6 +583,12 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     if (!mu_host || !X || !workspace_dev) return fail(ctx, RBS_E_ARG, "mu_host/X/workspace is NULL");
     rbs_status s0 = check_opts(ctx, o);
     if (s0 != RBS_OK) return s0;
+    if (ctx->nslab > 1) {
+        if (rhs_dev) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: rhs override not supported");
+        CK(cudaSetDevice(ctx->device));
+        return solve_slabs(ctx, B, mu_host, o, X, iters, qstatus, relres, true_relres, a_n, history,
+                           workspace_dev, workspace_bytes, (cudaStream_t)stream);
+    }
     SolveLayout L = solve_layout(ctx, B, o, rhs_dev != nullptr, workspace_dev);
     if (workspace_bytes < solve_layout(ctx, B, o, rhs_dev != nullptr, nullptr).bytes)
         return fail(ctx, RBS_E_NOMEM, "workspace too small");
@@ -962,7 +977,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         CK(cudaStreamSynchronize(st));
         Xfin = (kc & 1) ? L.X2 : L.X;
     }
-    k_transpose_out<<<(unsigned)((g.N + 31) / 32), 256, 0, st>>>(Xfin, g.N, Bp, B, xdst);
+    k_transpose_out<<<(unsigned)((g.N + 31) / 32), 256, 0, st>>>(Xfin, g.N, Bp, B, xdst, g.N);
     ++launches;
     CKL();
     if (o->x_location == RBS_MEM_HOST)

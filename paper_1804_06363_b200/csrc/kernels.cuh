@@ -121,10 +121,10 @@ __device__ __forceinline__ void update_done(const SolveState& s) {
 // sum over the CTAs' partials part[(b*2+slot)*nctf + c] for every query b;
 // result in s_out[b].  Whole CTA participates (blockDim.x multiple of Bp).
 // (the producing kernel's own CTAs: gridDim.x columns, row stride s.nctf)
-__device__ void cta_sum_slot(const SolveState& s, int slot, double* s_buf, double* s_out) {
+__device__ void cta_sum_slot(const SolveState& s, int slot, double* s_buf, double* s_out, int cnt = -1) {
     const int gsz = blockDim.x / s.Bp;
     const int b = threadIdx.x / gsz, t = threadIdx.x - b * gsz;
-    const int cnt = gridDim.x;
+    if (cnt < 0) cnt = gridDim.x;
     double v0 = 0.0, v1 = 0.0;
     const double* p = s.partF + ((int64_t)b * 2 + slot) * s.nctf;
     int c = t;
@@ -170,6 +170,7 @@ struct ProjArgs {
     double vconst;
     double* part;             // [Bp][npad+1][nct]
     const int* done;
+    int col0;                 // first partial column of this launch (mesh slabs)
 };
 
 template <int MODE, int DIM>
@@ -210,9 +211,9 @@ __device__ __forceinline__ double proj_value(const ProjArgs& a, const double* s_
         const double rv = fma(-al, q, c2);
         a.X[e] = xv;
         a.R[e] = rv;
-        return rv;
+        return DIM == 3 && !owned(a.g, K) ? 0.0 : rv;     // slab ghost planes: not reduced
     }
-    return c1 - q;
+    return DIM == 3 && !owned(a.g, K) ? 0.0 : c1 - q;
 }
 
 template <int MODE, int DIM>
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
         const int j = t / Bp, bb = t - j * Bp;
         double s = s_red[j * Bp + bb];
         for (int l = 1; l < nlc; ++l) s += s_red[(l * rows + j) * Bp + bb];
-        a.part[((int64_t)bb * rows + j) * a.nct + blockIdx.x] = s;
+        a.part[((int64_t)bb * rows + j) * a.nct + a.col0 + blockIdx.x] = s;
     }
 }
 
@@ -397,6 +398,8 @@ struct GSArgs {
     int init;                 // LAST: 1 = rho_0 (RBCG Step 2-3)
     SolveState s;             // LAST: partials + bookkeeping
     const int* done;
+    int col0;                 // LAST: first partial column (mesh slabs)
+    int ext;                  // LAST: 1 = partials only, Step 10 by k_slab_beta
 };
 
 constexpr int kGsUnroll = 4;
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
                     yo[u] = gs_value<DIM>(a.g, k, rhs[u], nb[u]);
                     a.Y[e0 + u * stride] = yo[u];
                 }
-                if (LAST && ok[u]) {
+                if (LAST && ok[u] && (DIM == 2 || owned(a.g, K[u]))) {
                     yr = fma(yo[u], rhs[u], yr);
                     yy = fma(yo[u], yo[u], yy);
                 }
@@ -464,10 +467,10 @@ __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
                 sr += s_a[t];
                 sy += s_b[t];
             }
-            s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + blockIdx.x] = sr;
-            s.partF[((int64_t)threadIdx.x * 2 + 1) * s.nctf + blockIdx.x] = sy;
+            s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + a.col0 + blockIdx.x] = sr;
+            s.partF[((int64_t)threadIdx.x * 2 + 1) * s.nctf + a.col0 + blockIdx.x] = sy;
         }
-        if (cta_is_last(s.ticket, &s_last)) {
+        if (!a.ext && cta_is_last(s.ticket, &s_last)) {
             cta_sum_slot(s, 0, s_a, s_yr);
             cta_sum_slot(s, 1, s_a, s_yy);
             if (threadIdx.x < s.Bp) {
@@ -513,6 +516,8 @@ struct CGPArgs {
     double* Pnew;
     SolveState s;
     const int* done;
+    int col0;                 // first partial column (mesh slabs)
+    int ext;                  // 1 = partials only, Step 5 by k_slab_alpha
 };
 
 constexpr int kCgpUnroll = 2;
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
                     node_coords(a.g, (uint32_t)i, I[u], J[u], K[u]);
                     const int64_t off[6] = {-a.Bp, a.Bp, -sy, sy, -sz, sz};
                     const bool in[6] = {I[u] > 1, I[u] < a.g.m, J[u] > 1, J[u] < a.g.m,
-                                        K[u] > 1, K[u] < a.g.m};
+                                        has_zm(a.g, K[u]), has_zp(a.g, K[u])};
                     yv[u][0] = __ldg(a.Y + e);
                     pv[u][0] = __ldg(a.Pold + e);
 #pragma unroll
@@ -566,7 +571,7 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
                     for (int d = 0; d < 2 * DIM; ++d) nb[d] = fma(bet, pv[u][d + 1], yv[u][d + 1]);
                     const double q = stencil_apply<DIM>(a.g, k, pp, nb);
                     a.Pnew[e0 + u * stride] = pp;
-                    sig = fma(pp, q, sig);
+                    if (DIM == 2 || owned(a.g, K[u])) sig = fma(pp, q, sig);
                 }
         }
     }
@@ -579,9 +584,9 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
     if (threadIdx.x < a.Bp) {
         double t0 = 0.0;
         for (int t = threadIdx.x; t < kFlat; t += a.Bp) t0 += s_a[t];
-        s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + blockIdx.x] = t0;
+        s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + a.col0 + blockIdx.x] = t0;
     }
-    if (cta_is_last(s.ticket, &s_last)) {
+    if (!a.ext && cta_is_last(s.ticket, &s_last)) {
         cta_sum_slot(s, 0, s_a, s_sig);
         const int k = ld_flag(s.kcount);
         if (threadIdx.x < s.Bp) {
@@ -839,9 +844,9 @@ __global__ void k_fill_batch(double* __restrict__ v, int64_t N, int64_t N8, int 
     }
 }
 
-// out[B][N] (query-major) <- v[N8][Bp]; tiled transpose through shared memory
+// out[B][ldo] (query-major) <- v[N8][Bp] for N nodes; tiled transpose through shared memory
 __global__ void k_transpose_out(const double* __restrict__ v, int64_t N, int Bp, int B,
-                                double* __restrict__ out) {
+                                double* __restrict__ out, int64_t ldo) {
     __shared__ double tile[32][kMaxBatch + 1];
     const int64_t i0 = (int64_t)blockIdx.x * 32;
     for (int t = threadIdx.x; t < 32 * Bp; t += blockDim.x) {
@@ -851,7 +856,7 @@ __global__ void k_transpose_out(const double* __restrict__ v, int64_t N, int Bp,
     __syncthreads();
     for (int t = threadIdx.x; t < 32 * B; t += blockDim.x) {
         const int b = t >> 5, r = t & 31;
-        if (i0 + r < N) out[(int64_t)b * N + i0 + r] = tile[r][b];
+        if (i0 + r < N) out[(int64_t)b * ldo + i0 + r] = tile[r][b];
     }
 }
 
@@ -874,6 +879,65 @@ __global__ void __launch_bounds__(kThreads) k_apply_Aq(Geo g, int q, const doubl
         node_kappa<DIM>(g, s_th, 1, 0, I, J, K, k);
         node_nbrs<DIM>(g, Wi, npad, i, j, I, J, K, nb);
         Z[e] = stencil_apply<DIM>(g, k, Wi[i * npad + j], nb);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Mesh-slab mode: the passes write per-CTA partials of every
+// slab into one column range each; these single-CTA kernels sum all columns in
+// a fixed order and run the scalar step of the RBCG iteration.
+//   k_slab_alpha: Step 5 alpha = rho / (p^T A p), MAXIT / CURVATURE
+//   k_slab_beta:  Step 10 rho' = y^T r, PRECOND, beta = rho'/rho
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_slab_alpha(SolveState s, int ncols) {
+    if (ld_flag(s.done)) return;
+    __shared__ double s_a[512];
+    __shared__ double s_sig[kMaxBatch];
+    cta_sum_slot(s, 0, s_a, s_sig, ncols);
+    const int k = ld_flag(s.kcount);
+    if (threadIdx.x < s.Bp) {
+        const int bb = threadIdx.x;
+        double al = 0.0;
+        if (s.active[bb]) {
+            const double sg = s_sig[bb];
+            if (k >= s.maxit) { s.status[bb] = Q_MAXIT; s.its[bb] = k; s.active[bb] = 0; }
+            else if (!(sg > 0.0)) {
+                s.status[bb] = isfinite(sg) ? Q_CURVATURE : Q_NONFINITE;
+                s.its[bb] = k;
+                s.active[bb] = 0;
+            } else al = s.rho[bb] / sg;
+        }
+        s.alpha[bb] = al;
+    }
+    __syncthreads();
+    update_done(s);
+}
+
+__global__ void __launch_bounds__(512) k_slab_beta(SolveState s, int ncols, int init) {
+    if (ld_flag(s.done)) return;
+    __shared__ double s_a[512];
+    __shared__ double s_yr[kMaxBatch], s_yy[kMaxBatch];
+    cta_sum_slot(s, 0, s_a, s_yr, ncols);
+    cta_sum_slot(s, 1, s_a, s_yy, ncols);
+    if (threadIdx.x < s.Bp) {
+        const int bb = threadIdx.x;
+        if (s.active[bb]) {
+            const double r1 = s_yr[bb], y2 = s_yy[bb];
+            if (!(r1 > s.delta * sqrt(y2) * sqrt(s.rr[bb]))) {
+                s.status[bb] = isfinite(r1) ? Q_PRECOND : Q_NONFINITE;
+                s.active[bb] = 0;
+                s.beta[bb] = 0.0;
+            } else {
+                s.beta[bb] = init ? 0.0 : r1 / s.rho[bb];
+                s.rho[bb] = r1;
+            }
+        }
+    }
+    __syncthreads();
+    const int any = cta_any_active(s);
+    if (threadIdx.x == 0) {
+        *(volatile int*)s.done = any ? 0 : 1;
+        if (!init) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
     }
 }
 

@@ -48,7 +48,20 @@ struct Geo {
     FastDiv f2m1;     // division by 2(m+1) (cell -> block)
     double scale;     // (m+1)^2 = h^-2 (AMB-3)
     double h2;        // h^2
+    // 3D mesh slab: the local node range holds planes
+    // K = kofs+1 .. kofs+mz of the global grid; planes own_lo <= K-kofs-1 < own_hi
+    // are owned (count in reductions).  Full grid: kofs = 0, mz = m, own = [0, m).
+    int kofs, mz, own_lo, own_hi;
 };
+
+// z-neighbour availability of a node at global plane K inside its slab
+__device__ __forceinline__ bool has_zm(const Geo& g, int K) { return K > 1 && K - g.kofs > 1; }
+__device__ __forceinline__ bool has_zp(const Geo& g, int K) { return K < g.m && K - g.kofs < g.mz; }
+// owned-plane mask of the slab (1 for every node of a 2D / full grid)
+__device__ __forceinline__ bool owned(const Geo& g, int K) {
+    const int u = K - g.kofs - 1;
+    return u >= g.own_lo && u < g.own_hi;
+}
 
 // interior coordinates I,J,K in 1..m of node i (x fastest)
 __device__ __forceinline__ void node_coords(const Geo& g, uint32_t i, int& I, int& J, int& K) {
@@ -60,7 +73,7 @@ __device__ __forceinline__ void node_coords(const Geo& g, uint32_t i, int& I, in
     } else {
         uint32_t u = fdiv(t, g.fm);
         J = (int)(t - u * (uint32_t)g.m) + 1;
-        K = (int)u + 1;
+        K = (int)u + 1 + g.kofs;
     }
 }
 
@@ -144,8 +157,8 @@ __device__ __forceinline__ void node_nbrs(const Geo& g, const double* __restrict
     nb[3] = J < g.m ? __ldg(p + sy) : 0.0;
     if (DIM == 3) {
         const int64_t sz = sy * g.m;
-        nb[4] = K > 1 ? __ldg(p - sz) : 0.0;
-        nb[5] = K < g.m ? __ldg(p + sz) : 0.0;
+        nb[4] = has_zm(g, K) ? __ldg(p - sz) : 0.0;
+        nb[5] = has_zp(g, K) ? __ldg(p + sz) : 0.0;
     }
 }
 

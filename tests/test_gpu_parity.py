@@ -344,3 +344,38 @@ def test_c4_full_size_sampled(orc, rbs):
     """c4: 3D 255^3 (N = 16.6M), 2x2x2 blocks, B = 16."""
     out = _full_size_sampled(orc, rbs, "c4", 8, 31, 5, [0, 15])
     assert len(out["its"]) == 16
+
+
+# ----------------------------------------------------------------------------- mesh slabs
+@pytest.mark.parametrize("G", [2, 3])
+def test_virtual_slabs_match_oracle_and_full_solve(orc, rbs, G):
+    """Mesh-slab mode: G z-slabs with ghost planes, halo copies and
+    fixed-order cross-slab partial sums give the oracle's RBCG (its +-1, x 1e-9,
+    histories) and agree with the unpartitioned GPU solve to rounding."""
+    dim, m, blocks, n = 3, 23, (2, 2, 2), 8
+    g, res = oracle_basis(orc, dim, m, blocks, n, 30, 5)
+    rng = np.random.default_rng(31 + G)
+    mus = 0.1 * 100 ** rng.random((5, g.Q))
+    full = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    ref_gpu = full.solve_batch(mus, record_history=1)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"]).set_slabs(G)
+    out = s.solve_batch(mus, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg")
+    Xs, Xf = out["X"].cpu().numpy(), ref_gpu["X"].cpu().numpy()
+    assert np.abs(Xs - Xf).max() <= 1e-9 * np.abs(Xf).max()
+    assert np.all(np.abs(out["its"] - ref_gpu["its"]) <= 1)
+    assert np.allclose(out["true_relres"], ref_gpu["true_relres"], rtol=1e-3, atol=1e-13)
+    # fixed-iteration mode through the slab path
+    fx = s.solve_batch(mus, tol=0.0, max_iter=7)
+    compare(fx, g, res["W"], res["ANq"], res["fn"], mus, "rbcg", check_hist=False, tol=0.0, max_iter=7)
+
+
+def test_virtual_slabs_errors(rbs):
+    s2 = rbs.Solver(2, 15, (2, 2))
+    with pytest.raises(rbs.RbsError):
+        s2.set_slabs(2)                      # 2D: unsupported
+    s3 = rbs.Solver(3, 11, (2, 2, 2))
+    with pytest.raises(rbs.RbsError):
+        s3.set_slabs(4)                      # 11 planes / 4 slabs < 4 planes each
+    s3.set_slabs(2)
+    s3.set_slabs(1)
