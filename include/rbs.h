@@ -179,6 +179,30 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
  */
 rbs_status rbs_set_virtual_slabs(rbs_ctx* ctx, int G);
 
+/* Mesh slabs over ranks (one process per GPU, NCCL over NVLink):
+ * rbs_nccl_unique_id: write an NCCL unique id (128 bytes) into id_out (rank 0;
+ *   the caller distributes it, e.g. with torch.distributed).  Errors: RBS_E_ARG.
+ * rbs_dist_init: after rbs_set_operator_blocks (3D), join the communicator as
+ *   `rank` of `nranks`; this rank then owns planes [z0, z1) of the slab
+ *   partition (balanced to within one plane) and stores `ghost` planes per side
+ *   (>= the smoother's half-sweeps; 3 for the default symmetric sweep).  From
+ *   then on every N-length buffer of this context is rank-local: the basis
+ *   passed to rbs_load_basis is the rows of the STORED planes [g0, g1)
+ *   (rbs_local_range), with the offline blocks of the full basis passed on the
+ *   host (required); X returned by rbs_solve_batch is [B][owned nodes].  Every
+ *   rank calls rbs_solve_batch with the same mu list (collective).  Per RBCG
+ *   iteration: grouped ncclSend/ncclRecv of ghost planes with the neighbours
+ *   and three ncclAllReduce(sum) of [B]-, [B][n+1]- and [B][2]-sized partials.
+ *   Errors: RBS_E_STATE, RBS_E_UNSUPPORTED (2D), RBS_E_DIM (slabs too thin),
+ *   RBS_E_CUDA (NCCL failure, detail in rbs_last_error).
+ * rbs_local_range: this context's owned [z0, z1) and stored [g0, g1) planes and
+ *   the node counts (full grid when not distributed).
+ */
+rbs_status rbs_nccl_unique_id(void* id_out, size_t bytes);
+rbs_status rbs_dist_init(rbs_ctx* ctx, const void* nccl_id, int nranks, int rank, int ghost);
+rbs_status rbs_local_range(const rbs_ctx* ctx, int64_t* z0, int64_t* z1, int64_t* g0, int64_t* g1,
+                           int64_t* n_stored, int64_t* n_owned);
+
 /* Number of kernel launches issued by the last rbs_solve_batch (instrumentation). */
 int64_t rbs_last_launch_count(const rbs_ctx* ctx);
 

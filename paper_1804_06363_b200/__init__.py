@@ -52,6 +52,9 @@ _SIGS = {
                                           C.POINTER(C.c_int)]),
     "rbs_set_rhs_constant": (C.c_int, [C.c_void_p, C.c_double]),
     "rbs_set_virtual_slabs": (C.c_int, [C.c_void_p, C.c_int]),
+    "rbs_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "rbs_dist_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]),
+    "rbs_local_range": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int64)] * 6),
     "rbs_basis_storage_size": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_size_t)]),
     "rbs_load_basis": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
@@ -131,6 +134,23 @@ def rbs_set_rhs_constant(ctx, value):
 
 def rbs_set_virtual_slabs(ctx, G):
     _check(ctx, lib().rbs_set_virtual_slabs(ctx, int(G)), "rbs_set_virtual_slabs")
+
+
+def rbs_nccl_unique_id():
+    buf = (C.c_char * 128)()
+    _check(None, lib().rbs_nccl_unique_id(buf, 128), "rbs_nccl_unique_id")
+    return bytes(buf)
+
+
+def rbs_dist_init(ctx, nccl_id: bytes, nranks, rank, ghost=3):
+    buf = (C.c_char * 128).from_buffer_copy(nccl_id)
+    _check(ctx, lib().rbs_dist_init(ctx, buf, int(nranks), int(rank), int(ghost)), "rbs_dist_init")
+
+
+def rbs_local_range(ctx):
+    v = [C.c_int64() for _ in range(6)]
+    _check(ctx, lib().rbs_local_range(ctx, *[C.byref(x) for x in v]), "rbs_local_range")
+    return dict(zip(("z0", "z1", "g0", "g1", "n_stored", "n_owned"), (x.value for x in v)))
 
 
 def rbs_basis_storage_size(ctx, n):
@@ -257,6 +277,15 @@ class Solver:
         self._ws.clear()
         return self
 
+    def dist_init(self, nccl_id: bytes, nranks, rank, ghost=3):
+        """Mesh slabs over ranks: this context becomes rank's slab (rbs_dist_init)."""
+        rbs_dist_init(self.ctx, nccl_id, nranks, rank, ghost)
+        r = rbs_local_range(self.ctx)
+        self.N = r["n_stored"]
+        self.local = r
+        self._ws.clear()
+        return self
+
     def load_basis(self, W, ANq=None, fn=None, stream=None):
         """W: (N, n) array (numpy or torch); stored column-major on the device."""
         torch = self.torch
@@ -289,11 +318,12 @@ class Solver:
         o = self.opts(**kw)
         mu = np.ascontiguousarray(mu, dtype=np.float64)
         B = mu.shape[0]
+        nx = self.local["n_owned"] if getattr(self, "local", None) else self.N   # ranks: owned nodes
         if X is None:
             if o.x_location == RBS_MEM_HOST:
-                X = torch.empty((B, self.N), dtype=torch.float64, pin_memory=True)
+                X = torch.empty((B, nx), dtype=torch.float64, pin_memory=True)
             else:
-                X = torch.empty((B, self.N), dtype=torch.float64, device=self.device)
+                X = torch.empty((B, nx), dtype=torch.float64, device=self.device)
         its = np.zeros(B, dtype=np.int32)
         st = np.zeros(B, dtype=np.int32)
         rel = np.zeros(B)

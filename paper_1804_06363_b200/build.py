@@ -17,6 +17,17 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 
+def nccl_dir() -> str:
+    """NCCL of the torch wheel (nvidia-nccl): headers + libnccl.so.2 (mesh slabs over ranks)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for root in (list(spec.submodule_search_locations) if spec else []):
+        d = os.path.join(root, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("NCCL headers not found (nvidia-nccl wheel)")
+
+
 def nvcc() -> str:
     for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if c and (os.path.isabs(c) and os.path.exists(c) or not os.path.isabs(c)):
@@ -29,7 +40,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps = [d for d in DEPS if os.path.exists(d)]
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in deps):
         return SO
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", SO] + srcs + ["-lcudart"]
+    nd = nccl_dir()
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I" + os.path.join(nd, "include"), "-o", SO] + srcs + [
+        "-lcudart", "-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2",
+        "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/rbs.h"
 #include "march2.cuh"
 
@@ -38,6 +40,11 @@ struct rbs_ctx {
     std::vector<double> hANq, hfn;  // Q*n*n, n (fn = W^T 1)
     // mesh slabs (virtual, one process): 1 = off
     int nslab = 1;
+    // mesh slabs over ranks (rbs_dist_init): this rank's slab, NCCL communicator
+    bool dist = false;
+    int nranks = 1, rank = 0, dz0 = 0, dz1 = 0, dg0 = 0, dg1 = 0, dH = 0;
+    ncclComm_t comm = nullptr;
+    Geo gglob{};
     // instrumentation / polling
     int64_t launches = 0;
     int* h_flag = nullptr;
@@ -366,6 +373,7 @@ void rbs_destroy(rbs_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -422,9 +430,12 @@ rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], co
     g.own_lo = 0;
     g.own_hi = g.m;
     ctx->g = g;
+    ctx->gglob = g;
     ctx->N8 = round_up(N, 8);
     ctx->has_op = true;
     ctx->has_basis = false;
+    ctx->dist = false;
+    ctx->nslab = 1;
     return RBS_OK;
 }
 
@@ -453,6 +464,8 @@ rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
     if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
     if (n < 0 || n > RBS_MAX_N) return fail(ctx, RBS_E_DIM, "n out of range 0..64");
     if (n > 0 && (!W_dev || ldw < ctx->g.N)) return fail(ctx, RBS_E_DIM, "W_dev NULL or ldw < N");
+    if (ctx->dist && n > 0 && (!ANq_host || !fn_host))
+        return fail(ctx, RBS_E_ARG, "mesh slabs over ranks: pass the offline blocks (ANq_host, fn_host)");
     if (!storage_dev) return fail(ctx, RBS_E_ARG, "storage_dev is NULL");
     BasisLayout L = basis_layout(ctx, n, storage_dev);
     if (storage_bytes < L.bytes) return fail(ctx, RBS_E_NOMEM, "storage too small");
@@ -567,7 +580,7 @@ rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opt
     rbs_status s = check_opts(ctx, o);
     if (s != RBS_OK) return s;
     *bytes = solve_layout(ctx, B, o, true, nullptr).bytes;
-    if (ctx->nslab > 1) *bytes = std::max(*bytes, slab_plan(ctx, B, o, nullptr).bytes);
+    if (ctx->nslab > 1 || ctx->dist) *bytes = std::max(*bytes, slab_plan(ctx, B, o, nullptr).bytes);
     return RBS_OK;
 }
 
@@ -583,7 +596,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     if (!mu_host || !X || !workspace_dev) return fail(ctx, RBS_E_ARG, "mu_host/X/workspace is NULL");
     rbs_status s0 = check_opts(ctx, o);
     if (s0 != RBS_OK) return s0;
-    if (ctx->nslab > 1) {
+    if (ctx->nslab > 1 || ctx->dist) {
         if (rhs_dev) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: rhs override not supported");
         CK(cudaSetDevice(ctx->device));
         return solve_slabs(ctx, B, mu_host, o, X, iters, qstatus, relres, true_relres, a_n, history,

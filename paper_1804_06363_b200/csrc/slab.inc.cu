@@ -13,11 +13,14 @@
 //   K3 y0 = W e, H half-sweeps on the stored planes, y^T r / y^T y partials
 //                                                      -> k_slab_beta (Step 10)
 //   halo: y on 1 plane per side (K1 forms p on the first ghost plane)
-// Partials of all slabs land in one column range each of the shared partial
-// arrays and are summed in a fixed order.  This is the "virtual slabs" form
-// (all slabs in one process, halos as device copies); the multi-GPU form runs
-// one slab per rank with the same passes, NCCL send/recv for the halos and an
-// allreduce of the column sums.
+// Two transports share these passes:
+//  * virtual slabs (rbs_set_virtual_slabs): all slabs in one process; the
+//    partials of all slabs land in one column range each of the shared partial
+//    arrays and are summed in a fixed order; halos are device copies;
+//  * ranks (rbs_dist_init): one slab per GPU; before each scalar step the rank's
+//    columns are summed (k_reduce_rows) and ncclAllReduce'd over NVLink (three
+//    small allreduces per iteration: sigma, [W^T r, ||r||^2], [y^T r, y^T y]),
+//    halos are grouped ncclSend/ncclRecv of whole planes with the neighbours.
 namespace {
 
 struct Slab {
@@ -34,6 +37,7 @@ struct SlabPlan {
     std::vector<Slab> sl;
     int H = 1, totP = 0, totF = 0;
     SolveLayout L{};         // the shared small arrays (vectors unused)
+    double *colP = nullptr, *colF = nullptr;   // ranks: this rank's column sums (allreduced)
     size_t bytes = 0;
 };
 
@@ -47,17 +51,21 @@ void slab_range(int m, int G, int s, int& z0, int& z1) {
 
 SlabPlan slab_plan(const rbs_ctx* c, int B, const rbs_solve_opts* o, void* base) {
     SlabPlan P;
-    const Geo& g = c->g;
-    const int G = c->nslab, Bp = pow2_batch(B), m = g.m;
-    P.H = std::max<int>(1, (int)color_seq(o->smoother, o->sweeps).size());
+    const Geo& g = c->gglob;
+    const int G = c->dist ? 1 : c->nslab, Bp = pow2_batch(B), m = g.m;
+    P.H = c->dist ? c->dH : std::max<int>(1, (int)color_seq(o->smoother, o->sweeps).size());
     const int64_t plane = (int64_t)m * m;
     Carve cv(base);
     P.sl.resize(G);
     for (int s = 0; s < G; ++s) {
         Slab& q = P.sl[s];
-        slab_range(m, G, s, q.z0, q.z1);
-        q.g0 = std::max(1, q.z0 - P.H);
-        q.g1 = std::min(m + 1, q.z1 + P.H);
+        if (c->dist) {
+            q.z0 = c->dz0; q.z1 = c->dz1; q.g0 = c->dg0; q.g1 = c->dg1;
+        } else {
+            slab_range(m, G, s, q.z0, q.z1);
+            q.g0 = std::max(1, q.z0 - P.H);
+            q.g1 = std::min(m + 1, q.z1 + P.H);
+        }
         q.g = g;
         q.g.kofs = q.g0 - 1;
         q.g.mz = q.g1 - q.g0;
@@ -77,7 +85,8 @@ SlabPlan slab_plan(const rbs_ctx* c, int B, const rbs_solve_opts* o, void* base)
         q.P0 = cv.take<double>(vec);
         q.P1 = cv.take<double>(vec);
         q.Y = cv.take<double>(vec);
-        q.W = c->Wi ? c->Wi + (size_t)(q.g0 - 1) * plane * c->ldw : nullptr;
+        // virtual: rows of the full basis; ranks: the loaded basis is this slab's rows
+        q.W = c->Wi ? (c->dist ? c->Wi : c->Wi + (size_t)(q.g0 - 1) * plane * c->ldw) : nullptr;
     }
     // shared small arrays (SolveState); partial arrays sized for all slabs' columns
     const int npad = c->npad;
@@ -103,6 +112,8 @@ SlabPlan slab_plan(const rbs_ctx* c, int B, const rbs_solve_opts* o, void* base)
     L.its = cv.take<int>(Bp);
     L.pivot = cv.take<int>(Bp);
     L.ints = cv.take<int>(8);
+    P.colP = cv.take<double>((size_t)Bp * (npad + 1) + 8);
+    P.colF = cv.take<double>((size_t)Bp * 2 + 8);
     P.bytes = cv.off + 256;
     return P;
 }
@@ -122,6 +133,66 @@ extern "C" rbs_status rbs_set_virtual_slabs(rbs_ctx* ctx, int G) {
     return RBS_OK;
 }
 
+extern "C" rbs_status rbs_nccl_unique_id(void* id_out, size_t bytes) {
+    if (!id_out || bytes < sizeof(ncclUniqueId)) return RBS_E_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return RBS_E_CUDA;
+    std::memcpy(id_out, &id, sizeof id);
+    return RBS_OK;
+}
+
+extern "C" rbs_status rbs_dist_init(rbs_ctx* ctx, const void* nccl_id, int nranks, int rank, int ghost) {
+    if (!ctx || !nccl_id) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
+    const Geo gg = ctx->gglob;
+    if (gg.dim != 3) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs need a 3D operator");
+    if (nranks < 1 || rank < 0 || rank >= nranks || ghost < 1) return fail(ctx, RBS_E_ARG, "bad nranks/rank/ghost");
+    if (gg.m / nranks < std::max(4, ghost)) return fail(ctx, RBS_E_DIM, "a slab would own too few planes");
+    CK(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    if (ctx->comm) { ncclCommDestroy(ctx->comm); ctx->comm = nullptr; }
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+    if (r != ncclSuccess) return fail(ctx, RBS_E_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    int z0, z1;
+    slab_range(gg.m, nranks, rank, z0, z1);
+    ctx->nranks = nranks; ctx->rank = rank; ctx->dH = ghost;
+    ctx->dz0 = z0; ctx->dz1 = z1;
+    ctx->dg0 = std::max(1, z0 - ghost);
+    ctx->dg1 = std::min(gg.m + 1, z1 + ghost);
+    // the context's geometry becomes the rank's stored planes: basis rows, vectors
+    Geo lg = gg;
+    lg.kofs = ctx->dg0 - 1;
+    lg.mz = ctx->dg1 - ctx->dg0;
+    lg.own_lo = z0 - ctx->dg0;
+    lg.own_hi = z1 - ctx->dg0;
+    lg.N = (int64_t)gg.m * gg.m * lg.mz;
+    ctx->g = lg;
+    ctx->N8 = round_up(lg.N, 8);
+    ctx->dist = true;
+    ctx->nslab = 1;
+    ctx->has_basis = false;
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+    return RBS_OK;
+}
+
+extern "C" rbs_status rbs_local_range(const rbs_ctx* c, int64_t* z0, int64_t* z1, int64_t* g0, int64_t* g1,
+                                      int64_t* n_stored, int64_t* n_owned) {
+    if (!c) return RBS_E_ARG;
+    const Geo& gg = c->gglob;
+    const int64_t plane = gg.dim == 3 ? (int64_t)gg.m * gg.m : (int64_t)gg.m;
+    const int a0 = c->dist ? c->dz0 : 1, a1 = c->dist ? c->dz1 : gg.m + 1;
+    const int b0 = c->dist ? c->dg0 : 1, b1 = c->dist ? c->dg1 : gg.m + 1;
+    if (z0) *z0 = a0;
+    if (z1) *z1 = a1;
+    if (g0) *g0 = b0;
+    if (g1) *g1 = b1;
+    if (n_stored) *n_stored = (int64_t)(b1 - b0) * plane;
+    if (n_owned) *n_owned = (int64_t)(a1 - a0) * plane;
+    return RBS_OK;
+}
+
 namespace {
 
 rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* o, double* X,
@@ -134,7 +205,10 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
         return fail(ctx, RBS_E_NOMEM, "workspace too small");
     for (const Slab& q : P.sl)
         if (q.z1 - q.z0 < P.H) return fail(ctx, RBS_E_DIM, "a slab owns fewer planes than the halo depth");
-    const Geo& g = ctx->g;
+    const Geo& g = ctx->gglob;
+    const bool dist = ctx->dist;
+    if (dist && P.H < (int)color_seq(o->smoother, o->sweeps).size())
+        return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs over ranks: more half-sweeps than ghost planes");
     const int Bp = pow2_batch(B), lgB = ilog2(Bp), n = ctx->n, npad = ctx->npad, Q = g.Q;
     const int G = (int)P.sl.size();
     const int64_t plane = (int64_t)g.m * g.m;
@@ -196,6 +270,15 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             k_cgp<3><<<q.nctf, kFlat, fsm, st>>>(a);
             ++c;
         }
+        if (dist) {   // rank sum of the columns, allreduce over the ranks, Step 5
+            SolveState S1 = S;
+            S1.partF = P.colF;
+            S1.nctf = 1;
+            k_reduce_rows<<<Bp, 128, 0, st>>>(L.partF, 2, P.totF, P.colF);
+            ncclAllReduce(P.colF, P.colF, (size_t)Bp * 2, ncclDouble, ncclSum, ctx->comm, st);
+            k_slab_alpha<<<1, 512, 0, st>>>(S1, 1);
+            return c + 2;
+        }
         k_slab_alpha<<<1, 512, 0, st>>>(S, P.totF);
         return c + 1;
     };
@@ -210,12 +293,39 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             launch_proj<MODE_CG>(q.g, q.nct, psm, st, a);
             ++c;
         }
+        if (dist) {   // rank sum, allreduce of [W^T r, ||r||^2], Steps 7-9
+            SolveState S1 = S;
+            S1.partP = P.colP;
+            S1.nct = 1;
+            k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, P.totP, P.colP);
+            ncclAllReduce(P.colP, P.colP, (size_t)Bp * (npad + 1), ncclDouble, ncclSum, ctx->comm, st);
+            k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S1);
+            return c + 2;
+        }
         k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S);
         return c + 1;
     };
     // halo copies: ghost planes of slab s from the owners' stored planes
     auto halo = [&](int which, int depth) {
         int c = 0;
+        if (dist) {   // grouped send/recv of whole planes with the neighbouring ranks
+            Slab& q = P.sl[0];
+            double* v = which == 0 ? q.R : which == 1 ? q.Y : q.X;
+            const size_t pe = (size_t)plane * Bp;          // doubles per plane
+            ncclGroupStart();
+            if (ctx->rank > 0) {
+                const int d = std::min(depth, q.z0 - q.g0);
+                ncclSend(v + (size_t)(q.z0 - q.g0) * pe, d * pe, ncclDouble, ctx->rank - 1, ctx->comm, st);
+                ncclRecv(v + (size_t)(q.z0 - d - q.g0) * pe, d * pe, ncclDouble, ctx->rank - 1, ctx->comm, st);
+            }
+            if (ctx->rank + 1 < ctx->nranks) {
+                const int d = std::min(depth, q.g1 - q.z1);
+                ncclSend(v + (size_t)(q.z1 - d - q.g0) * pe, d * pe, ncclDouble, ctx->rank + 1, ctx->comm, st);
+                ncclRecv(v + (size_t)(q.z1 - q.g0) * pe, d * pe, ncclDouble, ctx->rank + 1, ctx->comm, st);
+            }
+            ncclGroupEnd();
+            return 0;
+        }
         for (int s = 0; s < G; ++s) {
             Slab& q = P.sl[s];
             double* dst = which == 0 ? q.R : which == 1 ? q.Y : q.X;
@@ -270,6 +380,15 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
                 ++c;
             }
         }
+        if (dist) {   // rank sum, allreduce of [y^T r, y^T y], Step 10
+            SolveState S1 = S;
+            S1.partF = P.colF;
+            S1.nctf = 1;
+            k_reduce_rows<<<Bp, 128, 0, st>>>(L.partF, 2, P.totF, P.colF);
+            ncclAllReduce(P.colF, P.colF, (size_t)Bp * 2, ncclDouble, ncclSum, ctx->comm, st);
+            k_slab_beta<<<1, 512, 0, st>>>(S1, 1, init);
+            return c + 2;
+        }
         k_slab_beta<<<1, 512, 0, st>>>(S, P.totF, init);
         return c + 1;
     };
@@ -289,8 +408,8 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     };
     const int chunk = o->graph_chunk;
     char keybuf[512];
-    snprintf(keybuf, sizeof keybuf, "slab|%d|%p|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%.17g",
-             G, workspace_dev, B, Bp, o->smoother, o->sweeps, o->max_iter, chunk, o->tol, o->delta,
+    snprintf(keybuf, sizeof keybuf, "slab|%d|%d|%p|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%.17g",
+             G, (int)dist, workspace_dev, B, Bp, o->smoother, o->sweeps, o->max_iter, chunk, o->tol, o->delta,
              o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist, n, npad, ctx->fconst);
     const std::string key(keybuf);
     if (!ctx->gexec || ctx->gkey != key) {
@@ -348,6 +467,7 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     }
     k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, P.totP, L.fproj);
     ++launches;
+    if (dist) ncclAllReduce(L.fproj, L.fproj, (size_t)Bp * (npad + 1), ncclDouble, ncclSum, ctx->comm, st);
     CKL();
     {
         std::vector<double> rows((size_t)Bp * (npad + 1));
@@ -355,16 +475,19 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
         CK(cudaStreamSynchronize(st));
         for (int b = 0; b < Bp; ++b) tr[b] = std::sqrt(rows[(size_t)b * (npad + 1) + npad]) / hfn[b];
     }
+    // X: [B][N] (virtual), [B][owned nodes of this rank] (ranks)
     double* xdst = o->x_location == RBS_MEM_HOST ? L.Xout : X;
+    const int64_t ldx = dist ? (int64_t)(P.sl[0].z1 - P.sl[0].z0) * plane : g.N;
     for (Slab& q : P.sl) {
         const int64_t nown = (int64_t)(q.z1 - q.z0) * plane;
         k_transpose_out<<<(unsigned)((nown + 31) / 32), 256, 0, st>>>(
-            q.X + (size_t)(q.z0 - q.g0) * plane * Bp, nown, Bp, B, xdst + (size_t)(q.z0 - 1) * plane, g.N);
+            q.X + (size_t)(q.z0 - q.g0) * plane * Bp, nown, Bp, B, xdst + (dist ? 0 : (size_t)(q.z0 - 1) * plane),
+            ldx);
         ++launches;
     }
     CKL();
     if (o->x_location == RBS_MEM_HOST)
-        CK(cudaMemcpyAsync(X, L.Xout, (size_t)B * g.N * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(X, L.Xout, (size_t)B * ldx * 8, cudaMemcpyDeviceToHost, st));
     if (a_n && n > 0) {
         std::vector<double> ha((size_t)Bp * npad);
         CK(cudaMemcpyAsync(ha.data(), L.a_n, ha.size() * 8, cudaMemcpyDeviceToHost, st));

@@ -379,3 +379,20 @@ def test_virtual_slabs_errors(rbs):
         s3.set_slabs(4)                      # 11 planes / 4 slabs < 4 planes each
     s3.set_slabs(2)
     s3.set_slabs(1)
+
+
+def test_dist_slab_single_rank_nccl(orc, rbs):
+    """Mesh slabs over ranks (rbs_dist_init) with one rank: the NCCL code path
+    (column sums + allreduce before every scalar step, grouped send/recv with no
+    neighbours, graph capture with NCCL calls) reproduces the oracle's RBCG.  The
+    multi-rank partition itself is the virtual-slab test's (same passes, halos,
+    partial columns); only the transport differs."""
+    dim, m, blocks, n = 3, 19, (2, 2, 2), 8
+    g, res = oracle_basis(orc, dim, m, blocks, n, 30, 6)
+    rng = np.random.default_rng(77)
+    mus = 0.1 * 100 ** rng.random((4, g.Q))
+    s = rbs.Solver(dim, m, blocks).dist_init(rbs.rbs_nccl_unique_id(), 1, 0, 3)
+    assert s.local["z0"] == 1 and s.local["z1"] == m + 1 and s.local["n_owned"] == g.N
+    s.load_basis(res["W"], res["ANq"], res["fn"])
+    out = s.solve_batch(mus, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg")
