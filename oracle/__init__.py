@@ -38,7 +38,8 @@ def build(force: bool = False) -> str:
 
 class _Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("smoother", C.c_int),
-                ("sweeps", C.c_int), ("omega", C.c_double), ("delta", C.c_double)]
+                ("sweeps", C.c_int), ("omega", C.c_double), ("delta", C.c_double),
+                ("n_active", C.c_int), ("gamma", C.c_double), ("active_n", C.POINTER(C.c_int))]
 
 
 _lib = None
@@ -118,14 +119,16 @@ class Grid:
         return ANq, fn
 
     # -- solvers ------------------------------------------------------------
-    def _solve(self, fname, W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps, omega, delta):
+    def _solve(self, fname, W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps, omega, delta,
+               n_active=0, gamma=0.0):
         n = 0 if W is None else W.shape[1]
         Wf = np.asfortranarray(W, dtype=np.float64) if n else np.zeros((1, 1))
         ANq = np.ascontiguousarray(ANq, dtype=np.float64) if n else np.zeros(1)
         fn = np.ascontiguousarray(fn, dtype=np.float64) if n else np.zeros(1)
         mu = np.ascontiguousarray(mu, dtype=np.float64)
         bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
-        o = _Opts(tol, max_iter, smoother, sweeps, omega, delta)
+        act = np.zeros(max_iter + 2, dtype=np.int32)
+        o = _Opts(tol, max_iter, smoother, sweeps, omega, delta, int(n_active), float(gamma), _i(act))
         x = np.empty(self.N)
         its = C.c_int(0)
         hist = np.full(max_iter + 2, np.nan)
@@ -136,17 +139,20 @@ class Grid:
                                    _d(hist), _d(a_n), C.byref(trr))
         k = its.value
         return dict(x=x, its=k, status=STATUS[st], hist=hist[:k + 1].copy(),
-                    a_n=a_n[:n].copy(), true_relres=trr.value)
+                    a_n=a_n[:n].copy(), true_relres=trr.value, active_n=act[:k].copy())
 
     def rbi(self, W, ANq, fn, mu, b=None, tol=1e-10, max_iter=500000, smoother=SYM_RBGS,
-            sweeps=1, omega=1.0, delta=1e-12):
+            sweeps=1, omega=1.0, delta=1e-12, n_active=0):
         return self._solve("or_rbi", W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps,
-                           omega, delta)
+                           omega, delta, n_active)
 
     def rbcg(self, W, ANq, fn, mu, b=None, tol=1e-10, max_iter=20000, smoother=SYM_RBGS,
-             sweeps=1, omega=1.0, delta=1e-12):
+             sweeps=1, omega=1.0, delta=1e-12, n_active=0, gamma=0.0):
+        """n_active: active RB dimension (0 = all columns); gamma > 0: the adaptive-n
+        rule of PAPER.md:287 (the result's active_n[k] is the dimension of the k-th
+        preconditioner application)."""
         return self._solve("or_rbcg", W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps,
-                           omega, delta)
+                           omega, delta, n_active, gamma)
 
     def cg(self, mu, b=None, tol=1e-10, max_iter=100000):
         mu = np.ascontiguousarray(mu, dtype=np.float64)
@@ -190,6 +196,12 @@ class Grid:
 
 
 # -- dense primitives --------------------------------------------------------
+def adapt_n(rnorm_k, rnorm_k1, gamma, na, n_max):
+    """The adaptive-n rule of PAPER.md:287 (or_adapt_n)."""
+    return int(lib().or_adapt_n(C.c_double(rnorm_k), C.c_double(rnorm_k1), C.c_double(gamma),
+                                int(na), int(n_max)))
+
+
 def cholesky(A):
     A = np.ascontiguousarray(A, dtype=np.float64)
     n = A.shape[0]

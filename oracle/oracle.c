@@ -321,7 +321,35 @@ typedef struct {
     const double* theta;
     const or_opts* o;
     double* rn; double* e;                   /* n */
+    int na;                                  /* active dimension (leading columns of W) */
 } solver_ctx;
+
+/* "if the residual norm ratio ||r_k||/||r_{k+1}|| < gamma ... then we
+ * increase N by 1" -- capped at the stored dimension (AMB-19). */
+int or_adapt_n(double rnorm_k, double rnorm_k1, double gamma, int na, int n_max)
+{
+    if (gamma > 0.0 && na < n_max && rnorm_k / rnorm_k1 < gamma) return na + 1;
+    return na;
+}
+
+/* the reduced system of the active dimension na: A_{na} = leading na x na block of
+ * A_n(mu), whose Cholesky factor is the leading block of L (nested spaces, AMB-19);
+ * e = A_{na}^{-1} rn[0..na), e[na..n) = 0 */
+static void solve_active(const solver_ctx* s, const double* rn, double* e)
+{
+    const int n = s->n, na = s->na;
+    for (int i = 0; i < na; ++i) {
+        double t = rn[i];
+        for (int k = 0; k < i; ++k) t -= s->L[i * n + k] * e[k];
+        e[i] = t / s->L[i * n + i];
+    }
+    for (int i = na - 1; i >= 0; --i) {
+        double t = e[i];
+        for (int k = i + 1; k < na; ++k) t -= s->L[k * n + i] * e[k];
+        e[i] = t / s->L[i * n + i];
+    }
+    for (int i = na; i < n; ++i) e[i] = 0.0;
+}
 
 /* r_n = W^T r (eq5) */
 static void project(const solver_ctx* s, const double* r, double* rn)
@@ -360,6 +388,7 @@ int or_rbi(int dim, int64_t m, const int* blocks, int n, const double* W,
     solver_ctx s = {dim, m, blocks, grid_N(dim, m), grid_Q(dim, blocks), n, W, NULL, mu, o,
                     NULL, NULL};
     int64_t N = s.N;
+    s.na = (o->n_active > 0 && o->n_active < n) ? o->n_active : n;
     s.L = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
     s.rn = (double*)malloc(sizeof(double) * (size_t)(n + 1));
     s.e = (double*)malloc(sizeof(double) * (size_t)(n + 1));
@@ -391,8 +420,9 @@ int or_rbi(int dim, int64_t m, const int* blocks, int n, const double* W,
         if (n > 0) {
             if (it == 0 && b_in == NULL) memcpy(s.rn, fn, sizeof(double) * (size_t)n);
             else project(&s, r, s.rn);
-            /* Step 5: A_n e_n = r_n */
-            or_chol_solve(n, s.L, s.rn, s.e);
+            /* Step 5: A_n e_n = r_n (active dimension n_active) */
+            solve_active(&s, s.rn, s.e);
+            if (o->active_n) o->active_n[it] = s.na;
             if (it == 0 && a_n) memcpy(a_n, s.e, sizeof(double) * (size_t)n);
             /* Step 6: x = x + W e_n */
             prolong_add(&s, s.e, x);
@@ -414,7 +444,7 @@ static void rbi_precond(const solver_ctx* s, const double* r, const double* rn_g
     if (s->n > 0) {
         if (rn_given) memcpy(s->rn, rn_given, sizeof(double) * (size_t)s->n);
         else project(s, r, s->rn);
-        or_chol_solve(s->n, s->L, s->rn, s->e);
+        solve_active(s, s->rn, s->e);
         if (e_out) memcpy(e_out, s->e, sizeof(double) * (size_t)s->n);
         prolong_add(s, s->e, y);
     }
@@ -429,6 +459,7 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
     solver_ctx s = {dim, m, blocks, grid_N(dim, m), grid_Q(dim, blocks), n, W, NULL, mu, o,
                     NULL, NULL};
     int64_t N = s.N;
+    s.na = (o->n_active > 0 && o->n_active < n) ? o->n_active : n;
     s.L = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
     s.rn = (double*)malloc(sizeof(double) * (size_t)(n + 1));
     s.e = (double*)malloc(sizeof(double) * (size_t)(n + 1));
@@ -452,6 +483,7 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
     if (!(fnorm > 0.0)) { status = OR_CONVERGED; goto final; }
     if (!isfinite(fnorm)) { status = OR_NONFINITE; goto final; }
     /* Step 2: y_0 = RBI(A, r_0, W, 1);  W^T r_0 = W^T f = f_n when b = f */
+    if (o->active_n) o->active_n[0] = s.na;
     rbi_precond(&s, r, b_in == NULL ? fn : NULL, y, a_n);
     /* Step 3: p_0 = y_0 */
     memcpy(p, y, sizeof(double) * (size_t)N);
@@ -469,13 +501,18 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
         double alpha = rho / sigma;
         /* Step 6-7 */
         for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * p[i];
+        const double rnorm_k = norm2(N, r);
         for (int64_t i = 0; i < N; ++i) r[i] = r[i] - alpha * q[i];
-        double h = norm2(N, r) / fnorm;
+        const double rnorm_k1 = norm2(N, r);
+        double h = rnorm_k1 / fnorm;
         if (hist) hist[k + 1] = h;
         *its = k + 1;
         if (!isfinite(h)) { status = OR_NONFINITE; break; }
         /* Step 8 */
         if (h < o->tol) { status = OR_CONVERGED; break; }
+        /* adaptive n: grow the space of the next preconditioner */
+        s.na = or_adapt_n(rnorm_k, rnorm_k1, o->gamma, s.na, n);
+        if (o->active_n) o->active_n[k + 1] = s.na;
         /* Step 9: y_{k+1} = RBI(A, r_{k+1}, W, 1) */
         rbi_precond(&s, r, NULL, y, NULL);
         /* Step 10: beta_k = y_{k+1}^T r_{k+1} / y_k^T r_k */

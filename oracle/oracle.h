@@ -36,6 +36,11 @@ typedef struct {
     int sweeps;        /* nu */
     double omega;      /* Jacobi damping */
     double delta;      /* PRECOND breakdown threshold (AMB-11) */
+    int n_active;      /* active RB dimension (0 = n): the leading columns of W are used */
+    double gamma;      /* RBCG adaptive-n rule, 0 = off: grow the active
+                          dimension by one when ||r_k|| / ||r_{k+1}|| < gamma */
+    int* active_n;     /* optional, max_iter+1 entries: active dimension of the k-th
+                          preconditioner application (RBCG) / correction (RBI) */
 } or_opts;
 
 /* (A(theta) x) matrix-free, PAPER.md:98-103 (eq12) with AMB-1..4. */
@@ -47,6 +52,10 @@ void or_gs_halfsweep(int dim, int64_t m, const int* blocks, const double* theta,
 /* smoother S(A, b, y) in place, PAPER.md:148-153 (eq8). */
 void or_smooth(int dim, int64_t m, const int* blocks, const double* theta,
                const double* b, double* y, int kind, int sweeps, double omega);
+
+/* adaptive-n rule of PAPER.md:287 (DESIGN.md AMB-19): returns na + 1 when
+ * ||r_k|| / ||r_{k+1}|| < gamma (gamma > 0) and na < n_max, else na. */
+int or_adapt_n(double rnorm_k, double rnorm_k1, double gamma, int na, int n_max);
 
 /* dense Cholesky A = L L^T (right-looking); returns -1 or failing pivot. */
 int or_cholesky(int n, const double* A, double* L);

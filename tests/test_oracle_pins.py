@@ -378,3 +378,52 @@ def test_multifidelity_basis(orc):
     assert np.abs(mf["W"].T @ mf["W"] - np.eye(5)).max() < 1e-12
     out = fine.rbcg(mf["W"], mf["ANq"], mf["fn"], tr[3])
     assert out["status"] == "CONVERGED"
+
+
+# --------------------------------------------------------------------------- adaptive n (NEXT(2))
+def test_adapt_n_rule_spec_examples(orc):
+    """The gamma-rule of PAPER.md:287 on SPEC's worked examples (golden, cited)."""
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+    for ex in gold["adapt_n"]:
+        assert orc.adapt_n(ex["ratio"], 1.0, ex["gamma"], ex["na"], ex["n_max"]) == ex["out"], ex["cite"]
+    assert orc.adapt_n(2.0, 1.0, 0.0, 3, 8) == 3          # gamma = 0: rule off
+
+
+@pytest.mark.parametrize("k", [1, 3, 5])
+def test_active_dimension_is_the_truncated_basis(orc, small2d, k):
+    """Using the leading k columns (n_active = k) is the RB method with W_k: the
+    Cholesky factor of a leading principal block is the leading block of the full
+    factor, so the solves equal those of the truncated basis (W[:, :k], the k x k
+    leading blocks of A_{n,q}, f_n[:k]) -- bitwise, same operation order."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    Wk, Ak, fk = np.asfortranarray(W[:, :k]), np.ascontiguousarray(ANq[:, :k, :k]), fn[:k].copy()
+    mu = rand_mu(g.Q)
+    for solve, kw in ((g.rbcg, {}), (g.rbi, {})):
+        a = solve(W, ANq, fn, mu, n_active=k, **kw)
+        b = solve(Wk, Ak, fk, mu, **kw)
+        assert a["status"] == b["status"] and a["its"] == b["its"]
+        assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["hist"], b["hist"])
+        assert np.array_equal(a["a_n"][:k], b["a_n"]) and not np.any(a["a_n"][k:])
+    c = g.rbcg(W, ANq, fn, mu, n_active=k, gamma=0.0)
+    assert np.array_equal(c["x"], g.rbcg(Wk, Ak, fk, mu)["x"]) and np.all(c["active_n"] == k)
+
+
+def test_adaptive_n_grows_by_the_rule_and_converges(orc, small2d):
+    """gamma = 10 from n_active = 1: the active dimension is nondecreasing, grows by at
+    most one per iteration exactly when the residual ratio is below gamma (checked
+    against the returned history), stays <= n, and the iterate reaches the direct
+    solution."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    mu = rand_mu(g.Q)
+    out = g.rbcg(W, ANq, fn, mu, n_active=1, gamma=10.0)
+    act, h = out["active_n"], out["hist"]
+    assert out["status"] == "CONVERGED" and act[0] == 1
+    assert np.all(np.diff(act) >= 0) and np.all(np.diff(act) <= 1) and act.max() <= res["n"]
+    for k in range(out["its"] - 1):
+        grow = h[k] / h[k + 1] < 10.0 and act[k] < res["n"]
+        assert act[k + 1] == act[k] + (1 if grow else 0), k
+    A = refs.cellwise_fd(2, g.m, g.blocks, mu).toarray()
+    xs = np.linalg.solve(A, np.ones(g.N))
+    assert np.linalg.norm(out["x"] - xs) <= 1e-8 * np.linalg.norm(xs)
