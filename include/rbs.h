@@ -131,6 +131,14 @@ typedef struct {
     int graph_chunk;     /* iterations per captured CUDA graph (default 16, even) */
     int profile;         /* 1: launch eagerly (no graph) with CUDA events around every
                             kernel; per-class times via rbs_last_profile (default 0) */
+    int n_active;        /* active RB dimension: the leading n_active columns of W are used
+                            (0 = all; the iterations-vs-n study).  The
+                            reduced solve then uses the leading block of the Cholesky factor
+                            (nested spaces, DESIGN.md AMB-19). */
+    double gamma;        /* RBCG only, 0 = off: the adaptive-n rule of PAPER.md:287 -- after
+                            each x-update, if ||r_k|| / ||r_{k+1}|| < gamma the active
+                            dimension grows by one (capped at n) for the next preconditioner
+                            application; start value n_active.  Final values: rbs_last_n_active */
 } rbs_solve_opts;
 
 void rbs_default_opts(rbs_solve_opts* opts);
@@ -202,6 +210,10 @@ rbs_status rbs_nccl_unique_id(void* id_out, size_t bytes);
 rbs_status rbs_dist_init(rbs_ctx* ctx, const void* nccl_id, int nranks, int rank, int ghost);
 rbs_status rbs_local_range(const rbs_ctx* ctx, int64_t* z0, int64_t* z1, int64_t* g0, int64_t* g1,
                            int64_t* n_stored, int64_t* n_owned);
+
+/* Active RB dimension of every query at the end of the last rbs_solve_batch
+ * (host array of B; n unless opts.n_active / opts.gamma were used). */
+rbs_status rbs_last_n_active(const rbs_ctx* ctx, int* n_active_host);
 
 /* Number of kernel launches issued by the last rbs_solve_batch (instrumentation). */
 int64_t rbs_last_launch_count(const rbs_ctx* ctx);

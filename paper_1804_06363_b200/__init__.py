@@ -34,7 +34,7 @@ class rbs_solve_opts(C.Structure):
     _fields_ = [("method", C.c_int), ("tol", C.c_double), ("max_iter", C.c_int),
                 ("smoother", C.c_int), ("sweeps", C.c_int), ("delta", C.c_double),
                 ("record_history", C.c_int), ("x_location", C.c_int), ("graph_chunk", C.c_int),
-                ("profile", C.c_int)]
+                ("profile", C.c_int), ("n_active", C.c_int), ("gamma", C.c_double)]
 
 
 _lib = None
@@ -46,6 +46,7 @@ _SIGS = {
     "rbs_destroy": (None, [C.c_void_p]),
     "rbs_last_error": (C.c_char_p, [C.c_void_p]),
     "rbs_last_launch_count": (C.c_int64, [C.c_void_p]),
+    "rbs_last_n_active": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rbs_last_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "rbs_kernel_class_name": (C.c_char_p, [C.c_int]),
     "rbs_set_operator_blocks": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
@@ -196,6 +197,12 @@ def rbs_solve_batch(ctx, B, mu_host, opts, rhs_dev, X, iters, qstatus, relres, t
            "rbs_solve_batch")
 
 
+def rbs_last_n_active(ctx, B):
+    out = np.zeros(B, dtype=np.int32)
+    _check(ctx, lib().rbs_last_n_active(ctx, _ptr(out)), "rbs_last_n_active")
+    return out
+
+
 def rbs_last_launch_count(ctx):
     return int(lib().rbs_last_launch_count(ctx))
 
@@ -334,7 +341,7 @@ class Solver:
         rbs_solve_batch(self.ctx, B, mu, o, rhs, X, its, st, rel, trr, a_n, hist, ws, stream)
         out = dict(X=X, its=its, status=[QSTATUS[int(s)] for s in st], qstatus=st, relres=rel,
                    true_relres=trr, a_n=None if a_n is None else a_n[:, :(self.n or 0)],
-                   launches=rbs_last_launch_count(self.ctx))
+                   launches=rbs_last_launch_count(self.ctx), n_active=rbs_last_n_active(self.ctx, B))
         if o.profile:
             out["profile"] = rbs_last_profile(self.ctx)
         if hist is not None:

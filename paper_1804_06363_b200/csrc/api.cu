@@ -47,6 +47,7 @@ struct rbs_ctx {
     Geo gglob{};
     // instrumentation / polling
     int64_t launches = 0;
+    std::vector<int> last_na;   // active RB dimension per query of the last solve
     int* h_flag = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     // graph cache
@@ -250,7 +251,7 @@ struct SolveLayout {
     double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout;
     double *theta, *fproj, *L, *Ainv, *E, *a_n, *partP, *partF;
     double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist;
-    int *active, *status, *its, *pivot, *ints;
+    int *active, *status, *its, *pivot, *ints, *na;
     size_t bytes;
 };
 SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool rhs, void* base) {
@@ -289,8 +290,17 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.its = cv.take<int>(Bp);
     L.pivot = cv.take<int>(Bp);
     L.ints = cv.take<int>(8);
+    L.na = cv.take<int>(Bp);
     L.bytes = cv.off + 256;
     return L;
+}
+
+// active RB dimension (opts.n_active, gamma rule): leading-block reduced solves (AMB-19)
+void set_active_dim(SolveState& S, int* na, const rbs_solve_opts* o, int n) {
+    S.na = na;
+    S.na0 = (o->n_active > 0 && o->n_active < n) ? o->n_active : n;
+    S.gamma = o->method == RBS_RBCG ? o->gamma : 0.0;
+    S.tri = (S.na0 < n || S.gamma > 0.0) ? 1 : 0;
 }
 
 rbs_status check_opts(rbs_ctx* ctx, const rbs_solve_opts* o) {
@@ -304,6 +314,9 @@ rbs_status check_opts(rbs_ctx* ctx, const rbs_solve_opts* o) {
     if (o->x_location != RBS_MEM_DEVICE && o->x_location != RBS_MEM_HOST)
         return fail(ctx, RBS_E_ARG, "bad x_location");
     if (o->graph_chunk < 2 || (o->graph_chunk & 1)) return fail(ctx, RBS_E_ARG, "graph_chunk must be even >= 2");
+    if (o->n_active < 0 || o->n_active > ctx->n) return fail(ctx, RBS_E_ARG, "n_active out of range 0..n");
+    if (!(o->gamma >= 0.0)) return fail(ctx, RBS_E_ARG, "gamma must be >= 0");
+    if (o->gamma > 0.0 && o->method != RBS_RBCG) return fail(ctx, RBS_E_ARG, "gamma rule is RBCG only");
     return RBS_OK;
 }
 
@@ -384,6 +397,12 @@ void rbs_destroy(rbs_ctx* ctx) {
 const char* rbs_last_error(const rbs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
 
 int64_t rbs_last_launch_count(const rbs_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+rbs_status rbs_last_n_active(const rbs_ctx* ctx, int* out) {
+    if (!ctx || !out) return RBS_E_ARG;
+    for (size_t b = 0; b < ctx->last_na.size(); ++b) out[b] = ctx->last_na[b];
+    return RBS_OK;
+}
 
 rbs_status rbs_last_profile(const rbs_ctx* ctx, double* ms_total, int64_t* launches) {
     if (!ctx || !ms_total || !launches) return RBS_E_ARG;
@@ -570,6 +589,8 @@ void rbs_default_opts(rbs_solve_opts* o) {
     o->x_location = RBS_MEM_DEVICE;
     o->graph_chunk = 16;
     o->profile = 0;
+    o->n_active = 0;
+    o->gamma = 0.0;
 }
 
 rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opts* o, size_t* bytes) {
@@ -683,6 +704,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     S.rho = L.rho; S.rr = L.rr; S.fnorm = L.fnorm; S.relres = L.relres; S.active = L.active;
     S.status = L.status; S.its = L.its; S.pivot = L.pivot; S.kcount = kcount; S.done = done;
     S.ticket = ticket; S.hist = L.hist;
+    set_active_dim(S, L.na, o, n);
 
     k_setup_reduced<<<Bp, 128, 0, st>>>(S, cg ? 0 : 1);
     CKL();
@@ -965,6 +987,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     CK(cudaMemcpyAsync(hp.data(), L.pivot, Bp * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hrel.data(), L.relres, Bp * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hfn.data(), L.fnorm, Bp * 8, cudaMemcpyDeviceToHost, st));
+    ctx->last_na.assign(Bp, n);
+    CK(cudaMemcpyAsync(ctx->last_na.data(), L.na, Bp * 4, cudaMemcpyDeviceToHost, st));
     if (cg) {
         // true residual ||f - A x|| / ||f|| (not used for stopping)
         proj(MODE_RESID, nullptr, false);
@@ -1005,6 +1029,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     if (history && L.hist)
         CK(cudaMemcpyAsync(history, L.hist, (size_t)B * (o->max_iter + 1) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    ctx->last_na.resize(B);
     for (int b = 0; b < B; ++b) {
         if (iters) iters[b] = hi[b];
         if (qstatus) qstatus[b] = hs[b];
@@ -1037,6 +1062,7 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
     const int64_t N = ctx->g.N;
     const int P = ctx->g.Q, nb = ctx->n, hl = o->max_iter + 1;
     int64_t total = 0;
+    std::vector<int> na_all;
     for (int c0 = 0; c0 < B; c0 += 32) {
         const int b = std::min(32, B - c0);
         rbs_status s = solve_batch_impl(
@@ -1047,8 +1073,10 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
             workspace_dev, workspace_bytes, stream);
         total += ctx->launches;
         if (s != RBS_OK) return s;
+        na_all.insert(na_all.end(), ctx->last_na.begin(), ctx->last_na.begin() + b);
     }
     ctx->launches = total;
+    ctx->last_na = na_all;
     return RBS_OK;
 }
 

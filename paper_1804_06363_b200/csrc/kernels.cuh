@@ -45,6 +45,10 @@ struct SolveState {
     int* done;
     unsigned* ticket;
     double* hist;             // [Bp][maxit+1] or nullptr
+    int* na;                  // [Bp] active RB dimension per query
+    int na0;                  // its start value (n_active, or n)
+    int tri;                  // 1: reduced solves by the leading block of L (n_active < n or gamma)
+    double gamma;             // RBCG adaptive-n rule, 0 = off
 };
 
 __device__ __forceinline__ int ld_flag(const int* p) { return *(volatile const int*)p; }
@@ -624,7 +628,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
     __shared__ double s_rn[kMaxN + 1];
     __shared__ double s_chunk[(kMaxN + 1) * kRsChunks];
     __shared__ double s_e[kMaxN * 8];
-    __shared__ int s_go, s_last;
+    __shared__ double s_prev;
+    __shared__ int s_go, s_last, s_na;
     const int b = blockIdx.x, tid = threadIdx.x;
     const int rows = s.npad + 1, nr = s.n + 1;     // rows 0..n-1 and the rr row (npad)
     const bool act = s.active[b] != 0;
@@ -660,6 +665,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             if (s.hist) s.hist[(int64_t)b * (s.maxit + 1) + it] = h;
             s.its[b] = it;
             s.relres[b] = h;
+            s_prev = s.rr[b];                 // ||r_k||^2 (adaptive-n rule)
             s.rr[b] = rr2;
             int go = 1;
             if (!isfinite(h)) { s.status[b] = Q_NONFINITE; go = 0; }
@@ -669,6 +675,28 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             s_go = go;
         }
         __syncthreads();
+        if (s.tri) {
+            // active dimension (adaptive-n rule after the x-update), then
+            // e = A_{na}^{-1} r_n[0..na) with the leading block of L (AMB-19), zero beyond
+            if (tid == 0) {
+                int na = s.na[b];
+                const double prev = s_prev;
+                if (s_go && s.gamma > 0.0 && s.method == 1 && na < s.n && prev < s.gamma * s.gamma * s_rn[s.npad])
+                    ++na;
+                s.na[b] = na;
+                s_na = na;
+            }
+            __syncthreads();
+            if (tid < 32) {
+                const int na = s_na;
+                const double* Lb = s.L + (int64_t)b * s.npad * s.npad;
+                double z0 = (s_go && tid < na) ? s_rn[tid] : 0.0;
+                double z1 = (s_go && tid + 32 < na) ? s_rn[tid + 32] : 0.0;
+                if (s_go) warp_chol_solve(Lb, s.npad, na, &z0, &z1, tid);
+                if (tid < s.n) s.E[tid * s.Bp + b] = tid < na ? z0 : 0.0;
+                if (tid + 32 < s.n) s.E[(tid + 32) * s.Bp + b] = tid + 32 < na ? z1 : 0.0;
+            }
+        } else {
         // e = A_n^{-1} r_n: row i by 8 threads (fixed order), frozen lanes get e = 0
         const double* Ai = s.Ainv + (int64_t)b * s.npad * s.npad;
         for (int t = tid; t < s.n * 8; t += kRsThreads) {
@@ -683,6 +711,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             double v = 0.0;
             for (int l = 0; l < 8; ++l) v += s_e[tid * 8 + l];
             s.E[tid * s.Bp + b] = v;
+        }
         }
     }
     if (cta_is_last(s.ticket, &s_last)) {
@@ -794,13 +823,21 @@ __global__ void __launch_bounds__(128) k_setup_reduced(SolveState s, int rbi) {
             for (int i = n; i < ld; ++i) Ai[i * ld + j] = 0.0;
         }
     }
+    const int na0 = (s.na0 > 0 && s.na0 < n) ? s.na0 : n;   // zero-initialised state: all of W
+    if (tid == 0 && s.na) s.na[b] = na0;
     if (s_fail < 0 && n > 0 && tid < 32) {
-        // sA holds the factor in its lower triangle (only that part is read)
+        // sA holds the factor in its lower triangle (only that part is read); the first
+        // correction uses the active dimension na0 (leading block, AMB-19)
+        const int na = na0;
         const double* fn = s.fproj + (int64_t)b * (ld + 1);
-        double z0 = tid < n ? fn[tid] : 0.0, z1 = tid + 32 < n ? fn[tid + 32] : 0.0;
-        warp_chol_solve(sA, ld, n, &z0, &z1, tid);
-        if (tid < n) { s.E[tid * s.Bp + b] = z0; s.a_n[(int64_t)b * ld + tid] = z0; }
-        if (tid + 32 < n) { s.E[(tid + 32) * s.Bp + b] = z1; s.a_n[(int64_t)b * ld + tid + 32] = z1; }
+        double z0 = tid < na ? fn[tid] : 0.0, z1 = tid + 32 < na ? fn[tid + 32] : 0.0;
+        warp_chol_solve(sA, ld, na, &z0, &z1, tid);
+        if (tid < n) { z0 = tid < na ? z0 : 0.0; s.E[tid * s.Bp + b] = z0; s.a_n[(int64_t)b * ld + tid] = z0; }
+        if (tid + 32 < n) {
+            z1 = tid + 32 < na ? z1 : 0.0;
+            s.E[(tid + 32) * s.Bp + b] = z1;
+            s.a_n[(int64_t)b * ld + tid + 32] = z1;
+        }
     }
 }
 

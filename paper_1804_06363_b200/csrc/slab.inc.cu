@@ -112,6 +112,7 @@ SlabPlan slab_plan(const rbs_ctx* c, int B, const rbs_solve_opts* o, void* base)
     L.its = cv.take<int>(Bp);
     L.pivot = cv.take<int>(Bp);
     L.ints = cv.take<int>(8);
+    L.na = cv.take<int>(Bp);
     P.colP = cv.take<double>((size_t)Bp * (npad + 1) + 8);
     P.colF = cv.take<double>((size_t)Bp * 2 + 8);
     P.bytes = cv.off + 256;
@@ -252,6 +253,7 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     S.rho = L.rho; S.rr = L.rr; S.fnorm = L.fnorm; S.relres = L.relres; S.active = L.active;
     S.status = L.status; S.its = L.its; S.pivot = L.pivot; S.kcount = kcount; S.done = done;
     S.ticket = ticket; S.hist = L.hist;
+    set_active_dim(S, L.na, o, n);
     k_setup_reduced<<<Bp, 128, 0, st>>>(S, 0);
     CKL();
     ++launches;
@@ -455,6 +457,8 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     CK(cudaMemcpyAsync(hp.data(), L.pivot, Bp * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hrel.data(), L.relres, Bp * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hfn.data(), L.fnorm, Bp * 8, cudaMemcpyDeviceToHost, st));
+    ctx->last_na.assign(Bp, n);
+    CK(cudaMemcpyAsync(ctx->last_na.data(), L.na, Bp * 4, cudaMemcpyDeviceToHost, st));
     // true residual ||f - A x|| / ||f||: x halos, then per-slab residual partials
     halo(2, 1);
     for (Slab& q : P.sl) {
@@ -498,6 +502,7 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     if (history && L.hist)
         CK(cudaMemcpyAsync(history, L.hist, (size_t)B * (o->max_iter + 1) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    ctx->last_na.resize(B);
     for (int b = 0; b < B; ++b) {
         if (iters) iters[b] = hi[b];
         if (qstatus) qstatus[b] = hs[b];

@@ -396,3 +396,54 @@ def test_dist_slab_single_rank_nccl(orc, rbs):
     s.load_basis(res["W"], res["ANq"], res["fn"])
     out = s.solve_batch(mus, record_history=1)
     compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg")
+
+
+# ----------------------------------------------------------------------------- active RB dimension
+@pytest.mark.parametrize("dim,m,blocks,n,na,B", [
+    (2, 47, (3, 3), 24, 7, 9),       # fixed active dimension < n (iterations-vs-n study)
+    (2, 63, (3, 3), 40, 40, 5),      # n_active = n: same as the full solve
+    (3, 11, (2, 2, 2), 10, 4, 6),    # 3D flat kernels
+])
+@pytest.mark.parametrize("method", ["rbcg", "rbi"])
+def test_fixed_active_dimension(orc, rbs, dim, m, blocks, n, na, B, method):
+    """opts.n_active: leading-block reduced solves (DESIGN.md AMB-19) against the oracle."""
+    g, res = oracle_basis(orc, dim, m, blocks, n, max(30, n + 20), 2)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    rng = np.random.default_rng(300 + na)
+    mus = 0.1 * 100 ** rng.random((B, g.Q))
+    mi = 20000 if method == "rbcg" else 500000
+    out = s.solve_batch(mus, method=rbs.RBS_RBCG if method == "rbcg" else rbs.RBS_RBI,
+                        max_iter=mi, record_history=1, n_active=na)
+    assert np.all(out["n_active"] == na)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, method, max_iter=mi, n_active=na)
+
+
+@pytest.mark.parametrize("dim,m,blocks,n,na0,gamma,B", [
+    (2, 47, (3, 3), 24, 1, 3.0, 8),     # grows from 1 while the residual falls slowly
+    (2, 63, (3, 3), 40, 5, 1.5, 40),    # two sub-batches; multi-strip grid
+    (3, 11, (2, 2, 2), 10, 2, 4.0, 5),  # 3D
+])
+def test_adaptive_n_rule(orc, rbs, dim, m, blocks, n, na0, gamma, B):
+    """opts.gamma: the adaptive-n rule of PAPER.md:287 (RBCG); the final active
+    dimension of every query equals the oracle's trace, iterations/x/histories match."""
+    g, res = oracle_basis(orc, dim, m, blocks, n, max(30, n + 20), 2)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    rng = np.random.default_rng(400 + B)
+    mus = 0.1 * 100 ** rng.random((B, g.Q))
+    out = s.solve_batch(mus, record_history=1, n_active=na0, gamma=gamma)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg", n_active=na0, gamma=gamma)
+    grew = 0
+    for b, mu in enumerate(mus):
+        ref = g.rbcg(res["W"], res["ANq"], res["fn"], mu, n_active=na0, gamma=gamma)
+        assert int(out["n_active"][b]) == int(ref["active_n"][-1]), (b, out["n_active"][b], ref["active_n"])
+        grew += int(ref["active_n"][-1]) > na0
+    assert grew > 0   # the rule actually fired
+
+
+def test_active_dimension_errors(rbs):
+    import paper_1804_06363_b200 as r
+    s = rbs.Solver(2, 31, (2, 2)).load_basis(np.linalg.qr(np.random.default_rng(0).random((961, 6)))[0])
+    mus = np.ones((2, 4))
+    for kw in (dict(n_active=7), dict(n_active=-1), dict(gamma=-1.0), dict(method=r.RBS_RBI, gamma=2.0)):
+        with pytest.raises(RuntimeError):
+            s.solve_batch(mus, **kw)
