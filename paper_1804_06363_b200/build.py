@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in deps):
         return SO
     nd = nccl_dir()
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I" + os.path.join(nd, "include"), "-o", SO] + srcs + [
+    extra = os.environ.get("RBS_NVCC_EXTRA", "").split()   # instrumented builds (tools/)
+    cmd = [nvcc()] + NVCC_FLAGS + extra + ["-I" + os.path.join(nd, "include"), "-o", SO] + srcs + [
         "-lcudart", "-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2",
         "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     if verbose:

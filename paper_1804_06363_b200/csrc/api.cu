@@ -154,9 +154,11 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
+// k_smooth2 dynamic shared memory cap: 227 KB per CTA minus its static part
+constexpr int kSmooth2MaxDyn = 225 * 1024;
 template <int BP, bool R, int TX>
 void set_attrs_smooth2() {
-    const int mx = 214 * 1024;
+    const int mx = kSmooth2MaxDyn;
     cudaFuncSetAttribute(k_smooth2<BP, 0, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_smooth2<BP, 1, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_smooth2<BP, 2, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -397,6 +399,16 @@ void rbs_destroy(rbs_ctx* ctx) {
 const char* rbs_last_error(const rbs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
 
 int64_t rbs_last_launch_count(const rbs_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+#ifdef RBS_CLK
+// instrumented builds: per-warp cycle accounting of k_smooth2 (march2.cuh), read and reset
+int rbs_debug_s2clk(unsigned long long* host) {
+    if (cudaMemcpyFromSymbol(host, g_s2clk, sizeof(g_s2clk)) != cudaSuccess) return 1;
+    if (cudaMemcpyFromSymbol(host + 148 * 16 * 6, g_s2t, sizeof(g_s2t)) != cudaSuccess) return 1;
+    static unsigned long long zero[148 * 16 * 6];
+    return cudaMemcpyToSymbol(g_s2clk, zero, sizeof(zero)) != cudaSuccess;
+}
+#endif
 
 rbs_status rbs_last_n_active(const rbs_ctx* ctx, int* out) {
     if (!ctx || !out) return RBS_E_ARG;
@@ -840,7 +852,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
         a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
         pb(RBS_K_GS);
-        const size_t kMaxDyn = (size_t)214 * 1024;
+        const size_t kMaxDyn = (size_t)kSmooth2MaxDyn;
         int TX2 = 32;
         size_t sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad).total;
         if (sm2 > kMaxDyn) {

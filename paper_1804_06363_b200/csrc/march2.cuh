@@ -23,6 +23,28 @@
 
 namespace rbs {
 
+// RBS_CLK: per-warp cycle accounting of k_smooth2 (instrumented builds only, tools/s2clk.py)
+#ifdef RBS_CLK
+__device__ unsigned long long g_s2clk[148 * 16 * 6];
+__device__ unsigned long long g_s2t[148 * 3];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define S2CLK_ENTRY if (threadIdx.x == 0 && blockIdx.x < 148) g_s2t[blockIdx.x * 3] = gtimer();
+#define S2CLK_DECL unsigned long long c_[6] = {0, 0, 0, 0, 0, 0}; long long t_ = clock64(), u_; \
+    if (threadIdx.x == 0 && blockIdx.x < 148) g_s2t[blockIdx.x * 3 + 1] = gtimer();
+#define S2CLK(k) do { u_ = clock64(); c_[k] += (unsigned long long)(u_ - t_); t_ = u_; } while (0)
+#define S2CLK_FLUSH do { if (threadIdx.x == 0 && blockIdx.x < 148) g_s2t[blockIdx.x * 3 + 2] = gtimer(); \
+    if (lane == 0 && blockIdx.x < 148) for (int k_ = 0; k_ < 6; ++k_) \
+    atomicAdd(&g_s2clk[(blockIdx.x * 16 + warp) * 6 + k_], c_[k_]); } while (0)
+#else
+#define S2CLK_ENTRY
+#define S2CLK_DECL
+#define S2CLK(k) do {} while (0)
+#define S2CLK_FLUSH do {} while (0)
+#endif
 constexpr int kMT = kMarchThreads;        // 512 threads, 16 warps
 constexpr int kNW = kMT / 32;
 
@@ -116,6 +138,7 @@ struct Smooth2Smem {
 // before any update of that step.
 template <int BP, int S, bool HAS_RHS, int TX>
 __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
+    S2CLK_ENTRY
     if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
     constexpr int TW = TX + 2 * S;
@@ -224,20 +247,33 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     const int hwg = S - 1 - sgi;
     const int rlog = max(1, y0 - hwg), rhig = min(m, y1 - 1 + hwg);
     const int colg = a.seq[sgi] - xlo;                       // colour term of this group's sweep
+    // block column info of this thread's nodes (both parities) in registers: the
+    // h^2/(4 theta) load of a node does not wait on a column-table load
+    constexpr int ITER = (NPAIRS + PPI - 1) / PPI;
+    int cu0[ITER], cu1[ITER];
+#pragma unroll
+    for (int i = 0; i < ITER; ++i) {
+        const int pp = p0 + i * PPI;
+        cu0[i] = pp < NPAIRS ? s_cu[2 * pp] : -1;
+        cu1[i] = pp < NPAIRS ? s_cu[2 * pp + 1] : -1;
+    }
     const int nco = min(S + TX - 1, cmax) - S + 1;        // owned output columns
     double* yg = a.Y + ((int64_t)(Jfirst - (2 * S + 1) - 1) * m + (x0 - 1)) * BP;
 
+    S2CLK_DECL
     for (int t = 0; t < nsteps; ++t, yg += (int64_t)m * BP) {
         const int Jb = Jfirst + t;
         if (tid == 0) {
             if (Jb + kS2D <= JlastP) issue_w(t + kS2D);
             if (has_rhs && Jb <= JlastP) issue_r(t);
         }
+        S2CLK(0);
         if (tensor) {
             // ---- stage P: y0 of row Jb (lag 0) --------------------------------
             if (Jb <= JlastP) {
                 const int ws = t % kS2WR;
                 mbar_wait(&wbar[ws], (uint32_t)((t / kS2WR) & 1));
+                S2CLK(1);
                 const int yn = YR + (t & (kS2YR - 1)) * VROW;
                 const int xs = XO + ws * VROW;
                 if (Jb < 1 || Jb > m) {
@@ -292,6 +328,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
             constexpr int RL = S == 0 ? 1 : 2;
             if (has_rhs && t >= RL && Jb - RL <= JlastP)
                 mbar_wait(&rbar[(t - RL) & (kS2RR - 1)], (uint32_t)(((t - RL) >> 3) & 1));
+            S2CLK(1);
             // ---- half-sweep of this group on row R = Jb - 2(grp+1) ----------------
             const int R = Jb - 2 * (sgi + 1);
             if (S > 0 && R >= rlog && R <= rhig && qact) {
@@ -305,17 +342,16 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
                 const int by1 = axis_block(a.g, R, a.g.py) * a.g.px;
                 const bool rowu = by0 == by1;
                 const uint32_t chb = sbase + 8u * (CHO + by0 * BP + b);
-                const uint32_t cub = smem_u32(s_cu);
-#pragma unroll 1
-                for (int p = p0; p < NPAIRS; p += PPI) {
+#pragma unroll
+                for (int i = 0; i < ITER; ++i) {
+                    const int p = p0 + i * PPI;
                     const int col = 2 * p + par;
-                    if (col < c0g || col > c1g) continue;
+                    if (p >= NPAIRS || col < c0g || col > c1g) continue;
+                    const int cu = par ? cu1[i] : cu0[i];
                     const uint32_t o = 8u * col * BP;
                     const double n0 = ldsd(yc + o - 8 * BP), n1 = ldsd(yc + o + 8 * BP);
                     const double n2 = ldsd(ydn + o), n3 = ldsd(yup + o);
                     const double rh = HAS_RHS ? ldsd(rrw + o) : rconst;
-                    int cu;
-                    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(cu) : "r"(cub + 4u * col) : "memory");
                     double v;
                     if (rowu && cu >= 0) {
                         v = fma(ldsd(chb + 8u * cu * BP), rh, 0.25 * ((n0 + n1) + (n2 + n3)));
@@ -328,6 +364,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
                     stsd(yc + o, v);
                 }
             }
+            S2CLK(2);
             // ---- output row Ro = Jb - (2S+1): stores + y^T r, y^T y -----------------
             const int Ro = Jb - (2 * S + 1);
             if (Ro >= y0 && Ro < y1) {
@@ -347,8 +384,11 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
                 }
             }
         }
+        S2CLK(3);
         __syncthreads();
+        S2CLK(4);
     }
+    S2CLK_FLUSH;
     if (!a.last) return;
     // ---- partials and RBCG Step 10 in the last CTA (rings are dead) ----------
     double* s_a = smd;
