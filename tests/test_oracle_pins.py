@@ -104,6 +104,41 @@ def test_rbgs_is_textbook_gs_in_red_black_order(orc, dim, m, blocks):
     assert (red[0] != y0[0]) == (par == 0)
 
 
+@pytest.mark.parametrize("dim,m,blocks,omega,sweeps", [(2, 7, (3, 3), 1.0, 1), (2, 6, (2, 2), 0.8, 2),
+                                                       (3, 4, (2, 2, 2), 2.0 / 3.0, 3)])
+def test_jacobi_is_textbook_damped_jacobi(orc, dim, m, blocks, omega, sweeps):
+    """S = Jacobi ("the smoother (Jacobi or Gauss-Seidel)"): each sweep is
+    y <- y + omega D^-1 (b - A y) on the independently assembled matrix (tests/refs.py)."""
+    g = orc.Grid(dim, m, blocks)
+    mu = rand_mu(g.Q)
+    A = refs.cellwise_fd(dim, m, blocks, mu).toarray()
+    b = RNG.standard_normal(g.N)
+    y = RNG.standard_normal(g.N)
+    got = g.smooth(mu, b, y, orc.JACOBI, sweeps, omega)
+    d = np.diag(A)
+    for _ in range(sweeps):
+        y = y + omega * (b - A @ y) / d
+    assert np.abs(got - y).max() <= 1e-12 * np.abs(y).max()
+
+
+def test_jacobi_contracts_on_the_laplacian(orc):
+    """undamped Jacobi does not increase ||x - x*||_inf on the constant-
+    coefficient Laplacian (||D^-1 (L + U)||_inf = 1) and reduces it over sweeps; x* is fixed."""
+    g = orc.Grid(2, 9, (2, 2))
+    mu = np.ones(g.Q)
+    A = refs.cellwise_fd(2, 9, (2, 2), mu).toarray()
+    b = RNG.standard_normal(g.N)
+    xs = np.linalg.solve(A, b)
+    assert np.abs(g.smooth(mu, b, xs, orc.JACOBI, 1, 1.0) - xs).max() <= 1e-13 * np.abs(xs).max()
+    y = RNG.standard_normal(g.N)
+    e0 = np.abs(y - xs).max()
+    for _ in range(4):
+        y2 = g.smooth(mu, b, y, orc.JACOBI, 1, 1.0)
+        assert np.abs(y2 - xs).max() <= np.abs(y - xs).max() * (1 + 1e-14)   # ||J||_inf = 1
+        y = y2
+    assert np.abs(y - xs).max() < e0
+
+
 def test_symmetric_rbgs_is_rbr_bitwise(orc):
     """R,B,B,R == R,B,R bitwise (the repeated black half-sweep is a no-op, AMB-6)."""
     g = orc.Grid(2, 13, (3, 3))
