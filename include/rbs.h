@@ -66,7 +66,11 @@ typedef enum {
 } rbs_qstatus;
 
 enum { RBS_RBI = 0, RBS_RBCG = 1 };
-enum { RBS_SMOOTH_SYM_RBGS = 0, RBS_SMOOTH_FWD_RBGS = 1 };
+/* smoother S of PAPER.md:148-153 (eq8), "the smoother (Jacobi or Gauss-Seidel)":
+ * red-black Gauss-Seidel, symmetric (R,B,R per sweep) or forward (R,B) -- AMB-5/6 --
+ * or damped Jacobi y <- y + omega D^-1 (b - A y) (opts.omega; flat kernels, not with
+ * mesh slabs) */
+enum { RBS_SMOOTH_SYM_RBGS = 0, RBS_SMOOTH_FWD_RBGS = 1, RBS_SMOOTH_JACOBI = 2 };
 enum { RBS_MEM_DEVICE = 0, RBS_MEM_HOST = 1 };
 enum { RBS_GREEDY_PLAIN = 0, RBS_GREEDY_ADAPTIVE = 1 };
 
@@ -123,7 +127,8 @@ typedef struct {
     int method;          /* RBS_RBI | RBS_RBCG (default RBCG) */
     double tol;          /* relative residual ||r||/||f|| (default 1e-10, AMB-7) */
     int max_iter;        /* default 20000 (RBCG) -- RBI callers set e.g. 500000 */
-    int smoother;        /* RBS_SMOOTH_SYM_RBGS (default) | RBS_SMOOTH_FWD_RBGS (AMB-5/6) */
+    int smoother;        /* RBS_SMOOTH_SYM_RBGS (default) | RBS_SMOOTH_FWD_RBGS (AMB-5/6) |
+                            RBS_SMOOTH_JACOBI */
     int sweeps;          /* nu >= 0 (default 1); 0 = no smoothing (Lemma 2 tests) */
     double delta;        /* PRECOND threshold (default 1e-12, AMB-11) */
     int record_history;  /* 1: fill history[B][max_iter+1] */
@@ -139,6 +144,7 @@ typedef struct {
                             each x-update, if ||r_k|| / ||r_{k+1}|| < gamma the active
                             dimension grows by one (capped at n) for the next preconditioner
                             application; start value n_active.  Final values: rbs_last_n_active */
+    double omega;        /* Jacobi damping, 0 < omega < 2 (default 1); ignored by Gauss-Seidel */
 } rbs_solve_opts;
 
 void rbs_default_opts(rbs_solve_opts* opts);

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "librbs.so")
 
 RBS_RBI, RBS_RBCG = 0, 1
-RBS_SMOOTH_SYM_RBGS, RBS_SMOOTH_FWD_RBGS = 0, 1
+RBS_SMOOTH_SYM_RBGS, RBS_SMOOTH_FWD_RBGS, RBS_SMOOTH_JACOBI = 0, 1, 2
 RBS_MEM_DEVICE, RBS_MEM_HOST = 0, 1
 RBS_GREEDY_PLAIN, RBS_GREEDY_ADAPTIVE = 0, 1
 QSTATUS = {0: "CONVERGED", 1: "MAXIT", 2: "REDUCED_NOT_SPD", 3: "CURVATURE", 4: "PRECOND",
@@ -34,7 +34,8 @@ class rbs_solve_opts(C.Structure):
     _fields_ = [("method", C.c_int), ("tol", C.c_double), ("max_iter", C.c_int),
                 ("smoother", C.c_int), ("sweeps", C.c_int), ("delta", C.c_double),
                 ("record_history", C.c_int), ("x_location", C.c_int), ("graph_chunk", C.c_int),
-                ("profile", C.c_int), ("n_active", C.c_int), ("gamma", C.c_double)]
+                ("profile", C.c_int), ("n_active", C.c_int), ("gamma", C.c_double),
+                ("omega", C.c_double)]
 
 
 _lib = None

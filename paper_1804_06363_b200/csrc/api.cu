@@ -250,7 +250,7 @@ BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
 
 // solve workspace
 struct SolveLayout {
-    double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout;
+    double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout, *T;
     double *theta, *fproj, *L, *Ainv, *E, *a_n, *partP, *partF;
     double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist;
     int *active, *status, *its, *pivot, *ints, *na;
@@ -264,7 +264,9 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     SolveLayout L{};
     const bool cg = o->method == RBS_RBCG;
     L.X = cv.take<double>(vec);
-    L.X2 = (!cg && c->g.dim == 2) ? cv.take<double>(vec) : nullptr;   // RBI ping-pong (march)
+    L.X2 = (!cg && c->g.dim == 2 && o->smoother != RBS_SMOOTH_JACOBI) ? cv.take<double>(vec)
+                                                                        : nullptr;   // RBI ping-pong (march)
+    L.T = o->smoother == RBS_SMOOTH_JACOBI ? cv.take<double>(vec) : nullptr;   // Jacobi ping-pong
     L.R = cg ? cv.take<double>(vec) : nullptr;
     L.P0 = cg ? cv.take<double>(vec) : nullptr;
     L.P1 = cg ? cv.take<double>(vec) : nullptr;
@@ -308,8 +310,11 @@ void set_active_dim(SolveState& S, int* na, const rbs_solve_opts* o, int n) {
 rbs_status check_opts(rbs_ctx* ctx, const rbs_solve_opts* o) {
     if (!o) return fail(ctx, RBS_E_ARG, "opts is NULL");
     if (o->method != RBS_RBI && o->method != RBS_RBCG) return fail(ctx, RBS_E_ARG, "bad method");
-    if (o->smoother != RBS_SMOOTH_SYM_RBGS && o->smoother != RBS_SMOOTH_FWD_RBGS)
-        return fail(ctx, RBS_E_UNSUPPORTED, "smoother must be SYM_RBGS or FWD_RBGS");
+    if (o->smoother != RBS_SMOOTH_SYM_RBGS && o->smoother != RBS_SMOOTH_FWD_RBGS &&
+        o->smoother != RBS_SMOOTH_JACOBI)
+        return fail(ctx, RBS_E_UNSUPPORTED, "smoother must be SYM_RBGS, FWD_RBGS or JACOBI");
+    if (o->smoother == RBS_SMOOTH_JACOBI && !(o->omega > 0.0 && o->omega < 2.0))
+        return fail(ctx, RBS_E_ARG, "Jacobi damping omega must be in (0, 2)");
     if (o->sweeps < 0 || o->sweeps > 64) return fail(ctx, RBS_E_ARG, "sweeps out of range");
     if (o->max_iter < 0) return fail(ctx, RBS_E_ARG, "max_iter < 0");
     if (!(o->tol >= 0.0)) return fail(ctx, RBS_E_ARG, "tol must be >= 0");
@@ -603,6 +608,7 @@ void rbs_default_opts(rbs_solve_opts* o) {
     o->profile = 0;
     o->n_active = 0;
     o->gamma = 0.0;
+    o->omega = 1.0;
 }
 
 rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opts* o, size_t* bytes) {
@@ -631,6 +637,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     if (s0 != RBS_OK) return s0;
     if (ctx->nslab > 1 || ctx->dist) {
         if (rhs_dev) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: rhs override not supported");
+        if (o->smoother == RBS_SMOOTH_JACOBI)
+            return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: Jacobi smoother not supported");
         CK(cudaSetDevice(ctx->device));
         return solve_slabs(ctx, B, mu_host, o, X, iters, qstatus, relres, true_relres, a_n, history,
                            workspace_dev, workspace_bytes, (cudaStream_t)stream);
@@ -758,7 +766,47 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         pe();
         return 1;
     };
+    const bool jac = o->smoother == RBS_SMOOTH_JACOBI;
+    // Jacobi: sweeps alternate between Ys and the other buffer (T, or Yf when Ys == T);
+    // the result must end in Yf (a device copy when the parity leaves it elsewhere)
+    auto smooth_jac = [&](double* Ys, double* Yf, const double* rhs, double rconst, bool last, int init) {
+        GSArgs a{};
+        a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
+        a.Rhs = rhs; a.rconst = rconst; a.init = init; a.s = S; a.done = done; a.omega = o->omega;
+        double* buf[2] = {Ys, Ys == L.T ? Yf : L.T};
+        const int nu = o->sweeps;
+        int cnt = 0;
+        for (int t = 0; t < nu; ++t) {
+            a.Yin = buf[t & 1];
+            a.Y = buf[(t + 1) & 1];
+            const bool l = last && t + 1 == nu;
+            pb(RBS_K_GS);
+            if (g.dim == 2) {
+                if (l) k_jac<2, true><<<nctf, kFlat, fsm, st>>>(a);
+                else k_jac<2, false><<<nctf, kFlat, fsm, st>>>(a);
+            } else {
+                if (l) k_jac<3, true><<<nctf, kFlat, fsm, st>>>(a);
+                else k_jac<3, false><<<nctf, kFlat, fsm, st>>>(a);
+            }
+            pe();
+            ++cnt;
+        }
+        if (buf[nu & 1] != Yf) {
+            cudaMemcpyAsync(Yf, buf[nu & 1], (size_t)ctx->N8 * Bp * 8, cudaMemcpyDeviceToDevice, st);  // CKL after
+        }
+        if (nu == 0 && last) {   // no sweep: y = y0, Step 10 partials by an empty GS pass
+            a.Y = Yf;
+            a.color = -1;
+            pb(RBS_K_GS);
+            if (g.dim == 2) k_gs<2, true><<<nctf, kFlat, fsm, st>>>(a);
+            else k_gs<3, true><<<nctf, kFlat, fsm, st>>>(a);
+            pe();
+            ++cnt;
+        }
+        return cnt;
+    };
     auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last, int init) {
+        if (jac) return smooth_jac(Yv, Yv, rhs, rconst, last, init);
         GSArgs a{};
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.Y = Yv; a.Rhs = rhs; a.rconst = rconst; a.init = init; a.s = S; a.done = done;
@@ -841,7 +889,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
 
     // 2D: prolongation + all half-sweeps (+ y^T r) in one row-marching pass
-    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps;
+    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac;
     auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
                      int init) {
         SmoothMarchArgs a{};
@@ -884,7 +932,11 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     // ---- RBCG Step 2-3: y_0 = RBI(A, r_0, W, 1), rho_0 = r_0^T y_0 ------------
     if (cg) {
         if (use_march) launches += march(nullptr, L.Y, L.R, 0.0, true, 1);   // + rho_0, PRECOND
-        else {
+        else if (jac) {
+            double* y0b = (o->sweeps & 1) ? L.T : L.Y;
+            launches += prolong(y0b, 0);
+            launches += smooth_jac(y0b, L.Y, L.R, 0.0, true, 1);
+        } else {
             launches += prolong(L.Y, 0);
             launches += smooth(L.Y, L.R, 0.0, true, 1);
         }
@@ -907,6 +959,10 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Step 8
             if (use_march) {
                 c += march(nullptr, L.Y, L.R, 0.0, true, 0);   // Step 9 + Step 10 (last CTA)
+            } else if (jac) {
+                double* y0b = (o->sweeps & 1) ? L.T : L.Y;
+                c += prolong(y0b, 0);                          // Step 9: y0 = W e
+                c += smooth_jac(y0b, L.Y, L.R, 0.0, true, 0);  // Jacobi sweeps; Step 10
             } else {
                 c += prolong(L.Y, 0);             // Step 9: y0 = W e
                 c += smooth(L.Y, L.R, 0.0, true, 0);  // y = S(A, r, y0); Step 10 in last CTA
@@ -927,10 +983,10 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
     const int chunk = o->graph_chunk;
     char keybuf[512];
-    snprintf(keybuf, sizeof keybuf, "%p|%p|%d|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%d|%.17g",
+    snprintf(keybuf, sizeof keybuf, "%p|%p|%d|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%d|%.17g|%d|%.17g|%.17g",
              workspace_dev, (void*)Fv, B, Bp, o->method, o->smoother, o->sweeps, o->max_iter, chunk,
              o->tol, o->delta, o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist,
-             rhs_dev ? 1 : 0, n, npad, ctx->fconst);
+             rhs_dev ? 1 : 0, n, npad, ctx->fconst, o->n_active, o->gamma, o->omega);
     const std::string key(keybuf);
     if (prof) {
         // eager launches, one iteration at a time, events on the launching stream
@@ -1020,7 +1076,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     // X: [N8][Bp] -> [B][N]
     double* xdst = o->x_location == RBS_MEM_HOST ? L.Xout : X;
     const double* Xfin = L.X;
-    if (L.X2) {  // RBI ping-pong: corrections applied so far decide the buffer
+    if (L.X2 && use_march) {  // RBI ping-pong: corrections applied so far decide the buffer
         int kc = 0;
         CK(cudaMemcpyAsync(&kc, kcount, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));

@@ -404,9 +404,57 @@ struct GSArgs {
     const int* done;
     int col0;                 // LAST: first partial column (mesh slabs)
     int ext;                  // LAST: 1 = partials only, Step 10 by k_slab_beta
+    const double* Yin;        // k_jac: sweep input (Y is its output)
+    double omega;             // k_jac: damping
 };
 
 constexpr int kGsUnroll = 4;
+
+// LAST pass of the smoother: y^T r, y^T y partials of this CTA and RBCG Step 10
+// (beta = y_{k+1}^T r_{k+1} / y_k^T r_k) in the last CTA (AMB-11)
+__device__ __forceinline__ void gs_step10(GSArgs& a, double yr, double yy) {
+    __shared__ double s_a[kFlat], s_b[kFlat];
+    __shared__ double s_yr[kMaxBatch], s_yy[kMaxBatch];
+    __shared__ int s_last;
+    SolveState& s = a.s;
+    s_a[threadIdx.x] = yr;
+    s_b[threadIdx.x] = yy;
+    __syncthreads();
+    if (threadIdx.x < a.Bp) {
+        double sr = 0.0, sy = 0.0;
+        for (int t = threadIdx.x; t < kFlat; t += a.Bp) {
+            sr += s_a[t];
+            sy += s_b[t];
+        }
+        s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + a.col0 + blockIdx.x] = sr;
+        s.partF[((int64_t)threadIdx.x * 2 + 1) * s.nctf + a.col0 + blockIdx.x] = sy;
+    }
+    if (!a.ext && cta_is_last(s.ticket, &s_last)) {
+        cta_sum_slot(s, 0, s_a, s_yr);
+        cta_sum_slot(s, 1, s_a, s_yy);
+        if (threadIdx.x < s.Bp) {
+            const int bb = threadIdx.x;
+            if (s.active[bb]) {
+                const double r1 = s_yr[bb], y2 = s_yy[bb];
+                if (!(r1 > s.delta * sqrt(y2) * sqrt(s.rr[bb]))) {
+                    s.status[bb] = isfinite(r1) ? Q_PRECOND : Q_NONFINITE;
+                    s.active[bb] = 0;
+                    s.beta[bb] = 0.0;
+                } else {
+                    s.beta[bb] = a.init ? 0.0 : r1 / s.rho[bb];
+                    s.rho[bb] = r1;
+                }
+            }
+        }
+        __threadfence();
+        const int any = cta_any_active(s);
+        if (threadIdx.x == 0) {
+            *(volatile int*)s.done = any ? 0 : 1;
+            if (!a.init) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
+        }
+        release_ticket(s.ticket);
+    }
+}
 
 template <int DIM, bool LAST>
 __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
@@ -457,49 +505,65 @@ __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
             }
         }
     }
-    if (LAST) {
-        __shared__ double s_a[kFlat], s_b[kFlat];
-        __shared__ double s_yr[kMaxBatch], s_yy[kMaxBatch];
-        __shared__ int s_last;
-        SolveState& s = a.s;
-        s_a[threadIdx.x] = yr;
-        s_b[threadIdx.x] = yy;
-        __syncthreads();
-        if (threadIdx.x < a.Bp) {
-            double sr = 0.0, sy = 0.0;
-            for (int t = threadIdx.x; t < kFlat; t += a.Bp) {
-                sr += s_a[t];
-                sy += s_b[t];
-            }
-            s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + a.col0 + blockIdx.x] = sr;
-            s.partF[((int64_t)threadIdx.x * 2 + 1) * s.nctf + a.col0 + blockIdx.x] = sy;
-        }
-        if (!a.ext && cta_is_last(s.ticket, &s_last)) {
-            cta_sum_slot(s, 0, s_a, s_yr);
-            cta_sum_slot(s, 1, s_a, s_yy);
-            if (threadIdx.x < s.Bp) {
-                const int bb = threadIdx.x;
-                if (s.active[bb]) {
-                    const double r1 = s_yr[bb], y2 = s_yy[bb];
-                    if (!(r1 > s.delta * sqrt(y2) * sqrt(s.rr[bb]))) {
-                        s.status[bb] = isfinite(r1) ? Q_PRECOND : Q_NONFINITE;
-                        s.active[bb] = 0;
-                        s.beta[bb] = 0.0;
-                    } else {
-                        s.beta[bb] = a.init ? 0.0 : r1 / s.rho[bb];
-                        s.rho[bb] = r1;
-                    }
+    if (LAST) gs_step10(a, yr, yy);
+}
+
+// ---------------------------------------------------------------------------
+// Damped Jacobi sweep ("the smoother (Jacobi or Gauss-Seidel)"):
+//   y_out = y_in + omega (g - y_in), g = the Gauss-Seidel point value of y_in,
+// i.e. y_in + omega D^-1 (b - A y_in).  Ping-pong buffers; frozen lanes copy.
+// ---------------------------------------------------------------------------
+template <int DIM, bool LAST>
+__global__ void __launch_bounds__(kFlat, 2) k_jac(GSArgs a) {
+    if (a.done && ld_flag(a.done)) return;
+    extern __shared__ double smem[];
+    double* s_th = smem;
+    int* s_act = (int*)(s_th + a.g.Q * a.Bp);
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kFlat) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kFlat) s_act[t] = a.active[t];
+    __syncthreads();
+    double yr = 0.0, yy = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kFlat;
+    const int b = threadIdx.x & (a.Bp - 1);
+    const bool act = s_act[b] != 0;
+    for (int64_t e0 = blockIdx.x * (int64_t)kFlat + threadIdx.x; e0 < a.NB; e0 += kGsUnroll * stride) {
+        double nb[kGsUnroll][2 * DIM], rhs[kGsUnroll], yi[kGsUnroll];
+        int I[kGsUnroll], J[kGsUnroll], K[kGsUnroll];
+        bool ok[kGsUnroll];
+#pragma unroll
+        for (int u = 0; u < kGsUnroll; ++u) {
+            const int64_t e = e0 + u * stride;
+            ok[u] = e < a.NB;
+            rhs[u] = a.rconst;
+            yi[u] = 0.0;
+            if (ok[u]) {
+                const int64_t i = e >> a.lgB;
+                node_coords(a.g, (uint32_t)i, I[u], J[u], K[u]);
+                yi[u] = a.Yin[e];
+                if (act) {
+                    if (a.Rhs) rhs[u] = __ldg(a.Rhs + e);
+                    node_nbrs<DIM>(a.g, a.Yin, a.Bp, i, b, I[u], J[u], K[u], nb[u]);
                 }
             }
-            __threadfence();
-            const int any = cta_any_active(s);
-            if (threadIdx.x == 0) {
-                *(volatile int*)s.done = any ? 0 : 1;
-                if (!a.init) *(volatile int*)s.kcount = *(volatile int*)s.kcount + 1;
+        }
+#pragma unroll
+        for (int u = 0; u < kGsUnroll; ++u) {
+            if (!ok[u]) continue;
+            double yo = yi[u];
+            if (act) {
+                double k[2 * DIM];
+                node_kappa<DIM>(a.g, s_th, a.Bp, b, I[u], J[u], K[u], k);
+                const double gv = gs_value<DIM>(a.g, k, rhs[u], nb[u]);
+                yo = yi[u] + a.omega * (gv - yi[u]);
+                if (LAST && (DIM == 2 || owned(a.g, K[u]))) {
+                    yr = fma(yo, rhs[u], yr);
+                    yy = fma(yo, yo, yy);
+                }
             }
-            release_ticket(s.ticket);
+            a.Y[e0 + u * stride] = yo;
         }
     }
+    if (LAST) gs_step10(a, yr, yy);
 }
 
 // ---------------------------------------------------------------------------

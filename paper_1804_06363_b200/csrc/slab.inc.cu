@@ -410,9 +410,10 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     };
     const int chunk = o->graph_chunk;
     char keybuf[512];
-    snprintf(keybuf, sizeof keybuf, "slab|%d|%d|%p|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%.17g",
+    snprintf(keybuf, sizeof keybuf, "slab|%d|%d|%p|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%.17g|%d|%.17g",
              G, (int)dist, workspace_dev, B, Bp, o->smoother, o->sweeps, o->max_iter, chunk, o->tol, o->delta,
-             o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist, n, npad, ctx->fconst);
+             o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist, n, npad, ctx->fconst, o->n_active,
+             o->gamma);
     const std::string key(keybuf);
     if (!ctx->gexec || ctx->gkey != key) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }

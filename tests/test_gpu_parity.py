@@ -447,3 +447,57 @@ def test_active_dimension_errors(rbs):
     for kw in (dict(n_active=7), dict(n_active=-1), dict(gamma=-1.0), dict(method=r.RBS_RBI, gamma=2.0)):
         with pytest.raises(RuntimeError):
             s.solve_batch(mus, **kw)
+
+
+# ----------------------------------------------------------------------------- Jacobi smoother
+@pytest.mark.parametrize("dim,m,blocks,n,B,omega,sweeps,method", [
+    (2, 37, (3, 3), 12, 5, 1.0, 1, "rbcg"),     # undamped, odd sweeps: prolongation into T
+    (2, 47, (3, 3), 20, 8, 0.8, 2, "rbcg"),     # even sweeps
+    (3, 11, (2, 2, 2), 10, 3, 0.8, 1, "rbcg"),  # 3D
+    (2, 37, (3, 3), 12, 5, 0.8, 1, "rbi"),      # RBI: odd sweeps end in T -> copy
+    (2, 31, (2, 2), 8, 9, 0.7, 2, "rbi"),
+    (3, 9, (2, 2, 2), 8, 4, 0.8, 3, "rbi"),
+])
+def test_jacobi_smoother(orc, rbs, dim, m, blocks, n, B, omega, sweeps, method):
+    """S = damped Jacobi ("the smoother (Jacobi or Gauss-Seidel)") in RBI and RBCG."""
+    g, res = oracle_basis(orc, dim, m, blocks, n, max(30, n + 20), 2)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    rng = np.random.default_rng(500 + B)
+    mus = 0.1 * 100 ** rng.random((B, g.Q))
+    mi = 20000 if method == "rbcg" else 500000
+    out = s.solve_batch(mus, method=rbs.RBS_RBCG if method == "rbcg" else rbs.RBS_RBI, max_iter=mi,
+                        record_history=1, smoother=rbs.RBS_SMOOTH_JACOBI, sweeps=sweeps, omega=omega)
+    assert all(st == "CONVERGED" for st in out["status"]), out["status"]
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, method, max_iter=mi, smoother=orc.JACOBI,
+            sweeps=sweeps, omega=omega)
+
+
+def test_jacobi_errors_and_graph_reuse(orc, rbs):
+    """omega outside (0, 2) is an argument error; one Solver alternating smoothers and
+    active dimensions rebuilds its iteration graph (results equal fresh solves)."""
+    g, res = oracle_basis(orc, 2, 31, (2, 2), 8, 30, 2)
+    s = rbs.Solver(2, 31, (2, 2)).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = 0.1 * 100 ** np.random.default_rng(7).random((3, g.Q))
+    for om in (0.0, 2.0, -1.0):
+        with pytest.raises(RuntimeError):
+            s.solve_batch(mus, smoother=rbs.RBS_SMOOTH_JACOBI, omega=om)
+    a = s.solve_batch(mus)
+    b = s.solve_batch(mus, smoother=rbs.RBS_SMOOTH_JACOBI, omega=0.9)
+    c = s.solve_batch(mus, n_active=3)
+    d = s.solve_batch(mus)
+    assert np.array_equal(a["X"].cpu().numpy(), d["X"].cpu().numpy())
+    for out, kw in ((b, dict(smoother=orc.JACOBI, omega=0.9)), (c, dict(n_active=3))):
+        compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg", check_hist=False, **kw)
+
+
+@pytest.mark.parametrize("smoother,sweeps", [(0, 2), (1, 3)])
+def test_rbi_many_half_sweeps_flat_path(orc, rbs, smoother, sweeps):
+    """RBI on a 2D grid with more half-sweeps than the row march holds (flat kernels)."""
+    c = CONFIGS["c1"]
+    g, res = c1_basis(orc)
+    s = rbs.Solver(c.dim, c.m, c.blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = query_set(c)[:3]
+    out = s.solve_batch(mus, method=rbs.RBS_RBI, max_iter=500000, smoother=smoother, sweeps=sweeps,
+                        record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbi", max_iter=500000, smoother=smoother,
+            sweeps=sweeps)
