@@ -685,7 +685,8 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
 // inverse formed once per query at setup.
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 512;
-constexpr int kRsChunks = 8;      // chunks per row (rows <= 65 -> 520 > 512 handled by loop)
+constexpr int kRsChunks = 32;     // chunks per row (one warp lane each in the second stage)
+constexpr int kRsPer = 12;        // columns of a chunk loaded together
 
 __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
     if (ld_flag(s.done)) return;
@@ -697,7 +698,19 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
     const int b = blockIdx.x, tid = threadIdx.x;
     const int rows = s.npad + 1, nr = s.n + 1;     // rows 0..n-1 and the rr row (npad)
     const bool act = s.active[b] != 0;
+    // A_n^{-1} row slice of this thread for the fixed-order matvec below, loaded
+    // before the partial sums so the two global-load latencies overlap
+    const int mi = tid >> 3, ml = tid & 7;
+    double ai[kMaxN / 8];
+    {
+        const bool mv = act && !s.tri && mi < s.n;
+        const double* Ai = s.Ainv + (int64_t)b * s.npad * s.npad + mi * s.npad;
+#pragma unroll
+        for (int k = 0; k < kMaxN / 8; ++k) ai[k] = (mv && ml + 8 * k < s.n) ? __ldcg(Ai + ml + 8 * k) : 0.0;
+    }
     if (act) {
+        // two-stage fixed-order sums: 32 chunks of <= 10 columns per row (all loads of a
+        // chunk in flight at once), then one warp per row combines its 32 chunks
         const int per = (s.nct + kRsChunks - 1) / kRsChunks;
         for (int t = tid; t < nr * kRsChunks; t += kRsThreads) {
             const int r = t / kRsChunks, c = t - r * kRsChunks;
@@ -705,21 +718,26 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             const double* p = s.partP + ((int64_t)b * rows + j) * s.nct;
             const int c0 = c * per, c1 = min(s.nct, c0 + per);
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int k = c0;
-            for (; k + 3 < c1; k += 4) {
-                a0 += __ldcg(p + k);
-                a1 += __ldcg(p + k + 1);
-                a2 += __ldcg(p + k + 2);
-                a3 += __ldcg(p + k + 3);
+            for (int k0 = c0; k0 < c1; k0 += kRsPer) {
+                double v[kRsPer];
+#pragma unroll
+                for (int u = 0; u < kRsPer; ++u) v[u] = k0 + u < c1 ? __ldcg(p + k0 + u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < kRsPer; u += 4) {
+                    a0 += v[u];
+                    a1 += v[u + 1];
+                    a2 += v[u + 2];
+                    a3 += v[u + 3];
+                }
             }
-            for (; k < c1; ++k) a0 += __ldcg(p + k);
             s_chunk[r * kRsChunks + c] = (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
-        if (tid < nr) {
-            double v = 0.0;
-            for (int c = 0; c < kRsChunks; ++c) v += s_chunk[tid * kRsChunks + c];
-            s_rn[tid < s.n ? tid : s.npad] = v;
+        for (int r = tid >> 5; r < nr; r += kRsThreads / 32) {
+            double v = s_chunk[r * kRsChunks + (tid & 31)];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((tid & 31) == 0) s_rn[r < s.n ? r : s.npad] = v;
         }
         __syncthreads();
         if (tid == 0) {
@@ -762,13 +780,14 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             }
         } else {
         // e = A_n^{-1} r_n: row i by 8 threads (fixed order), frozen lanes get e = 0
-        const double* Ai = s.Ainv + (int64_t)b * s.npad * s.npad;
-        for (int t = tid; t < s.n * 8; t += kRsThreads) {
-            const int i = t >> 3, l = t & 7;
+        if (mi < s.n) {
             double v = 0.0;
-            if (s_go)
-                for (int j = l; j < s.n; j += 8) v = fma(Ai[i * s.npad + j], s_rn[j], v);
-            s_e[t] = v;
+            if (s_go) {
+#pragma unroll
+                for (int k = 0; k < kMaxN / 8; ++k)
+                    if (ml + 8 * k < s.n) v = fma(ai[k], s_rn[ml + 8 * k], v);
+            }
+            s_e[tid] = v;
         }
         __syncthreads();
         if (tid < s.n) {
