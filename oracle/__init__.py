@@ -66,28 +66,48 @@ def _blocks(blocks):
 
 
 class Grid:
-    """dim, m (interior nodes per axis), blocks (subdomains per axis)."""
+    """dim, m (interior nodes per axis), blocks (subdomains per axis) -- or faces: a
+    general affine operator given by face coefficients faces[q][d][idx] (Q x dim x
+    (m+1) m^(dim-1), layout in oracle.c; NEXT(4), DESIGN.md AMB-23)."""
 
-    def __init__(self, dim: int, m: int, blocks):
-        self.dim, self.m, self.blocks = int(dim), int(m), tuple(int(b) for b in blocks)
-        assert len(self.blocks) == self.dim
+    def __init__(self, dim: int, m: int, blocks=None, faces=None):
+        self.dim, self.m = int(dim), int(m)
         self.N = self.m ** self.dim
-        self.Q = int(np.prod(self.blocks))
-        self._cb = _blocks(self.blocks)
+        if faces is not None:
+            nf = (self.m + 1) * self.m ** (self.dim - 1)
+            self.faces = np.ascontiguousarray(faces, dtype=np.float64).reshape(-1, self.dim, nf)
+            self.Q = self.faces.shape[0]
+            self.blocks = None
+            self._cb = (C.c_int * 3)(0, 0, 0)
+        else:
+            self.faces = None
+            self.blocks = tuple(int(b) for b in blocks)
+            assert len(self.blocks) == self.dim
+            self.Q = int(np.prod(self.blocks))
+            self._cb = _blocks(self.blocks)
+
+    def _lib(self):
+        """the oracle library with this grid's face operator bound (or none)."""
+        L = lib()
+        if self.faces is not None:
+            L.or_set_faces(self.Q, _d(self.faces))
+        else:
+            L.or_set_faces(0, None)
+        return L
 
     # -- operator / smoother ------------------------------------------------
     def apply_A(self, theta, x):
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty(self.N)
-        lib().or_apply_A(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(x), _d(y))
+        self._lib().or_apply_A(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(x), _d(y))
         return y
 
     def gs_halfsweep(self, theta, b, y, color):
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
         y = np.array(y, dtype=np.float64, copy=True)
-        lib().or_gs_halfsweep(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(b), _d(y),
+        self._lib().or_gs_halfsweep(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(b), _d(y),
                               int(color))
         return y
 
@@ -95,7 +115,7 @@ class Grid:
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
         y = np.array(y, dtype=np.float64, copy=True)
-        lib().or_smooth(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(b), _d(y),
+        self._lib().or_smooth(self.dim, C.c_int64(self.m), self._cb, _d(theta), _d(b), _d(y),
                         int(kind), int(sweeps), C.c_double(omega))
         return y
 
@@ -115,7 +135,7 @@ class Grid:
         n = W.shape[1]
         ANq = np.empty((self.Q, n, n))
         fn = np.empty(n)
-        lib().or_offline_blocks(self.dim, C.c_int64(self.m), self._cb, n, _d(W), _d(ANq), _d(fn))
+        self._lib().or_offline_blocks(self.dim, C.c_int64(self.m), self._cb, n, _d(W), _d(ANq), _d(fn))
         return ANq, fn
 
     # -- solvers ------------------------------------------------------------
@@ -134,7 +154,7 @@ class Grid:
         hist = np.full(max_iter + 2, np.nan)
         a_n = np.full(max(n, 1), np.nan)
         trr = C.c_double(0)
-        st = getattr(lib(), fname)(self.dim, C.c_int64(self.m), self._cb, n, _d(Wf), _d(ANq),
+        st = getattr(self._lib(), fname)(self.dim, C.c_int64(self.m), self._cb, n, _d(Wf), _d(ANq),
                                    _d(fn), _d(mu), _d(bb), C.byref(o), _d(x), C.byref(its),
                                    _d(hist), _d(a_n), C.byref(trr))
         k = its.value
@@ -159,7 +179,7 @@ class Grid:
         bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
         x = np.empty(self.N)
         its = C.c_int(0)
-        st = lib().or_cg(self.dim, C.c_int64(self.m), self._cb, _d(mu), _d(bb), C.c_double(tol),
+        st = self._lib().or_cg(self.dim, C.c_int64(self.m), self._cb, _d(mu), _d(bb), C.c_double(tol),
                          int(max_iter), _d(x), C.byref(its))
         return dict(x=x, its=its.value, status=STATUS[st])
 
@@ -173,7 +193,7 @@ class Grid:
         ind = np.full(n_max, np.nan)
         its = np.zeros(n_max, dtype=np.int32)
         rej = C.c_int(0)
-        n = lib().or_greedy(self.dim, C.c_int64(self.m), self._cb, nt, _d(mu_train), n_max,
+        n = self._lib().or_greedy(self.dim, C.c_int64(self.m), self._cb, nt, _d(mu_train), n_max,
                             int(adaptive), C.c_double(snapshot_tol), C.c_double(drop_tol),
                             _d(W), _d(ANq), _d(fn), _i(sel), _d(ind), _i(its), C.byref(rej))
         return dict(W=np.asfortranarray(W[:, :n]), ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(),
@@ -188,7 +208,7 @@ class Grid:
         fn = np.zeros(cnt)
         its = np.zeros(cnt, dtype=np.int32)
         rej = C.c_int(0)
-        n = lib().or_basis_from_samples(self.dim, C.c_int64(self.m), self._cb, cnt, _d(mus),
+        n = self._lib().or_basis_from_samples(self.dim, C.c_int64(self.m), self._cb, cnt, _d(mus),
                                         C.c_double(snapshot_tol), C.c_double(drop_tol), _d(W),
                                         _d(ANq), _d(fn), _i(its), C.byref(rej))
         return dict(W=np.asfortranarray(W[:, :n]), ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(),

@@ -32,12 +32,52 @@ static double cell_theta(int dim, int64_t m, const int* blocks, const double* th
     return theta[q];
 }
 
+/* General affine operator (NEXT(4), DESIGN.md AMB-23): face coefficients
+ * kappa_e(theta) = sum_q theta_q F_q[e] given per face (or_set_faces), selected
+ * by blocks[0] == 0.  faces[(q*dim + d)*nf + idx], nf = (m+1) m^(dim-1) faces per
+ * direction; the face between nodes a and a+1 along d (a = 0..m; 0 and m+1 are
+ * Dirichlet nodes) has idx  x: a + (m+1)((J-1) + m(K-1)),  y: (I-1) + m(a + (m+1)(K-1)),
+ * z: (I-1) + m((J-1) + m a). */
+static int g_face_Q = 0;
+static const double* g_faces = NULL;
+
+void or_set_faces(int Q, const double* faces)
+{
+    g_face_Q = Q;
+    g_faces = faces;
+}
+
+static double face_kappa(int dim, int64_t m, const double* theta, int d, int64_t a, int64_t I,
+                         int64_t J, int64_t K)
+{
+    int64_t nf = (m + 1) * (dim == 3 ? m * m : m);
+    int64_t idx;
+    if (d == 0) idx = a + (m + 1) * ((J - 1) + m * (K - 1));
+    else if (d == 1) idx = (I - 1) + m * (a + (m + 1) * (K - 1));
+    else idx = (I - 1) + m * ((J - 1) + m * a);
+    double s = 0.0;
+    for (int q = 0; q < g_face_Q; ++q) s += theta[q] * g_faces[((int64_t)q * dim + d) * nf + idx];
+    return s;
+}
+
 /* Edge coefficients of node (I,J,K) in neighbour order -x,+x,-y,+y(,-z,+z).
  * Each is the mean of the cells sharing the edge (AMB-1), summed in the order
- * of AMB-4. */
+ * of AMB-4 -- or, for a face operator, the face coefficients above. */
 static void node_kappa(int dim, int64_t m, const int* blocks, const double* theta,
                        int64_t I, int64_t J, int64_t K, double* k)
 {
+    if (blocks[0] == 0) {
+        int64_t Kk = dim == 3 ? K : 1;
+        k[0] = face_kappa(dim, m, theta, 0, I - 1, I, J, Kk);
+        k[1] = face_kappa(dim, m, theta, 0, I, I, J, Kk);
+        k[2] = face_kappa(dim, m, theta, 1, J - 1, I, J, Kk);
+        k[3] = face_kappa(dim, m, theta, 1, J, I, J, Kk);
+        if (dim == 3) {
+            k[4] = face_kappa(dim, m, theta, 2, K - 1, I, J, K);
+            k[5] = face_kappa(dim, m, theta, 2, K, I, J, K);
+        }
+        return;
+    }
     if (dim == 2) {
         double c00 = cell_theta(2, m, blocks, theta, I - 1, J - 1, 0);
         double c10 = cell_theta(2, m, blocks, theta, I, J - 1, 0);
@@ -250,6 +290,7 @@ int or_mgs_append(int64_t N, int n, double* W, const double* v, double drop_tol)
 static int64_t grid_N(int dim, int64_t m) { return dim == 3 ? m * m * m : m * m; }
 static int grid_Q(int dim, const int* blocks)
 {
+    if (blocks[0] == 0) return g_face_Q;   /* face operator */
     return blocks[0] * blocks[1] * (dim == 3 ? blocks[2] : 1);
 }
 

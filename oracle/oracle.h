@@ -43,6 +43,11 @@ typedef struct {
                           preconditioner application (RBCG) / correction (RBI) */
 } or_opts;
 
+/* General affine operator (NEXT(4), AMB-23): blocks = {0,0,0} selects face
+ * coefficients kappa_e = sum_q theta_q faces[q][d][idx] (layout in oracle.c) set
+ * here; the pointer is kept (caller owns it) until the next call. */
+void or_set_faces(int Q, const double* faces);
+
 /* (A(theta) x) matrix-free, PAPER.md:98-103 (eq12) with AMB-1..4. */
 void or_apply_A(int dim, int64_t m, const int* blocks, const double* theta,
                 const double* x, double* y);
