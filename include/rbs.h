@@ -41,6 +41,7 @@ extern "C" {
 #define RBS_MAX_BATCH 64     /* queries per rbs_solve_batch call */
 #define RBS_MAX_N 64         /* RB dimension n */
 #define RBS_MAX_Q 64         /* affine terms */
+#define RBS_MAX_R 64         /* right-hand-side terms (rbs_affine_rhs) */
 
 typedef struct rbs_ctx rbs_ctx;
 
@@ -94,6 +95,29 @@ const char* rbs_last_error(const rbs_ctx* ctx);
  * Errors: RBS_E_ARG / RBS_E_DIM.
  */
 rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], const int blocks[3]);
+
+/* ---------------------------------------------------------------------------
+ * General affine operator (NEXT(4); DESIGN.md AMB-23; the paper's Case 1/2,
+ * PAPER.md:319-383): A(theta) = (m+1)^2 K(theta), (K x)_P = sum_e kappa_e (x_P - x_P')
+ * over the 2*dim faces e of node P (Dirichlet zero outside), with
+ *   kappa_e(theta) = sum_q theta_q faces[q][d][idx]   (q ascending),
+ * faces_dev: device, row-major [Q][dim][nf], nf = (m+1) m^(dim-1), BORROWED (the
+ * caller keeps it alive while the context uses this operator).  The face between
+ * nodes a and a+1 (a = 0..m) along axis d has idx
+ *   x: a + (m+1)((J-1) + m(K-1)),  y: (I-1) + m(a + (m+1)(K-1)),  z: (I-1) + m((J-1) + m a)
+ * (I,J,K in 1..m; K = 1 in 2D).  theta = mu (the caller passes theta as mu to
+ * rbs_solve_batch, P = Q).  Runs the flat kernels (no row march).  Invalidates any
+ * loaded basis.  Errors: RBS_E_ARG, RBS_E_DIM.
+ */
+rbs_status rbs_set_operator_faces(rbs_ctx* ctx, int dim, int64_t m, int Q, const double* faces_dev);
+
+/* Affine right-hand sides f(mu_b) = sum_r phi[b][r] f_r for a batch (PAPER.md:98-103,
+ * eq12 with R terms): out_dev[b][i] = sum_r phi_host[b*R + r] * terms_dev[r*N + i]
+ * (r ascending).  terms_dev [R][N] and out_dev [B][N] are device, caller-owned;
+ * out_dev is the rhs_dev of rbs_solve_batch.  Synchronises `stream`.
+ * Errors: RBS_E_STATE (no operator), RBS_E_DIM, RBS_E_ARG, RBS_E_CUDA. */
+rbs_status rbs_affine_rhs(rbs_ctx* ctx, int B, int R, const double* phi_host, const double* terms_dev,
+                          double* out_dev, void* stream);
 
 /* R = 1, f_1 = value * ones(N), phi_1 = 1 (the BASELINE configs use 1.0). */
 rbs_status rbs_set_rhs_constant(rbs_ctx* ctx, double value);

@@ -53,6 +53,9 @@ _SIGS = {
     "rbs_set_operator_blocks": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int)]),
     "rbs_set_rhs_constant": (C.c_int, [C.c_void_p, C.c_double]),
+    "rbs_set_operator_faces": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p]),
+    "rbs_affine_rhs": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]),
     "rbs_set_virtual_slabs": (C.c_int, [C.c_void_p, C.c_int]),
     "rbs_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
     "rbs_dist_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]),
@@ -128,6 +131,16 @@ def rbs_set_operator_blocks(ctx, dim, m, blocks):
     mm = (C.c_int64 * 3)(*([int(m)] * 3))
     bb = (C.c_int * 3)(*(list(blocks) + [1] * (3 - len(blocks))))
     _check(ctx, lib().rbs_set_operator_blocks(ctx, int(dim), mm, bb), "rbs_set_operator_blocks")
+
+
+def rbs_set_operator_faces(ctx, dim, m, Q, faces_dev):
+    _check(ctx, lib().rbs_set_operator_faces(ctx, int(dim), int(m), int(Q), _ptr(faces_dev)),
+           "rbs_set_operator_faces")
+
+
+def rbs_affine_rhs(ctx, B, R, phi_host, terms_dev, out_dev, stream=None):
+    _check(ctx, lib().rbs_affine_rhs(ctx, int(B), int(R), _ptr(phi_host), _ptr(terms_dev), _ptr(out_dev),
+                                     _stream(stream)), "rbs_affine_rhs")
 
 
 def rbs_set_rhs_constant(ctx, value):
@@ -255,16 +268,27 @@ def rbs_build_greedy(ctx, mu_train, n_max, mode, snapshot_tol, drop_tol, W_out, 
 class Solver:
     """Owns a context plus the torch buffers it borrows (storage, workspace)."""
 
-    def __init__(self, dim, m, blocks, device=0, rhs_constant=1.0):
+    def __init__(self, dim, m, blocks=None, device=0, rhs_constant=1.0, faces=None):
+        """blocks: thermal-block operator; or faces: (Q, dim, (m+1) m^(dim-1)) face
+        coefficients of a general affine operator (rbs_set_operator_faces)."""
         import torch
         self.torch = torch
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         self.ctx = rbs_create(device)
-        self.dim, self.m, self.blocks = int(dim), int(m), tuple(blocks)
+        self.dim, self.m = int(dim), int(m)
         self.N = self.m ** self.dim
-        self.Q = int(np.prod(self.blocks))
-        rbs_set_operator_blocks(self.ctx, dim, m, blocks)
+        if faces is not None:
+            f = torch.as_tensor(np.ascontiguousarray(faces), dtype=torch.float64)
+            self._faces = f.reshape(f.shape[0], -1).contiguous().to(self.device)   # kept alive (borrowed)
+            self.blocks = None
+            self.Q = int(self._faces.shape[0])
+            rbs_set_operator_faces(self.ctx, dim, m, self.Q, self._faces)
+        else:
+            self._faces = None
+            self.blocks = tuple(blocks)
+            self.Q = int(np.prod(self.blocks))
+            rbs_set_operator_blocks(self.ctx, dim, m, blocks)
         rbs_set_rhs_constant(self.ctx, rhs_constant)
         self.n = None
         self._storage = None
@@ -278,6 +302,17 @@ class Solver:
 
     def _bytes(self, nbytes):
         return self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.device)
+
+    def affine_rhs(self, phi, terms, stream=None):
+        """f(mu_b) = sum_r phi[b, r] terms[r] on the device -> (B, N) tensor for solve_batch(rhs=)."""
+        torch = self.torch
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        B, R = phi.shape
+        t = terms if torch.is_tensor(terms) else torch.as_tensor(np.ascontiguousarray(terms), dtype=torch.float64)
+        t = t.to(self.device).contiguous()
+        out = torch.empty((B, self.N), dtype=torch.float64, device=self.device)
+        rbs_affine_rhs(self.ctx, B, R, phi, t, out, stream)
+        return out
 
     def set_slabs(self, G):
         """Mesh-slab mode (3D, RBCG): solve slab by slab with G z-slabs (1 = off)."""

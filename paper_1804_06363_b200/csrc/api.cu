@@ -475,6 +475,43 @@ rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], co
     return RBS_OK;
 }
 
+rbs_status rbs_set_operator_faces(rbs_ctx* ctx, int dim, int64_t m, int Q, const double* faces_dev) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!faces_dev) return fail(ctx, RBS_E_ARG, "faces_dev is NULL");
+    if (Q < 1 || Q > RBS_MAX_Q) return fail(ctx, RBS_E_DIM, "Q must be in 1..RBS_MAX_Q");
+    const int64_t mm[3] = {m, m, m};
+    const int ones[3] = {1, 1, 1};
+    const rbs_status st = rbs_set_operator_blocks(ctx, dim, mm, ones);
+    if (st != RBS_OK) return st;
+    ctx->g.Q = Q;
+    ctx->g.faces = faces_dev;
+    ctx->g.nf = (m + 1) * (dim == 3 ? m * m : m);
+    ctx->gglob = ctx->g;
+    return RBS_OK;
+}
+
+rbs_status rbs_affine_rhs(rbs_ctx* ctx, int B, int R, const double* phi_host, const double* terms_dev,
+                          double* out_dev, void* stream) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "no operator");
+    if (B < 1 || R < 1 || R > RBS_MAX_R) return fail(ctx, RBS_E_DIM, "B >= 1 and 1 <= R <= RBS_MAX_R");
+    if (!phi_host || !terms_dev || !out_dev) return fail(ctx, RBS_E_ARG, "phi/terms/out is NULL");
+    const cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaSetDevice(ctx->device));
+    double* dphi = nullptr;
+    CK(cudaMallocAsync((void**)&dphi, (size_t)B * R * 8, st));
+    CK(cudaMemcpyAsync(dphi, phi_host, (size_t)B * R * 8, cudaMemcpyHostToDevice, st));
+    const int64_t tot = (int64_t)B * ctx->g.N;
+    k_affine_rhs<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(
+        dphi, R, terms_dev, ctx->g.N, B, out_dev);
+    CKL();
+    CK(cudaFreeAsync(dphi, st));
+    CK(cudaStreamSynchronize(st));
+    return RBS_OK;
+}
+
 rbs_status rbs_set_rhs_constant(rbs_ctx* ctx, double value) {
     if (!ctx) return RBS_E_ARG;
     ctx->err.clear();
@@ -655,7 +692,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     const int v2off = dv2 ? atoi(dv2) : 0;
     const bool cg = o->method == RBS_RBCG;
     // 2D, B_pad <= 32: the projection pass is the row march (k_resid_march)
-    const bool use_rmarch = g.dim == 2 && Bp <= 32;
+    const bool use_rmarch = g.dim == 2 && Bp <= 32 && !g.faces;   // row marches: block tables
     const MarchPart rpart = march_part(g, kRmTX, ctx->num_sms);
     const int nct = use_rmarch ? rpart.nsx * rpart.nsy : proj_ctas(g), nctf = part_ctas(g);
     const int nct_plain = proj_ctas(g);
@@ -871,7 +908,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.s = S; a.done = done;
         pb(RBS_K_CGP);
-        if (!(v2off & 2) && g.dim == 2 && Bp <= 32) {
+        if (!(v2off & 2) && g.dim == 2 && Bp <= 32 && !g.faces) {
             CGP2Args c2{};
             c2.g = g; c2.Bp = Bp; c2.theta = L.theta;
             c2.part = march_part(g, kC2TX, 2 * ctx->num_sms);   // 2 CTAs per SM
@@ -889,7 +926,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
 
     // 2D: prolongation + all half-sweeps (+ y^T r) in one row-marching pass
-    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac;
+    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac && !g.faces;
     auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
                      int init) {
         SmoothMarchArgs a{};

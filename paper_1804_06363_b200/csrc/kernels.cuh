@@ -410,6 +410,19 @@ struct GSArgs {
 
 constexpr int kGsUnroll = 4;
 
+// f(mu_b) = sum_r phi_r(mu_b) f_r (affine right-hand side, eq12 with R
+// terms; NEXT(4)): out[b][i] = sum_r phi[b][r] terms[r][i], r ascending
+__global__ void k_affine_rhs(const double* phi, int R, const double* terms, int64_t N, int B, double* out) {
+    const int64_t tot = (int64_t)B * N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(e / N);
+        const int64_t i = e - (int64_t)b * N;
+        double v = 0.0;
+        for (int r = 0; r < R; ++r) v = fma(phi[b * R + r], terms[(int64_t)r * N + i], v);
+        out[e] = v;
+    }
+}
+
 // LAST pass of the smoother: y^T r, y^T y partials of this CTA and RBCG Step 10
 // (beta = y_{k+1}^T r_{k+1} / y_k^T r_k) in the last CTA (AMB-11)
 __device__ __forceinline__ void gs_step10(GSArgs& a, double yr, double yy) {

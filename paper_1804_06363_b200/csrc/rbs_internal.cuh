@@ -52,6 +52,11 @@ struct Geo {
     // K = kofs+1 .. kofs+mz of the global grid; planes own_lo <= K-kofs-1 < own_hi
     // are owned (count in reductions).  Full grid: kofs = 0, mz = m, own = [0, m).
     int kofs, mz, own_lo, own_hi;
+    // general affine operator (rbs_set_operator_faces, NEXT(4), AMB-23): face
+    // coefficients faces[(q*dim + d)*nf + idx] (layout in include/rbs.h); nullptr
+    // for the thermal-block operator
+    const double* faces;
+    int64_t nf;
 };
 
 // z-neighbour availability of a node at global plane K inside its slab
@@ -86,9 +91,34 @@ __device__ __forceinline__ int axis_block(const Geo& g, int a, int p) {
 // Edge coefficients of node (I,J,K) in neighbour order -x,+x,-y,+y(,-z,+z):
 // mean of the cells sharing the edge (AMB-1), summed in AMB-4 order.
 // th: theta laid out [q][ldb] (ldb = batch stride), b = this lane's query.
+// face coefficient sum_q theta_q F_q of the face between nodes a and a+1 along d
+template <int DIM>
+__device__ __forceinline__ double face_kappa(const Geo& g, const double* th, int ldb, int b, int d, int a,
+                                             int I, int J, int K) {
+    const int64_t m = g.m;
+    int64_t idx;
+    if (d == 0) idx = a + (m + 1) * ((J - 1) + (DIM == 3 ? m * (K - 1) : 0));
+    else if (d == 1) idx = (I - 1) + m * (a + (DIM == 3 ? (m + 1) * (K - 1) : 0));
+    else idx = (I - 1) + m * ((J - 1) + m * a);
+    double s = 0.0;
+    for (int q = 0; q < g.Q; ++q) s = fma(th[q * ldb + b], __ldg(g.faces + ((int64_t)q * DIM + d) * g.nf + idx), s);
+    return s;
+}
+
 template <int DIM>
 __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int ldb, int b,
                                            int I, int J, int K, double* k) {
+    if (g.faces) {
+        k[0] = face_kappa<DIM>(g, th, ldb, b, 0, I - 1, I, J, K);
+        k[1] = face_kappa<DIM>(g, th, ldb, b, 0, I, I, J, K);
+        k[2] = face_kappa<DIM>(g, th, ldb, b, 1, J - 1, I, J, K);
+        k[3] = face_kappa<DIM>(g, th, ldb, b, 1, J, I, J, K);
+        if (DIM == 3) {
+            k[4] = face_kappa<DIM>(g, th, ldb, b, 2, K - 1, I, J, K);
+            k[5] = face_kappa<DIM>(g, th, ldb, b, 2, K, I, J, K);
+        }
+        return;
+    }
     const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
     const int by0 = axis_block(g, J - 1, g.py) * g.px, by1 = axis_block(g, J, g.py) * g.px;
     int bz0 = 0, bz1 = 0;
