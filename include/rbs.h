@@ -277,6 +277,20 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train_ho
                             double* indicator, int* snap_iters, int* n_rejected,
                             void* workspace_dev, size_t workspace_bytes, void* stream);
 
+/* rbs_build_greedy_affine: the same greedy for affine right-hand sides
+ * f(mu_t) = sum_r phi_train_host[t*R + r] f_r (terms_dev [R][N], device, borrowed;
+ * see rbs_affine_rhs): snapshots solve A(mu) x = f(mu); the offline vectors are
+ * f_{N,r} = W^T f_r, returned in fnr_host_out [R][n_max]; the indicator solves use
+ * f_N(mu_t) = sum_r phi_r(mu_t) f_{N,r}.  Later solves must pass rhs_dev (the
+ * context's constant right-hand side does not describe this problem).  1 <= R <=
+ * RBS_MAX_R; other arguments, workspace and errors as rbs_build_greedy. */
+rbs_status rbs_build_greedy_affine(rbs_ctx* ctx, int n_train, const double* mu_train_host, int R,
+                                   const double* phi_train_host, const double* terms_dev, int n_max,
+                                   int mode, double snapshot_tol, double drop_tol, double* W_out_dev,
+                                   double* ANq_host_out, double* fnr_host_out, int* n_out, int* selected,
+                                   double* indicator, int* snap_iters, int* n_rejected,
+                                   void* workspace_dev, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

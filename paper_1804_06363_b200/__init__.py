@@ -77,6 +77,11 @@ _SIGS = {
                                    C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.POINTER(C.c_int), C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.POINTER(C.c_int), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "rbs_build_greedy_affine": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.c_void_p,
+                                          C.c_size_t, C.c_void_p]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -244,23 +249,36 @@ def rbs_greedy_workspace_size(ctx, n_train, n_max):
 
 
 def rbs_build_greedy(ctx, mu_train, n_max, mode, snapshot_tol, drop_tol, W_out, workspace,
-                     stream=None):
+                     stream=None, phi_train=None, terms_dev=None):
+    """phi_train (nt, R) + terms_dev (R, N): affine right-hand sides (rbs_build_greedy_affine);
+    the result's fn is then (R, n) = W^T f_r."""
     mu_train = np.ascontiguousarray(mu_train, dtype=np.float64)
     nt, P = mu_train.shape
+    R = 0 if phi_train is None else int(np.shape(phi_train)[1])
     ANq = np.zeros((P, n_max, n_max))
-    fn = np.zeros(n_max)
+    fn = np.zeros((max(R, 1), n_max))
     n_out = C.c_int(0)
     rej = C.c_int(0)
     sel = np.full(n_max, -1, dtype=np.int32)
     ind = np.full(n_max, np.nan)
     its = np.zeros(n_max, dtype=np.int32)
-    _check(ctx, lib().rbs_build_greedy(ctx, nt, _ptr(mu_train), int(n_max), int(mode),
-                                       float(snapshot_tol), float(drop_tol), _ptr(W_out),
-                                       _ptr(ANq), _ptr(fn), C.byref(n_out), _ptr(sel), _ptr(ind),
-                                       _ptr(its), C.byref(rej), _ptr(workspace),
-                                       workspace.numel(), _stream(stream)), "rbs_build_greedy")
+    if R == 0:
+        _check(ctx, lib().rbs_build_greedy(ctx, nt, _ptr(mu_train), int(n_max), int(mode),
+                                           float(snapshot_tol), float(drop_tol), _ptr(W_out),
+                                           _ptr(ANq), _ptr(fn), C.byref(n_out), _ptr(sel), _ptr(ind),
+                                           _ptr(its), C.byref(rej), _ptr(workspace),
+                                           workspace.numel(), _stream(stream)), "rbs_build_greedy")
+    else:
+        phi = np.ascontiguousarray(phi_train, dtype=np.float64)
+        _check(ctx, lib().rbs_build_greedy_affine(ctx, nt, _ptr(mu_train), R, _ptr(phi), _ptr(terms_dev),
+                                                  int(n_max), int(mode), float(snapshot_tol),
+                                                  float(drop_tol), _ptr(W_out), _ptr(ANq), _ptr(fn),
+                                                  C.byref(n_out), _ptr(sel), _ptr(ind), _ptr(its),
+                                                  C.byref(rej), _ptr(workspace), workspace.numel(),
+                                                  _stream(stream)), "rbs_build_greedy_affine")
     n = n_out.value
-    return dict(n=n, ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(), selected=sel[:n].copy(),
+    fn = fn[:, :n].copy()
+    return dict(n=n, ANq=ANq[:, :n, :n].copy(), fn=fn[0] if R == 0 else fn, selected=sel[:n].copy(),
                 indicator=ind[:n].copy(), snap_iters=its[:n].copy(), n_rejected=rej.value)
 
 
@@ -385,16 +403,22 @@ class Solver:
         return out
 
     def build_greedy(self, mu_train, n_max, adaptive=True, snapshot_tol=1e-12, drop_tol=1e-10,
-                     stream=None, load=True):
+                     stream=None, load=True, phi_train=None, terms=None):
+        """mu_train (nt, P).  Affine right-hand sides: phi_train (nt, R) and terms (R, N)."""
         torch = self.torch
         mu_train = np.ascontiguousarray(mu_train, dtype=np.float64)
         Wcol = torch.zeros((n_max, self.N), dtype=torch.float64, device=self.device)
         ws = self._bytes(rbs_greedy_workspace_size(self.ctx, mu_train.shape[0], n_max))
+        tdev = None
+        if phi_train is not None:
+            tdev = terms if torch.is_tensor(terms) else torch.as_tensor(np.ascontiguousarray(terms))
+            tdev = tdev.to(device=self.device, dtype=torch.float64).contiguous()
         res = rbs_build_greedy(self.ctx, mu_train, n_max,
                                RBS_GREEDY_ADAPTIVE if adaptive else RBS_GREEDY_PLAIN,
-                               snapshot_tol, drop_tol, Wcol, ws, stream)
+                               snapshot_tol, drop_tol, Wcol, ws, stream, phi_train, tdev)
         n = res["n"]
         res["W"] = Wcol[:n].t()  # (N, n) view of the column-major result
         if load:
-            self.load_basis(res["W"], res["ANq"], res["fn"], stream)
+            fn1 = res["fn"] if phi_train is None else res["fn"][0]
+            self.load_basis(res["W"], res["ANq"], fn1, stream)
         return res

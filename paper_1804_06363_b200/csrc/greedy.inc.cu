@@ -58,7 +58,7 @@ namespace {
 constexpr int kDotCtas = 296;
 
 struct GreedyLayout {
-    double *Wi, *ANq, *Z, *part, *rows, *x, *w, *dpart, *scal;
+    double *Wi, *ANq, *Z, *part, *rows, *x, *w, *dpart, *scal, *phi;
     double *tr_theta, *tr_fproj, *tr_L, *tr_E, *tr_a;
     double *tr_d[6];
     int* tr_i[5];
@@ -80,6 +80,7 @@ GreedyLayout greedy_layout(rbs_ctx* c, int nt, int n_max, void* base) {
     L.w = cv.take<double>((size_t)c->N8);
     L.dpart = cv.take<double>(kDotCtas);
     L.scal = cv.take<double>(8);
+    L.phi = cv.take<double>(RBS_MAX_R);
     L.tr_theta = cv.take<double>((size_t)c->g.Q * nt);
     L.tr_fproj = cv.take<double>((size_t)nt * (npad + 1));
     L.tr_L = cv.take<double>((size_t)nt * npad * npad + 8);
@@ -93,7 +94,7 @@ GreedyLayout greedy_layout(rbs_ctx* c, int nt, int n_max, void* base) {
     tmp.ldw = w_ld(npad);
     rbs_solve_opts o;
     rbs_default_opts(&o);
-    L.solve_bytes = solve_layout(&tmp, 1, &o, false, nullptr).bytes;
+    L.solve_bytes = solve_layout(&tmp, 1, &o, true, nullptr).bytes;   // rhs buffer: affine snapshots
     L.solve_ws = cv.take<char>(L.solve_bytes);
     L.bytes = cv.off + 256;
     return L;
@@ -112,11 +113,16 @@ rbs_status rbs_greedy_workspace_size(const rbs_ctx* c, int n_train, int n_max, s
     return RBS_OK;
 }
 
-rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, int n_max, int mode,
-                            double snapshot_tol, double drop_tol, double* W_out,
-                            double* ANq_out, double* fn_out, int* n_out, int* selected,
-                            double* indicator, int* snap_iters, int* n_rejected,
-                            void* workspace, size_t ws_bytes, void* stream) {
+// Greedy core.  R = 0: the constant right-hand side (rbs_set_rhs_constant);
+// R > 0: affine right-hand sides f(mu_t) = sum_r phi_train[t][r] f_r (terms_dev
+// [R][N]): snapshots solve with that f, the offline vectors are f_{N,r} = W^T f_r
+// (fn_out [R][n]) and the indicator solves use f_N(mu_t) = sum_r phi_r(mu_t) f_{N,r}.
+static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train, int R,
+                              const double* phi_train, const double* terms, int n_max, int mode,
+                              double snapshot_tol, double drop_tol, double* W_out,
+                              double* ANq_out, double* fn_out, int* n_out, int* selected,
+                              double* indicator, int* snap_iters, int* n_rejected,
+                              void* workspace, size_t ws_bytes, void* stream) {
     if (!ctx) return RBS_E_ARG;
     ctx->err.clear();
     if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
@@ -147,7 +153,8 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
     ctx->hfn.assign(0, 0.0);
     ctx->has_basis = true;
 
-    std::vector<double> hA((size_t)Q * npad * npad, 0.0), hf(npad, 0.0);
+    const int RT = R > 0 ? R : 1;           // right-hand-side terms tracked
+    std::vector<double> hA((size_t)Q * npad * npad, 0.0), hf((size_t)RT * npad, 0.0);
     // training parameters theta [Q][nt]
     {
         std::vector<double> th((size_t)Q * nt);
@@ -180,7 +187,14 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
         // within 2*its_1 + 50 -> fall back to SGS-PCG; its < 0.
         int its = 0, qs = 0;
         so.max_iter = (ctx->n == 0) ? 200000 : 2 * (its_first > 0 ? its_first : 1000) + 50;
-        rbs_status s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, nullptr, L.x, &its,
+        const double* srhs = nullptr;
+        if (R > 0) {   // f(mu_cand) = sum_r phi_r f_r -> L.Z
+            CK(cudaMemcpyAsync(L.phi, phi_train + (size_t)cand * R, (size_t)R * 8, cudaMemcpyHostToDevice, st));
+            k_affine_rhs<<<grid_for(g.N, 256, ctx->num_sms * 8), 256, 0, st>>>(L.phi, R, terms, g.N, 1, L.Z);
+            CKL();
+            srhs = L.Z;
+        }
+        rbs_status s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, srhs, L.x, &its,
                                        &qs, nullptr, nullptr, nullptr, nullptr, L.solve_ws,
                                        L.solve_bytes, stream);
         if (s != RBS_OK) return s;
@@ -190,7 +204,7 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
             ctx->hfn.clear();
             ctx->hANq.clear();
             so.max_iter = 200000;
-            s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, nullptr, L.x, &its, &qs,
+            s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, srhs, L.x, &its, &qs,
                                 nullptr, nullptr, nullptr, nullptr, L.solve_ws, L.solve_bytes, stream);
             if (s != RBS_OK) return s;
             its = -its;
@@ -237,17 +251,26 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
                     hA[((size_t)q * npad + n) * npad + i] = v;
                 }
             }
-            {   // f_{N,1}[n] = w_n^T 1
+            for (int r = 0; r < RT; ++r) {   // f_{N,r}[n] = w_n^T f_r  (f_1 = 1 for R = 0)
                 ProjArgs a{};
                 a.g = g; a.Bp = 8; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ldw;
-                a.W = L.Wi; a.V = nullptr; a.vconst = 1.0; a.part = L.part;
+                a.W = L.Wi; a.part = L.part;
+                if (R > 0) {
+                    // the projection pass reads [N][8] node-major batches: f_r goes to column 0
+                    k_fill_batch<<<grid_for(g.N, 256, ctx->num_sms * 8), 256, 0, st>>>(
+                        L.Z, g.N, ctx->N8, 8, 1, terms + (size_t)r * g.N, 0.0);
+                    a.V = L.Z;
+                } else {
+                    a.V = nullptr;
+                    a.vconst = 1.0;
+                }
                 launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, npad), st, a);
                 k_reduce_rows<<<1, 128, 0, st>>>(L.part, npad + 1, nct, L.rows);
                 CKL();
                 double v;
                 CK(cudaMemcpyAsync(&v, L.rows + n, 8, cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
-                hf[n] = v;
+                hf[(size_t)r * npad + n] = v;
             }
             if (selected) selected[n] = cand;
             if (snap_iters) snap_iters[n] = its;
@@ -264,7 +287,14 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
         {
             std::vector<double> fp((size_t)nt * (npad + 1), 0.0);
             for (int t = 0; t < nt; ++t) {
-                for (int j = 0; j < n; ++j) fp[(size_t)t * (npad + 1) + j] = hf[j];
+                for (int j = 0; j < n; ++j) {
+                    double v = 0.0;
+                    if (R > 0)
+                        for (int r = 0; r < R; ++r) v += phi_train[(size_t)t * R + r] * hf[(size_t)r * npad + j];
+                    else
+                        v = hf[j];
+                    fp[(size_t)t * (npad + 1) + j] = v;
+                }
                 fp[(size_t)t * (npad + 1) + npad] = 1.0;
             }
             CK(cudaMemcpyAsync(L.tr_fproj, fp.data(), fp.size() * 8, cudaMemcpyHostToDevice, st));
@@ -306,7 +336,8 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
                     ANq_out[((size_t)q * n_max + i) * n_max + j] =
                         (i < n && j < n) ? hA[((size_t)q * npad + i) * npad + j] : 0.0;
     if (fn_out)
-        for (int j = 0; j < n_max; ++j) fn_out[j] = j < n ? hf[j] : 0.0;
+        for (int r = 0; r < RT; ++r)
+            for (int j = 0; j < n_max; ++j) fn_out[(size_t)r * n_max + j] = j < n ? hf[(size_t)r * npad + j] : 0.0;
     // the context keeps the built basis (workspace retained)
     ctx->n = n;
     ctx->hfn.assign(hf.begin(), hf.begin() + n);
@@ -318,6 +349,30 @@ rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, i
     if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
     CK(cudaStreamSynchronize(st));
     return RBS_OK;
+}
+
+rbs_status rbs_build_greedy(rbs_ctx* ctx, int n_train, const double* mu_train, int n_max, int mode,
+                            double snapshot_tol, double drop_tol, double* W_out,
+                            double* ANq_out, double* fn_out, int* n_out, int* selected,
+                            double* indicator, int* snap_iters, int* n_rejected,
+                            void* workspace, size_t ws_bytes, void* stream) {
+    return greedy_core(ctx, n_train, mu_train, 0, nullptr, nullptr, n_max, mode, snapshot_tol, drop_tol,
+                       W_out, ANq_out, fn_out, n_out, selected, indicator, snap_iters, n_rejected, workspace,
+                       ws_bytes, stream);
+}
+
+rbs_status rbs_build_greedy_affine(rbs_ctx* ctx, int n_train, const double* mu_train, int R,
+                                   const double* phi_train_host, const double* terms_dev, int n_max,
+                                   int mode, double snapshot_tol, double drop_tol, double* W_out,
+                                   double* ANq_out, double* fnr_out, int* n_out, int* selected,
+                                   double* indicator, int* snap_iters, int* n_rejected,
+                                   void* workspace, size_t ws_bytes, void* stream) {
+    if (!ctx) return RBS_E_ARG;
+    if (R < 1 || R > RBS_MAX_R) return fail(ctx, RBS_E_DIM, "R must be in 1..RBS_MAX_R");
+    if (!phi_train_host || !terms_dev) return fail(ctx, RBS_E_ARG, "phi_train/terms is NULL");
+    return greedy_core(ctx, n_train, mu_train, R, phi_train_host, terms_dev, n_max, mode, snapshot_tol,
+                       drop_tol, W_out, ANq_out, fnr_out, n_out, selected, indicator, snap_iters, n_rejected,
+                       workspace, ws_bytes, stream);
 }
 
 }  // extern "C"

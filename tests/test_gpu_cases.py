@@ -98,3 +98,32 @@ def test_case_parity(orc, rbs, case, m, n_train, B, method):
         hg, hr = out["history"][b], ref["hist"]
         k = min(len(hg), len(hr))
         assert np.all(np.abs(hg[:k] - hr[:k]) <= 1e-6 * np.abs(hr[:k]) + 1e-13)
+
+
+@pytest.mark.parametrize("case", [1, 2])
+def test_gpu_greedy_affine_rhs(orc, rbs, case):
+    """rbs_build_greedy_affine: orthonormal W; offline blocks equal the oracle's W^T A_q W;
+    f_{N,r} = W^T f_r; every selected parameter is reproduced from span W (Lemma 1,
+    PAPER.md:184-196: one RBCG iteration to the snapshot tolerance)."""
+    import torch
+    m, n_max = 11, 8
+    P = cases.case_problem(case, m)
+    g = orc.Grid(3, m, faces=P["faces"])
+    mus = cases.case_params(case, 24, 300 + case)
+    th = np.stack([P["theta"](mu) for mu in mus])
+    phi = np.stack([P["phi"](mu) for mu in mus])
+    s = rbs.Solver(3, m, faces=P["faces"])
+    res = s.build_greedy(th, n_max, phi_train=phi, terms=P["terms"])
+    n = res["n"]
+    assert n == n_max
+    W = res["W"].cpu().numpy()
+    assert np.abs(W.T @ W - np.eye(n)).max() < 1e-12
+    ANq, _ = g.offline_blocks(W)
+    assert np.abs(res["ANq"] - ANq).max() <= 1e-11 * np.abs(ANq).max()
+    assert np.abs(res["fn"] - P["terms"] @ W).max() <= 1e-11 * np.abs(res["fn"]).max()
+    sel = res["selected"]
+    assert sel[0] == 0 and len(set(sel.tolist())) == n
+    rhs = s.affine_rhs(phi[sel], P["terms"])
+    out = s.solve_batch(th[sel], rhs=rhs, tol=1e-9)
+    assert np.all(out["its"] <= 1), out["its"]
+    assert torch.isfinite(out["X"]).all()
