@@ -179,8 +179,106 @@ def run_reference(a):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+# Case 1 with RB dimension 1 and 5, Case 2 with 2 and 10 (AMB-17: the
+# text's 10 over the caption's 20), 100 random parameters per case (96 = 6 batches of 16 here)
+CASE_M, CASE_B, CASE_TRAIN, CASE_QUERIES = 127, 16, 64, 96
+CASE_N = {1: 5, 2: 10}
+
+
+def run_case(a, case):
+    """NEXT(4) measurement: the paper's Case 1 / Case 2 (Table 1) as a
+    7-point FD face operator on 127^3 interior nodes (h = 1/128, N = 2,048,383; AMB-23):
+    GPU greedy basis from 64 seeded training mu with the affine right-hand side
+    (untimed; n = 5 for Case 1, 10 for Case 2), 96 queries in batches of
+    B = 16, RBCG to 1e-10.  A step = one batch:
+    device assembly of f(mu) (rbs_affine_rhs) + rbs_solve_batch.  1 GPU only."""
+    import torch
+    import paper_1804_06363_b200 as rbs
+    from synth import cases
+    torch.cuda.set_device(0)
+    P = cases.case_problem(case, CASE_M)
+    s = rbs.Solver(3, CASE_M, faces=P["faces"])
+    terms = torch.as_tensor(P["terms"]).to(s.device)
+    t0 = time.perf_counter()
+    tr = cases.case_params(case, CASE_TRAIN, 1000 + case)
+    gr = s.build_greedy(np.stack([P["theta"](mu) for mu in tr]), CASE_N[case],
+                        phi_train=np.stack([P["phi"](mu) for mu in tr]), terms=terms)
+    torch.cuda.synchronize()
+    offline_s = time.perf_counter() - t0
+    q = cases.case_params(case, CASE_QUERIES, 2000 + case)
+    th = np.stack([P["theta"](mu) for mu in q])
+    phi = np.stack([P["phi"](mu) for mu in q])
+    nb = CASE_QUERIES // CASE_B
+    N = s.N
+    X = torch.empty((CASE_B, N), dtype=torch.float64, device=s.device)
+    stream = torch.cuda.current_stream()
+
+    def step(k, **kw):
+        b = k % nb
+        sl = slice(b * CASE_B, (b + 1) * CASE_B)
+        rhs = s.affine_rhs(phi[sl], terms)
+        return s.solve_batch(th[sl], rhs=rhs, X=X, want_a_n=False, **kw)
+
+    for w in range(max(a.warmup, 1)):
+        step(w)
+    clocks = Clocks(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches, its = 0, []
+    for k in range(a.steps):
+        out = step(k)
+        launches += out["launches"] + 1
+        its += [int(i) for i in out["its"]]
+        assert all(st == "CONVERGED" for st in out["status"]), out["status"]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    prof = step(0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
+    hbm, hbm_src = peaks()
+    n, B = gr["n"], CASE_B
+    face_b = 8 * 2 * 3 * N          # Q = 2 face arrays, 3 new faces per node, read once per pass
+    alg = {"k_cgp": 24 * B * N + face_b, "k_proj": 40 * B * N + 8 * N * n + face_b,
+           "k_gs": 16 * B * N + face_b, "k_prolong": 8 * B * N + 8 * N * n}
+    tot_ms = sum(v[0] for v in prof.values())
+    kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
+                   "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
+    for k, kb in alg.items():
+        if k in kernels:
+            d = kernels[k]["avg_us"] * 1e-6
+            kernels[k].update(alg_bytes=kb, GBps=kb / d / 1e9, hbm_frac=kb / d / 1e9 / hbm)
+    top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
+    kt = kernels[top]
+    line = {"metric": f"parameter queries solved/sec to rel. residual 1e-10 (Case {case}, RBCG, 1 GPU)",
+            "value": a.steps * B / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"case{case}: PAPER.md Table 1 Case {case}, 3D 7-point FD face operator "
+                                   f"{CASE_M}^3 (N={N}), Q=2, R={P['terms'].shape[0]}, GPU greedy n={n} "
+                                   f"from {CASE_TRAIN} train mu, {CASE_QUERIES} queries, B={B}, RBCG "
+                                   "sym-RBGS nu=1 (flat kernels), tol 1e-10",
+                       "B": B, "n": n, "its_min_med_max": [min(its), int(np.median(its)), max(its)],
+                       "offline_greedy_s": round(offline_s, 2),
+                       "l2": "inputs larger than L2 (4 x 262 MB state)"},
+            "clocks": clk, "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm,
+                         "unit": "GB/s", "frac": kt["GBps"] / hbm, "traffic": None,
+                         "peak_source": hbm_src, "alg_bytes_per_launch": kt["alg_bytes"],
+                         "avg_launch_us": kt["avg_us"], "share_of_iteration": kt["share"]},
+            "kernels": kernels}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
+    if a.config in ("case1", "case2"):
+        if a.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "case workloads: GPU measurement only"}))
+        elif int(os.environ.get("RANK", "0")) == 0:
+            run_case(a, int(a.config[-1]))
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -480,6 +480,8 @@ rbs_status rbs_set_operator_faces(rbs_ctx* ctx, int dim, int64_t m, int Q, const
     ctx->err.clear();
     if (!faces_dev) return fail(ctx, RBS_E_ARG, "faces_dev is NULL");
     if (Q < 1 || Q > RBS_MAX_Q) return fail(ctx, RBS_E_DIM, "Q must be in 1..RBS_MAX_Q");
+    if ((int64_t)dim * (m + 1) * (dim == 3 ? m * m : m) >= (int64_t(1) << 32))
+        return fail(ctx, RBS_E_DIM, "face arrays too large (dim * nf >= 2^32)");
     const int64_t mm[3] = {m, m, m};
     const int ones[3] = {1, 1, 1};
     const rbs_status st = rbs_set_operator_blocks(ctx, dim, mm, ones);

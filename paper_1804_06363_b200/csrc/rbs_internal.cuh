@@ -91,31 +91,30 @@ __device__ __forceinline__ int axis_block(const Geo& g, int a, int p) {
 // Edge coefficients of node (I,J,K) in neighbour order -x,+x,-y,+y(,-z,+z):
 // mean of the cells sharing the edge (AMB-1), summed in AMB-4 order.
 // th: theta laid out [q][ldb] (ldb = batch stride), b = this lane's query.
-// face coefficient sum_q theta_q F_q of the face between nodes a and a+1 along d
-template <int DIM>
-__device__ __forceinline__ double face_kappa(const Geo& g, const double* th, int ldb, int b, int d, int a,
-                                             int I, int J, int K) {
-    const int64_t m = g.m;
-    int64_t idx;
-    if (d == 0) idx = a + (m + 1) * ((J - 1) + (DIM == 3 ? m * (K - 1) : 0));
-    else if (d == 1) idx = (I - 1) + m * (a + (DIM == 3 ? (m + 1) * (K - 1) : 0));
-    else idx = (I - 1) + m * ((J - 1) + m * a);
-    double s = 0.0;
-    for (int q = 0; q < g.Q; ++q) s = fma(th[q * ldb + b], __ldg(g.faces + ((int64_t)q * DIM + d) * g.nf + idx), s);
-    return s;
-}
-
 template <int DIM>
 __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int ldb, int b,
                                            int I, int J, int K, double* k) {
     if (g.faces) {
-        k[0] = face_kappa<DIM>(g, th, ldb, b, 0, I - 1, I, J, K);
-        k[1] = face_kappa<DIM>(g, th, ldb, b, 0, I, I, J, K);
-        k[2] = face_kappa<DIM>(g, th, ldb, b, 1, J - 1, I, J, K);
-        k[3] = face_kappa<DIM>(g, th, ldb, b, 1, J, I, J, K);
-        if (DIM == 3) {
-            k[4] = face_kappa<DIM>(g, th, ldb, b, 2, K - 1, I, J, K);
-            k[5] = face_kappa<DIM>(g, th, ldb, b, 2, K, I, J, K);
+        // face indices from the node index P (layout in include/rbs.h):
+        // x: P + (J-1) + m(K-1) (+1), y: P + m(K-1) (+m), z: P (+m^2); kappa = sum_q theta_q F_q
+        const uint32_t m = (uint32_t)g.m, nf = (uint32_t)g.nf;
+        const uint32_t P = (uint32_t)(I - 1) + m * ((uint32_t)(J - 1) + (DIM == 3 ? m * (uint32_t)(K - 1) : 0u));
+        const uint32_t kz = DIM == 3 ? m * (uint32_t)(K - 1) : 0u;
+        const uint32_t ix = P + (uint32_t)(J - 1) + kz, iy = nf + P + kz, iz = 2u * nf + P;
+#pragma unroll
+        for (int e = 0; e < 2 * DIM; ++e) k[e] = 0.0;
+#pragma unroll 2
+        for (int q = 0; q < g.Q; ++q) {
+            const double t = th[q * ldb + b];
+            const double* F = g.faces + (size_t)q * DIM * nf;
+            k[0] = fma(t, __ldg(F + ix), k[0]);
+            k[1] = fma(t, __ldg(F + ix + 1), k[1]);
+            k[2] = fma(t, __ldg(F + iy), k[2]);
+            k[3] = fma(t, __ldg(F + iy + m), k[3]);
+            if (DIM == 3) {
+                k[4] = fma(t, __ldg(F + iz), k[4]);
+                k[5] = fma(t, __ldg(F + iz + m * m), k[5]);
+            }
         }
         return;
     }
