@@ -182,6 +182,19 @@ def run_reference(a):
 # Case 1 with RB dimension 1 and 5, Case 2 with 2 and 10 (AMB-17: the
 # text's 10 over the caption's 20), 100 random parameters per case (96 = 6 batches of 16 here)
 CASE_M, CASE_B, CASE_TRAIN, CASE_QUERIES = 127, 16, 64, 96
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_final_traffic.json")
+
+
+def ncu_traffic(config, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
+    ncu --set full capture of the same kernel and configuration (profiles/), else None."""
+    try:
+        d = json.load(open(TRAFFIC_FILE))
+        if d.get("config") == config and kernel in d:
+            return d[kernel]["dram_bytes_per_launch"], f"{os.path.relpath(TRAFFIC_FILE, ROOT)}: {d[kernel]['kernel']}"
+    except (OSError, ValueError, KeyError):
+        pass
+    return None, None
 CASE_N = {1: 5, 2: 10}
 
 
@@ -406,8 +419,9 @@ def main():
     kt = kernels[top]
     iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bq queries
     iter_bytes = sum(alg.values())
+    traffic, traffic_src = ncu_traffic(a.config, top)
     roof = {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
-            "frac": kt["GBps"] / hbm, "traffic": None, "peak_source": hbm_src,
+            "frac": kt["GBps"] / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
             "alg_bytes_per_launch": kt["alg_bytes"], "avg_launch_us": kt["avg_us"],
             "share_of_iteration": kt["share"],
             "iteration": {"us": iter_us, "alg_bytes": iter_bytes,
