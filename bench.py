@@ -9,7 +9,9 @@ B = 32, RBCG to tol 1e-10 with symmetric red-black GS.
 
 A step = one rbs_solve_batch of B queries to convergence (every row of the
 hot path: reduced assembly + Cholesky, residual, projection, reduced solve,
-prolongation, smoothing, CG recurrences, stop test).  N > 1: one process per
+prolongation, smoothing, CG recurrences, stop test).  Batches are independent:
+--streams S (default 2) runs S of them at a time on S CUDA streams, each with
+its own context, so one batch's latency-bound passes overlap another's.  N > 1: one process per
 GPU (torchrun), queries sharded (rank r solves its own 256), no collective on
 the data path: weak scaling.  Timing: CUDA events on the solve stream after a
 barrier + synchronize, max over ranks.  The working set (W 84 MB + four 67 MB
@@ -26,6 +28,7 @@ import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 import numpy as np
@@ -52,6 +55,7 @@ def parse():
     p.add_argument("--config", default="c2")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-iters", type=int, default=30)
+    p.add_argument("--streams", type=int, default=2, help="concurrent batch streams (1 = one batch at a time)")
     return p.parse_args()
 
 
@@ -335,14 +339,40 @@ def main():
     mus_all = query_set(c, nq * world)
     mus = mus_all[rank * nq:(rank + 1) * nq]
     nb = nq // c.B
-    X = torch.empty((c.B, c.N), dtype=torch.float64, device=s.device)
+    # S concurrent batch streams (DESIGN.md §7 "Concurrent batches"): batch k runs on stream
+    # k mod S, each stream with its own context (same basis) and buffers; the batches are
+    # independent, so this is a scheduling choice that lets one batch's latency-bound
+    # passes overlap another's
+    S = max(1, a.streams)
+    ss = [s] + [rbs.Solver(c.dim, c.m, c.blocks, device=local).load_basis(W, ANq.cpu().numpy(), fn.cpu().numpy())
+                for _ in range(S - 1)]
+    sts = [torch.cuda.Stream(device=s.device) for _ in range(S)]
+    Xs = [torch.empty((c.B, c.N), dtype=torch.float64, device=s.device) for _ in range(S)]
 
-    def step(k, **kw):
+    def step(t, k, **kw):
         b = k % nb
-        return s.solve_batch(mus[b * c.B:(b + 1) * c.B], X=X, want_a_n=False, **kw)
+        return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xs[t], stream=sts[t], want_a_n=False, **kw)
 
-    for w in range(max(a.warmup, 1)):
-        step(w)
+    def run(nsteps, fn, nvtx=None):
+        outs = [[] for _ in range(S)]
+
+        def worker(t):
+            torch.cuda.set_device(local)
+            if nvtx:
+                torch.cuda.nvtx.range_push(nvtx)
+            for k in range(t, nsteps, S):
+                outs[t].append(fn(t, k))
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
+
+        th = [threading.Thread(target=worker, args=(t,)) for t in range(S)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        return [o for ol in outs for o in ol]
+
+    run(max(a.warmup, S), step)
     # ---- timed region (device events, max over ranks) ------------------------
     clocks = Clocks(local)
     clocks.start()
@@ -352,16 +382,17 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include "timed/" profiles only this
     ev0.record(stream)
-    launches, its = 0, []
-    for k in range(a.steps):
-        out = step(k)
-        launches += out["launches"]
-        its += [int(i) for i in out["its"]]
-        assert all(st == "CONVERGED" for st in out["status"]), out["status"]
+    outs = run(a.steps, step, nvtx="timed")     # every worker thread marks its launches too
+    torch.cuda.synchronize()
     ev1.record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    launches, its = 0, []
+    for out in outs:
+        launches += out["launches"]
+        its += [int(i) for i in out["its"]]
+        assert all(st == "CONVERGED" for st in out["status"]), out["status"]
     if world > 1:
         t = torch.tensor([ms], device=s.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -375,15 +406,18 @@ def main():
         its = [int(v) for v in all_its.cpu()]
 
     # ---- e2e: public API with host buffers (pinned X, host mu) --------------
-    Xh = torch.empty((c.B, c.N), dtype=torch.float64, pin_memory=True)
+    Xh = [torch.empty((c.B, c.N), dtype=torch.float64, pin_memory=True) for _ in range(S)]
+
+    def step_host(t, k):
+        b = k % nb
+        return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xh[t], x_location=rbs.RBS_MEM_HOST,
+                                 stream=sts[t], want_a_n=True)
+
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t = time.perf_counter()
-    for k in range(a.steps):
-        b = k % nb
-        s.solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xh, x_location=rbs.RBS_MEM_HOST,
-                      want_a_n=True)
+    run(a.steps, step_host)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t
     if world > 1:
@@ -395,7 +429,7 @@ def main():
            "d2h_bytes_per_step": c.B * c.N * 8 + c.B * (4 + 4 + 8 + 8 + 8 * c.n)}
 
     # ---- per-kernel device times (eager, events on the launching stream) -----
-    prof = step(0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
+    prof = step(0, 0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
     hbm, hbm_src = peaks()
     # queries per pass: 2D batches above 32 run as 32-query sub-batches
     Bq, N, n = (min(c.B, 32) if c.dim == 2 else c.B), c.N, c.n
@@ -435,6 +469,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(c), "queries_per_gpu": nq, "B": c.B, "n": c.n,
                        "parallelism": f"query-shard x{world}" if world > 1 else "1 GPU",
+                       "concurrent_batches": S,
                        "l2": "inputs larger than L2 (W 84 MB + 4 x 67 MB state > 126 MB)",
                        "its_min_med_max": [min(its), int(np.median(its)), max(its)],
                        "offline_greedy_s": round(offline_s, 2), "snapshot_its": snap[:6]},
