@@ -73,7 +73,11 @@ enum { RBS_RBI = 0, RBS_RBCG = 1 };
  * mesh slabs) */
 enum { RBS_SMOOTH_SYM_RBGS = 0, RBS_SMOOTH_FWD_RBGS = 1, RBS_SMOOTH_JACOBI = 2 };
 enum { RBS_MEM_DEVICE = 0, RBS_MEM_HOST = 1 };
-enum { RBS_GREEDY_PLAIN = 0, RBS_GREEDY_ADAPTIVE = 1 };
+/* greedy modes: PLAIN (algorithm0), ADAPTIVE (algorithm3),
+ * SAMPLES: adaptive snapshots at the given parameters in list order, no selection -- the
+ * fine-grid half of the multi-fidelity approach: select on a coarse grid,
+ * then build the fine basis from the selected parameters */
+enum { RBS_GREEDY_PLAIN = 0, RBS_GREEDY_ADAPTIVE = 1, RBS_GREEDY_SAMPLES = 2 };
 
 int rbs_version(void);
 const char* rbs_status_string(rbs_status s);

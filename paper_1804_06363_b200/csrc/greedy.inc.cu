@@ -128,7 +128,9 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
     if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
     if (n_train < 1 || n_max < 1 || n_max > RBS_MAX_N) return fail(ctx, RBS_E_DIM, "bad n_train/n_max");
     if (!mu_train || !W_out || !n_out || !workspace) return fail(ctx, RBS_E_ARG, "NULL argument");
-    if (mode != RBS_GREEDY_PLAIN && mode != RBS_GREEDY_ADAPTIVE) return fail(ctx, RBS_E_ARG, "bad mode");
+    if (mode != RBS_GREEDY_PLAIN && mode != RBS_GREEDY_ADAPTIVE && mode != RBS_GREEDY_SAMPLES)
+        return fail(ctx, RBS_E_ARG, "bad mode");
+    const bool from_list = mode == RBS_GREEDY_SAMPLES;   // multi-fidelity fine half
     GreedyLayout L = greedy_layout(ctx, n_train, n_max, workspace);
     if (ws_bytes < L.bytes) return fail(ctx, RBS_E_NOMEM, "workspace too small");
     CK(cudaSetDevice(ctx->device));
@@ -175,7 +177,7 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
     };
     while (n < n_max && cand >= 0) {
         // ---- Step 3: snapshot x(mu_N) = RBCG(A, f, W_{N-1}) -------------------
-        ctx->n = mode == RBS_GREEDY_ADAPTIVE ? n : 0;
+        ctx->n = mode != RBS_GREEDY_PLAIN ? n : 0;
         ctx->hfn.assign(hf.begin(), hf.begin() + ctx->n);
         ctx->hANq.assign((size_t)Q * ctx->n * ctx->n, 0.0);
         for (int q = 0; q < Q; ++q)
@@ -276,6 +278,10 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
             if (snap_iters) snap_iters[n] = its;
             ++n;
             CK(cudaMemcpyAsync(L.ANq, hA.data(), hA.size() * 8, cudaMemcpyHostToDevice, st));
+        }
+        if (from_list) {             // next sample in list order; no indicator solves
+            cand = cand + 1 < nt ? cand + 1 : -1;
+            continue;
         }
         if (n == 0) {
             cand = -1;

@@ -501,3 +501,25 @@ def test_rbi_many_half_sweeps_flat_path(orc, rbs, smoother, sweeps):
                         record_history=1)
     compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbi", max_iter=500000, smoother=smoother,
             sweeps=sweeps)
+
+
+def test_gpu_basis_from_samples_matches_oracle(orc, rbs):
+    """RBS_GREEDY_SAMPLES (multi-fidelity fine half): select on a coarse grid
+    (oracle greedy on 31^2), then build the fine basis from the selected parameters on the
+    GPU; equals the oracle's or_basis_from_samples (same snapshots, MGS, offline blocks)."""
+    dim, blocks, n = 2, (3, 3), 8
+    gc = orc.Grid(dim, 31, blocks)
+    rng = np.random.default_rng(31)
+    tr = 0.1 * 100 ** rng.random((60, gc.Q))
+    coarse = gc.greedy(tr, n)
+    mus = tr[coarse["selected"]]
+    gf = orc.Grid(dim, 63, blocks)
+    ref = gf.basis_from_samples(mus)
+    s = rbs.Solver(dim, 63, blocks)
+    res = s.build_greedy(mus, n, samples=True)
+    assert res["n"] == ref["n"] == n
+    assert np.array_equal(res["selected"], np.arange(n))
+    W = res["W"].cpu().numpy()
+    assert np.abs(W - ref["W"]).max() <= 1e-8
+    assert np.abs(res["ANq"] - ref["ANq"]).max() <= 1e-8 * np.abs(ref["ANq"]).max()
+    assert np.abs(res["fn"] - ref["fn"]).max() <= 1e-8 * np.abs(ref["fn"]).max()
