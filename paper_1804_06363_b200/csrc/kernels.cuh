@@ -522,6 +522,105 @@ __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Red-black half-sweep for 3D grids, row-pencil form: each group of Bp lanes (one
+// query per lane) walks a (J, K) row of nodes in x, keeping the x-neighbours in
+// registers (one new load per node) and updating the nodes of the sweep's colour
+// with the same arithmetic as k_gs (node_kappa, gs_value; eq8,
+// AMB-5/6).  Nodes inside one block take the block's theta without the cell-average
+// (bitwise the same, see node_kappa).  LAST: y^T r, y^T y over every owned node.
+// Requires Bp <= 32.
+// ---------------------------------------------------------------------------
+
+// the general edge coefficients (block interfaces, face operators) out of line: keeps the
+// register footprint of the common uniform-block path small
+__device__ __noinline__ void node_kappa3_call(const Geo& g, const double* th, int ldb, int b, int I, int J,
+                                              int K, double* k) {
+    node_kappa<3>(g, th, ldb, b, I, J, K, k);
+}
+
+template <bool LAST, int kGsSeg>
+__global__ void __launch_bounds__(kFlat, kGsSeg <= 2 ? 2 : 1) k_gs3r(GSArgs a) {
+    if (a.done && ld_flag(a.done)) return;
+    extern __shared__ double smem[];
+    double* s_th = smem;
+    int* s_act = (int*)(s_th + a.g.Q * a.Bp);
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kFlat) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kFlat) s_act[t] = a.active[t];
+    __syncthreads();
+    const Geo& g = a.g;
+    const int Bp = a.Bp, m = g.m;
+    const int lane = threadIdx.x & 31, rpw = 32 >> a.lgB;
+    const int sub = lane >> a.lgB, b = lane & (Bp - 1);
+    const int nseg = (m + kGsSeg - 1) / kGsSeg;
+    const int64_t items = (int64_t)m * g.mz * nseg;
+    const int64_t nw = ((int64_t)gridDim.x * kFlat) >> 5;
+    const int64_t w0 = (blockIdx.x * (int64_t)kFlat + threadIdx.x) >> 5;
+    const int64_t sy = (int64_t)m * Bp, sz = sy * m;
+    double yr = 0.0, yy = 0.0;
+    if (s_act[b]) {
+        for (int64_t it = w0 * rpw + sub; it < items; it += nw * rpw) {
+            const int64_t row = it / nseg;
+            const int x0 = 1 + (int)(it - row * nseg) * kGsSeg;
+            const int J = (int)(row % m) + 1, Kl = (int)(row / m), K = Kl + 1 + g.kofs;
+            double* Yr = a.Y + ((int64_t)Kl * m * m + (int64_t)(J - 1) * m) * Bp + b;   // node x at Yr[(x-1)Bp]
+            const double* Rr = a.Rhs ? a.Rhs + ((int64_t)Kl * m * m + (int64_t)(J - 1) * m) * Bp + b : nullptr;
+            const bool hym = J > 1, hyp = J < m, hzm = has_zm(g, K), hzp = has_zp(g, K);
+            const int px = (a.color - J - K) & 1;          // parity of the active x
+            // ---- all loads of the segment first (x-window, y/z neighbours, rhs) ----
+            double yv[kGsSeg + 2], q[kGsSeg][4], rh[kGsSeg];
+#pragma unroll
+            for (int j = 0; j < kGsSeg + 2; ++j) {
+                const int x = x0 - 1 + j;
+                yv[j] = (x >= 1 && x <= m) ? __ldg(Yr + (int64_t)(x - 1) * Bp) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < kGsSeg; ++j) {
+                const int x = x0 + j;
+                const int64_t o = (int64_t)(x - 1) * Bp;
+                const bool in = x <= m, act = in && ((x ^ px) & 1) == 0;
+                q[j][0] = act && hym ? __ldg(Yr + o - sy) : 0.0;
+                q[j][1] = act && hyp ? __ldg(Yr + o + sy) : 0.0;
+                q[j][2] = act && hzm ? __ldg(Yr + o - sz) : 0.0;
+                q[j][3] = act && hzp ? __ldg(Yr + o + sz) : 0.0;
+                rh[j] = (Rr && in && (act || LAST)) ? __ldg(Rr + o) : a.rconst;
+            }
+            // ---- updates of the sweep's colour ----------------------------------------
+            const int by0 = axis_block(g, J - 1, g.py) * g.px, by1 = axis_block(g, J, g.py) * g.px;
+            const int pxy = g.px * g.py;
+            const int bz0 = axis_block(g, K - 1, g.pz) * pxy, bz1 = axis_block(g, K, g.pz) * pxy;
+            const bool rowu = !g.faces && by0 == by1 && bz0 == bz1;
+            const bool own = owned(g, K);
+#pragma unroll
+            for (int j = 0; j < kGsSeg; ++j) {
+                const int x = x0 + j;
+                if (x > m) break;
+                if (((x ^ px) & 1) == 0) {
+                    double nb[6] = {yv[j], yv[j + 2], q[j][0], q[j][1], q[j][2], q[j][3]}, k[6];
+                    const int bxl = axis_block(g, x - 1, g.px), bxr = axis_block(g, x, g.px);
+                    if (rowu && bxl == bxr) {
+                        const double c = s_th[(bxr + by0 + bz0) * Bp + b];
+#pragma unroll
+                        for (int e = 0; e < 6; ++e) k[e] = c;
+                    } else {
+                        node_kappa3_call(g, s_th, Bp, b, x, J, K, k);
+                    }
+                    const double v = gs_value<3>(g, k, rh[j], nb);
+                    Yr[(int64_t)(x - 1) * Bp] = v;
+                    if (LAST && own) {
+                        yr = fma(v, rh[j], yr);
+                        yy = fma(v, v, yy);
+                    }
+                } else if (LAST && own) {
+                    yr = fma(yv[j + 1], rh[j], yr);
+                    yy = fma(yv[j + 1], yv[j + 1], yy);
+                }
+            }
+        }
+    }
+    if (LAST) gs_step10(a, yr, yy);
+}
+
+// ---------------------------------------------------------------------------
 // Damped Jacobi sweep ("the smoother (Jacobi or Gauss-Seidel)"):
 //   y_out = y_in + omega (g - y_in), g = the Gauss-Seidel point value of y_in,
 // i.e. y_in + omega D^-1 (b - A y_in).  Ping-pong buffers; frozen lanes copy.

@@ -1,0 +1,32 @@
+"""Profiling driver for the flat 3D passes: thermal blocks 2x2x2 on M^3 (default 127), B = 16,
+GPU greedy n = 20 from 64 training mu, then K RBCG iterations eagerly (tol = 0).
+python tools/prof_3d.py [--m 127] [--iters 2] [--faces]"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1804_06363_b200 as rbs  # noqa: E402
+from synth import cases  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--m", type=int, default=127)
+ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--faces", action="store_true")
+a = ap.parse_args()
+blocks = (2, 2, 2)
+rng = np.random.default_rng(5)
+tr = 0.1 * 100 ** rng.random((64, 8))
+if a.faces:
+    s = rbs.Solver(3, a.m, faces=cases.faces_from_blocks(3, a.m, blocks))
+else:
+    s = rbs.Solver(3, a.m, blocks)
+s.build_greedy(tr, 20)
+mus = 0.1 * 100 ** rng.random((16, 8))
+out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False)
+torch.cuda.synchronize()
+print(json.dumps({k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]] for k, v in out["profile"].items() if v[1]}))
