@@ -702,6 +702,43 @@ struct CGPArgs {
 
 constexpr int kCgpUnroll = 2;
 
+// sigma partials of this CTA and RBCG Step 5 (alpha = rho / p^T A p) with
+// the MAXIT / CURVATURE checks in the last CTA (AMB-11)
+__device__ __forceinline__ void cgp_step5(CGPArgs& a, double sig) {
+    __shared__ double s_a[kFlat];
+    __shared__ double s_sig[kMaxBatch];
+    __shared__ int s_last;
+    SolveState& s = a.s;
+    s_a[threadIdx.x] = sig;
+    __syncthreads();
+    if (threadIdx.x < a.Bp) {
+        double t0 = 0.0;
+        for (int t = threadIdx.x; t < kFlat; t += a.Bp) t0 += s_a[t];
+        s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + a.col0 + blockIdx.x] = t0;
+    }
+    if (!a.ext && cta_is_last(s.ticket, &s_last)) {
+        cta_sum_slot(s, 0, s_a, s_sig);
+        const int k = ld_flag(s.kcount);
+        if (threadIdx.x < s.Bp) {
+            const int bb = threadIdx.x;
+            double al = 0.0;
+            if (s.active[bb]) {
+                const double sg = s_sig[bb];
+                if (k >= s.maxit) { s.status[bb] = Q_MAXIT; s.its[bb] = k; s.active[bb] = 0; }
+                else if (!(sg > 0.0)) {
+                    s.status[bb] = isfinite(sg) ? Q_CURVATURE : Q_NONFINITE;
+                    s.its[bb] = k;
+                    s.active[bb] = 0;
+                } else al = s.rho[bb] / sg;
+            }
+            s.alpha[bb] = al;
+        }
+        __threadfence();
+        update_done(s);
+        release_ticket(s.ticket);
+    }
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
     if (a.done && ld_flag(a.done)) return;
@@ -755,38 +792,7 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
                 }
         }
     }
-    __shared__ double s_a[kFlat];
-    __shared__ double s_sig[kMaxBatch];
-    __shared__ int s_last;
-    SolveState& s = a.s;
-    s_a[threadIdx.x] = sig;
-    __syncthreads();
-    if (threadIdx.x < a.Bp) {
-        double t0 = 0.0;
-        for (int t = threadIdx.x; t < kFlat; t += a.Bp) t0 += s_a[t];
-        s.partF[((int64_t)threadIdx.x * 2 + 0) * s.nctf + a.col0 + blockIdx.x] = t0;
-    }
-    if (!a.ext && cta_is_last(s.ticket, &s_last)) {
-        cta_sum_slot(s, 0, s_a, s_sig);
-        const int k = ld_flag(s.kcount);
-        if (threadIdx.x < s.Bp) {
-            const int bb = threadIdx.x;
-            double al = 0.0;
-            if (s.active[bb]) {
-                const double sg = s_sig[bb];
-                if (k >= s.maxit) { s.status[bb] = Q_MAXIT; s.its[bb] = k; s.active[bb] = 0; }
-                else if (!(sg > 0.0)) {
-                    s.status[bb] = isfinite(sg) ? Q_CURVATURE : Q_NONFINITE;
-                    s.its[bb] = k;
-                    s.active[bb] = 0;
-                } else al = s.rho[bb] / sg;
-            }
-            s.alpha[bb] = al;
-        }
-        __threadfence();
-        update_done(s);
-        release_ticket(s.ticket);
-    }
+    cgp_step5(a, sig);
 }
 
 // ---------------------------------------------------------------------------

@@ -29,4 +29,14 @@ s.build_greedy(tr, 20)
 mus = 0.1 * 100 ** rng.random((16, 8))
 out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False)
 torch.cuda.synchronize()
-print(json.dumps({k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]] for k, v in out["profile"].items() if v[1]}))
+prof = {k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]] for k, v in out["profile"].items() if v[1]}
+# graph-mode iteration time (the way bench.py runs): a fixed 200-iteration solve
+s.solve_batch(mus, tol=0.0, max_iter=50, want_a_n=False)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+e0.record()
+s.solve_batch(mus, tol=0.0, max_iter=200, want_a_n=False)
+e1.record()
+torch.cuda.synchronize()
+prof["graph_us_per_iter"] = round(e0.elapsed_time(e1) * 1e3 / 200, 1)
+print(json.dumps(prof))
