@@ -862,8 +862,13 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             } else if (Bp <= 32 && !(v2off & 8) && a.color >= 0) {   // row pencils (x in registers)
                 // 4-node row segments, all loads of a segment in flight (128 registers,
                 // one CTA per SM: measured 2.2x the element-per-thread k_gs at 127^3, B = 16)
-                if (l) k_gs3r<true, 4><<<nctf, kFlat, fsm, st>>>(a);
-                else k_gs3r<false, 4><<<nctf, kFlat, fsm, st>>>(a);
+                if (g.faces) {
+                    if (l) k_gs3r<true, 4, true><<<nctf, kFlat, fsm, st>>>(a);
+                    else k_gs3r<false, 4, true><<<nctf, kFlat, fsm, st>>>(a);
+                } else {
+                    if (l) k_gs3r<true, 4, false><<<nctf, kFlat, fsm, st>>>(a);
+                    else k_gs3r<false, 4, false><<<nctf, kFlat, fsm, st>>>(a);
+                }
             } else {
                 if (l) k_gs<3, true><<<nctf, kFlat, fsm, st>>>(a);
                 else k_gs<3, false><<<nctf, kFlat, fsm, st>>>(a);

@@ -538,7 +538,7 @@ __device__ __noinline__ void node_kappa3_call(const Geo& g, const double* th, in
     node_kappa<3>(g, th, ldb, b, I, J, K, k);
 }
 
-template <bool LAST, int kGsSeg>
+template <bool LAST, int kGsSeg, bool FACES>
 __global__ void __launch_bounds__(kFlat, kGsSeg <= 2 ? 2 : 1) k_gs3r(GSArgs a) {
     if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
@@ -597,7 +597,9 @@ __global__ void __launch_bounds__(kFlat, kGsSeg <= 2 ? 2 : 1) k_gs3r(GSArgs a) {
                 if (((x ^ px) & 1) == 0) {
                     double nb[6] = {yv[j], yv[j + 2], q[j][0], q[j][1], q[j][2], q[j][3]}, k[6];
                     const int bxl = axis_block(g, x - 1, g.px), bxr = axis_block(g, x, g.px);
-                    if (rowu && bxl == bxr) {
+                    if (FACES) {            // face operator: inline face loads (AMB-23)
+                        node_kappa_faces<3>(g, s_th, Bp, b, x, J, K, k);
+                    } else if (rowu && bxl == bxr) {
                         const double c = s_th[(bxr + by0 + bz0) * Bp + b];
 #pragma unroll
                         for (int e = 0; e < 6; ++e) k[e] = c;

@@ -91,31 +91,38 @@ __device__ __forceinline__ int axis_block(const Geo& g, int a, int p) {
 // Edge coefficients of node (I,J,K) in neighbour order -x,+x,-y,+y(,-z,+z):
 // mean of the cells sharing the edge (AMB-1), summed in AMB-4 order.
 // th: theta laid out [q][ldb] (ldb = batch stride), b = this lane's query.
+// face-operator edge coefficients (rbs_set_operator_faces, AMB-23)
+template <int DIM>
+__device__ __forceinline__ void node_kappa_faces(const Geo& g, const double* th, int ldb, int b,
+                                                 int I, int J, int K, double* k) {
+    // face indices from the node index P (layout in include/rbs.h):
+    // x: P + (J-1) + m(K-1) (+1), y: P + m(K-1) (+m), z: P (+m^2); kappa = sum_q theta_q F_q
+    const uint32_t m = (uint32_t)g.m, nf = (uint32_t)g.nf;
+    const uint32_t P = (uint32_t)(I - 1) + m * ((uint32_t)(J - 1) + (DIM == 3 ? m * (uint32_t)(K - 1) : 0u));
+    const uint32_t kz = DIM == 3 ? m * (uint32_t)(K - 1) : 0u;
+    const uint32_t ix = P + (uint32_t)(J - 1) + kz, iy = nf + P + kz, iz = 2u * nf + P;
+#pragma unroll
+    for (int e = 0; e < 2 * DIM; ++e) k[e] = 0.0;
+#pragma unroll 2
+    for (int q = 0; q < g.Q; ++q) {
+        const double t = th[q * ldb + b];
+        const double* F = g.faces + (size_t)q * DIM * nf;
+        k[0] = fma(t, __ldg(F + ix), k[0]);
+        k[1] = fma(t, __ldg(F + ix + 1), k[1]);
+        k[2] = fma(t, __ldg(F + iy), k[2]);
+        k[3] = fma(t, __ldg(F + iy + m), k[3]);
+        if (DIM == 3) {
+            k[4] = fma(t, __ldg(F + iz), k[4]);
+            k[5] = fma(t, __ldg(F + iz + m * m), k[5]);
+        }
+    }
+}
+
 template <int DIM>
 __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int ldb, int b,
                                            int I, int J, int K, double* k) {
     if (g.faces) {
-        // face indices from the node index P (layout in include/rbs.h):
-        // x: P + (J-1) + m(K-1) (+1), y: P + m(K-1) (+m), z: P (+m^2); kappa = sum_q theta_q F_q
-        const uint32_t m = (uint32_t)g.m, nf = (uint32_t)g.nf;
-        const uint32_t P = (uint32_t)(I - 1) + m * ((uint32_t)(J - 1) + (DIM == 3 ? m * (uint32_t)(K - 1) : 0u));
-        const uint32_t kz = DIM == 3 ? m * (uint32_t)(K - 1) : 0u;
-        const uint32_t ix = P + (uint32_t)(J - 1) + kz, iy = nf + P + kz, iz = 2u * nf + P;
-#pragma unroll
-        for (int e = 0; e < 2 * DIM; ++e) k[e] = 0.0;
-#pragma unroll 2
-        for (int q = 0; q < g.Q; ++q) {
-            const double t = th[q * ldb + b];
-            const double* F = g.faces + (size_t)q * DIM * nf;
-            k[0] = fma(t, __ldg(F + ix), k[0]);
-            k[1] = fma(t, __ldg(F + ix + 1), k[1]);
-            k[2] = fma(t, __ldg(F + iy), k[2]);
-            k[3] = fma(t, __ldg(F + iy + m), k[3]);
-            if (DIM == 3) {
-                k[4] = fma(t, __ldg(F + iz), k[4]);
-                k[5] = fma(t, __ldg(F + iz + m * m), k[5]);
-            }
-        }
+        node_kappa_faces<DIM>(g, th, ldb, b, I, J, K, k);
         return;
     }
     const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
