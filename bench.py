@@ -436,7 +436,10 @@ def main():
     # algorithmic bytes per launch (each vector once, W once per batch)
     alg = {"k_cgp": 24 * Bq * N,                    # y, p_old read; p_new written
            "k_proj": 40 * Bq * N + 8 * N * n,       # p, x, r read; x, r written; W
-           "k_gs": 16 * Bq * N + 8 * N * n}         # r read, y written; W
+           "k_gs": 16 * Bq * N + 8 * N * n}         # 2D fused smoother: r read, y written; W
+    if c.dim == 3:   # separate prolongation pass; k_gs is one red-black half-sweep per launch
+        alg["k_prolong"] = 8 * Bq * N + 8 * N * n   # W read, y0 written
+        alg["k_gs"] = 16 * Bq * N                   # y read, r and y of one colour
     flops = {"k_proj": 2.0 * N * n * Bq, "k_gs": 2.0 * N * n * Bq}   # W^T r / W e on DMMA
     tot_ms = sum(v[0] for v in prof.values())
     kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
@@ -452,7 +455,7 @@ def main():
     top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
     kt = kernels[top]
     iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bq queries
-    iter_bytes = sum(alg.values())
+    iter_bytes = (80 * Bq + 16 * n) * N     # RBCG minimum per batch-iteration
     traffic, traffic_src = ncu_traffic(a.config, top)
     roof = {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": kt["GBps"] / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
