@@ -413,6 +413,7 @@ def main():
         return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xh[t], x_location=rbs.RBS_MEM_HOST,
                                  stream=sts[t], want_a_n=True)
 
+    run(S, step_host)      # warm-up: host-output workspace and its iteration graph per context
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
