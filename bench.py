@@ -468,13 +468,18 @@ def main():
             "fp64_tensor_peak_tflops": FP64_TENSOR_MEASURED_TFS,
             "fp64_tensor_peak_source": "measured, tools/fp64_peak.cu (DMMA m8n8k4, all SMs)"}
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+    wbytes, sbytes = c.N * (((c.n + 7) // 8) * 8 + 4) * 8, 4 * c.N * c.B * 8
+    l2 = (f"inputs larger than L2 (W {wbytes / 1e6:.0f} MB + 4 x {sbytes / 4e6:.0f} MB state > 126 MB)"
+          if wbytes + sbytes > 126e6 else
+          f"inputs fit in L2 (W {wbytes / 1e6:.1f} MB + state {sbytes / 1e6:.1f} MB): warm-L2 figure")
+    metric = METRIC.replace("(c2,", f"({c.name},")
+    line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(c), "queries_per_gpu": nq, "B": c.B, "n": c.n,
                        "parallelism": f"query-shard x{world}" if world > 1 else "1 GPU",
                        "concurrent_batches": S,
-                       "l2": "inputs larger than L2 (W 84 MB + 4 x 67 MB state > 126 MB)",
+                       "l2": l2,
                        "its_min_med_max": [min(its), int(np.median(its)), max(its)],
                        "offline_greedy_s": round(offline_s, 2), "snapshot_its": snap[:6]},
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
