@@ -169,7 +169,7 @@ def run_reference(a):
         its_all += its
     el = time.perf_counter() - t0
     v = tot_q / el
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+    line = {"impl": "reference", "metric": METRIC.replace("(c2,", f"({c.name},"), "value": v, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * el / a.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
