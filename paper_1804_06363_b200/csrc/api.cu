@@ -919,6 +919,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         CGPArgs a{};
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.s = S; a.done = done;
+        int nl = 1;
         pb(RBS_K_CGP);
         if (!(v2off & 2) && g.dim == 2 && Bp <= 32 && !g.faces) {
             CGP2Args c2{};
@@ -932,9 +933,15 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             else if (Bp == 16) k_cgp2<16><<<gr, kMT, csm, st>>>(c2);
             else k_cgp2<32><<<gr, kMT, csm, st>>>(c2);
         } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
-        else k_cgp<3><<<nctf, kFlat, fsm, st>>>(a);
+        else if (Bp <= 32 && !(v2off & 8)) {      // two passes: stream p_new, then sigma in row segments
+            const int64_t nb2 = (int64_t)g.N * Bp / 2;
+            k_pnew3<<<(unsigned)std::min<int64_t>((nb2 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(
+                a.Y, a.Pold, a.Pnew, a.beta, a.active, nb2, Bp, a.done);
+            k_sigma3r<4><<<nctf, kFlat, fsm, st>>>(a);
+            nl = 2;
+        } else k_cgp<3><<<nctf, kFlat, fsm, st>>>(a);
         pe();
-        return 1;
+        return nl;
     };
 
     // 2D: prolongation + all half-sweeps (+ y^T r) in one row-marching pass

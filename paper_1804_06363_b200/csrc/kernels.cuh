@@ -798,6 +798,102 @@ __global__ void __launch_bounds__(kFlat, 2) k_cgp(CGPArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// RBCG Step 11 + Step 5 for 3D grids in two passes (instead of recomputing p_new on
+// the six neighbours of every node): k_pnew3 streams p_new = y + beta p_old
+// for every node; k_sigma3r forms sigma = p_new^T A p_new (Step 5,
+// PAPER.md:269) in k_gs3r's row segments (x window + y/z neighbours loaded together)
+// and computes alpha in the last CTA.  Per node the same arithmetic as k_cgp<3>.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_pnew3(const double* __restrict__ Y, const double* __restrict__ Pold,
+                                               double* __restrict__ Pnew, const double* __restrict__ beta,
+                                               const int* __restrict__ active, int64_t NB2, int Bp,
+                                               const int* done) {
+    if (done && ld_flag(done)) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < NB2; e += stride) {
+        const int b = (int)((2 * e) & (Bp - 1));          // lanes b, b+1 of one node
+        const double2 y = __ldg(reinterpret_cast<const double2*>(Y) + e);
+        const double2 p = __ldg(reinterpret_cast<const double2*>(Pold) + e);
+        const bool a0 = active[b] != 0, a1 = active[b + 1] != 0;
+        if (!a0 && !a1) continue;
+        double2 o = reinterpret_cast<double2*>(Pnew)[e];
+        if (a0) o.x = fma(beta[b], p.x, y.x);
+        if (a1) o.y = fma(beta[b + 1], p.y, y.y);
+        reinterpret_cast<double2*>(Pnew)[e] = o;
+    }
+}
+
+template <int SEG>
+__global__ void __launch_bounds__(kFlat, 1) k_sigma3r(CGPArgs a) {
+    if (a.done && ld_flag(a.done)) return;
+    extern __shared__ double smem[];
+    double* s_th = smem;
+    int* s_act = (int*)(s_th + a.g.Q * a.Bp);
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kFlat) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kFlat) s_act[t] = a.active[t];
+    __syncthreads();
+    const Geo& g = a.g;
+    const int Bp = a.Bp, m = g.m;
+    const int lane = threadIdx.x & 31, rpw = 32 >> a.lgB;
+    const int sub = lane >> a.lgB, b = lane & (Bp - 1);
+    const int nseg = (m + SEG - 1) / SEG;
+    const int64_t items = (int64_t)m * g.mz * nseg;
+    const int64_t nw = ((int64_t)gridDim.x * kFlat) >> 5;
+    const int64_t w0 = (blockIdx.x * (int64_t)kFlat + threadIdx.x) >> 5;
+    const int64_t sy = (int64_t)m * Bp, sz = sy * m;
+    const double* P = a.Pnew;
+    double sig = 0.0;
+    if (s_act[b]) {
+        for (int64_t it = w0 * rpw + sub; it < items; it += nw * rpw) {
+            const int64_t row = it / nseg;
+            const int x0 = 1 + (int)(it - row * nseg) * SEG;
+            const int J = (int)(row % m) + 1, Kl = (int)(row / m), K = Kl + 1 + g.kofs;
+            const double* Pr = P + ((int64_t)Kl * m * m + (int64_t)(J - 1) * m) * Bp + b;
+            const bool hym = J > 1, hyp = J < m, hzm = has_zm(g, K), hzp = has_zp(g, K);
+            double pw[SEG + 2], q[SEG][4];
+#pragma unroll
+            for (int j = 0; j < SEG + 2; ++j) {
+                const int x = x0 - 1 + j;
+                pw[j] = (x >= 1 && x <= m) ? __ldg(Pr + (int64_t)(x - 1) * Bp) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const int x = x0 + j;
+                const int64_t o = (int64_t)(x - 1) * Bp;
+                const bool in = x <= m;
+                q[j][0] = in && hym ? __ldg(Pr + o - sy) : 0.0;
+                q[j][1] = in && hyp ? __ldg(Pr + o + sy) : 0.0;
+                q[j][2] = in && hzm ? __ldg(Pr + o - sz) : 0.0;
+                q[j][3] = in && hzp ? __ldg(Pr + o + sz) : 0.0;
+            }
+            const int by0 = axis_block(g, J - 1, g.py) * g.px, by1 = axis_block(g, J, g.py) * g.px;
+            const int pxy = g.px * g.py;
+            const int bz0 = axis_block(g, K - 1, g.pz) * pxy, bz1 = axis_block(g, K, g.pz) * pxy;
+            const bool rowu = !g.faces && by0 == by1 && bz0 == bz1;
+            const bool own = owned(g, K);
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) {
+                const int x = x0 + j;
+                if (x > m) break;
+                double k[6];
+                const int bxl = axis_block(g, x - 1, g.px), bxr = axis_block(g, x, g.px);
+                if (rowu && bxl == bxr) {
+                    const double c = s_th[(bxr + by0 + bz0) * Bp + b];
+#pragma unroll
+                    for (int e = 0; e < 6; ++e) k[e] = c;
+                } else {
+                    node_kappa3_call(g, s_th, Bp, b, x, J, K, k);
+                }
+                const double nb[6] = {pw[j], pw[j + 2], q[j][0], q[j][1], q[j][2], q[j][3]};
+                const double qv = stencil_apply<3>(g, k, pw[j + 1], nb);
+                if (own) sig = fma(pw[j + 1], qv, sig);
+            }
+        }
+    }
+    cgp_step5(a, sig);
+}
+
+// ---------------------------------------------------------------------------
 // Stage 2 of W^T r / ||r||^2 + stop test + reduced solve (RBCG Steps 7-9,
 // RBI Steps 2-5).  One CTA per query.  All partial loads are issued at once
 // (each thread sums a fixed chunk of one row, then the chunks are combined in
