@@ -910,10 +910,18 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         a.part = L.partP; a.done = use_active ? done : nullptr;
         a.nct = use_active ? nct : nct_plain;
         pb(RBS_K_PROJ);
-        if (mode == MODE_CG) launch_proj<MODE_CG>(g, a.nct, psm, st, a);
+        int nl = 1;
+        if (mode == MODE_CG && g.dim == 3 && use_active && Bp <= 32 && !(v2off & 8)) {
+            // two passes: x, r update in row segments, then W^T r, ||r||^2 on the new r
+            k_xr3r<4><<<nctf, kFlat, fsm, st>>>(a, lgB);
+            ProjArgs b2 = a;
+            b2.V = L.R;
+            launch_proj<MODE_PLAIN>(g, a.nct, psm, st, b2);
+            nl = 2;
+        } else if (mode == MODE_CG) launch_proj<MODE_CG>(g, a.nct, psm, st, a);
         else launch_proj<MODE_RESID>(g, a.nct, psm, st, a);
         pe();
-        return 1;
+        return nl;
     };
     auto cgp = [&](const double* Pold, double* Pnew) {
         CGPArgs a{};

@@ -309,6 +309,83 @@ __global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// RBCG Steps 6-7 for 3D grids in row segments (the first half of K2 in two passes):
+// x += alpha p, r -= alpha A p with the p window and the y/z
+// neighbours of a segment loaded together; the projection W^T r and ||r||^2 follow
+// in k_proj<MODE_PLAIN> on the updated r.  Per node the same arithmetic as
+// k_proj<MODE_CG, 3>.  Requires Bp <= 32; no mesh slabs (all planes owned).
+// ---------------------------------------------------------------------------
+template <int SEG>
+__global__ void __launch_bounds__(kFlat, 1) k_xr3r(ProjArgs a, int lgB) {
+    if (a.done && ld_flag(a.done)) return;
+    extern __shared__ double smem[];
+    double* s_th = smem;
+    int* s_act = (int*)(s_th + a.g.Q * a.Bp);
+    for (int t = threadIdx.x; t < a.g.Q * a.Bp; t += kFlat) s_th[t] = a.theta[t];
+    for (int t = threadIdx.x; t < a.Bp; t += kFlat) s_act[t] = a.active[t];
+    __syncthreads();
+    const Geo& g = a.g;
+    const int Bp = a.Bp, m = g.m;
+    const int lane = threadIdx.x & 31, rpw = 32 >> lgB;
+    const int sub = lane >> lgB, b = lane & (Bp - 1);
+    const int nseg = (m + SEG - 1) / SEG;
+    const int64_t items = (int64_t)m * g.mz * nseg;
+    const int64_t nw = ((int64_t)gridDim.x * kFlat) >> 5;
+    const int64_t w0 = (blockIdx.x * (int64_t)kFlat + threadIdx.x) >> 5;
+    const int64_t sy = (int64_t)m * Bp, sz = sy * m;
+    if (!s_act[b]) return;
+    const double al = a.alpha[b];
+    for (int64_t it = w0 * rpw + sub; it < items; it += nw * rpw) {
+        const int64_t row = it / nseg;
+        const int x0 = 1 + (int)(it - row * nseg) * SEG;
+        const int J = (int)(row % m) + 1, Kl = (int)(row / m), K = Kl + 1 + g.kofs;
+        const int64_t rb = ((int64_t)Kl * m * m + (int64_t)(J - 1) * m) * Bp + b;
+        const bool hym = J > 1, hyp = J < m, hzm = has_zm(g, K), hzp = has_zp(g, K);
+        double pw[SEG + 2], q[SEG][4], xv[SEG], rv[SEG];
+#pragma unroll
+        for (int j = 0; j < SEG + 2; ++j) {
+            const int x = x0 - 1 + j;
+            pw[j] = (x >= 1 && x <= m) ? __ldg(a.P + rb + (int64_t)(x - 1) * Bp) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) {
+            const int x = x0 + j;
+            const int64_t e = rb + (int64_t)(x - 1) * Bp;
+            const bool in = x <= m;
+            q[j][0] = in && hym ? __ldg(a.P + e - sy) : 0.0;
+            q[j][1] = in && hyp ? __ldg(a.P + e + sy) : 0.0;
+            q[j][2] = in && hzm ? __ldg(a.P + e - sz) : 0.0;
+            q[j][3] = in && hzp ? __ldg(a.P + e + sz) : 0.0;
+            xv[j] = in ? a.X[e] : 0.0;
+            rv[j] = in ? a.R[e] : 0.0;
+        }
+        const int by0 = axis_block(g, J - 1, g.py) * g.px, by1 = axis_block(g, J, g.py) * g.px;
+        const int pxy = g.px * g.py;
+        const int bz0 = axis_block(g, K - 1, g.pz) * pxy, bz1 = axis_block(g, K, g.pz) * pxy;
+        const bool rowu = !g.faces && by0 == by1 && bz0 == bz1;
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) {
+            const int x = x0 + j;
+            if (x > m) break;
+            double k[6];
+            const int bxl = axis_block(g, x - 1, g.px), bxr = axis_block(g, x, g.px);
+            if (rowu && bxl == bxr) {
+                const double c = s_th[(bxr + by0 + bz0) * Bp + b];
+#pragma unroll
+                for (int e = 0; e < 6; ++e) k[e] = c;
+            } else {
+                node_kappa3_call(g, s_th, Bp, b, x, J, K, k);
+            }
+            const double nb[6] = {pw[j], pw[j + 2], q[j][0], q[j][1], q[j][2], q[j][3]};
+            const double qv = stencil_apply<3>(g, k, pw[j + 1], nb);
+            const int64_t e = rb + (int64_t)(x - 1) * Bp;
+            a.X[e] = fma(al, pw[j + 1], xv[j]);
+            a.R[e] = fma(-al, qv, rv[j]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Prolongation  Y = W E  (or Y += W E), PAPER.md:144-147 (eq7) / 165.
 // DMMA with M = 8 nodes, N = 8 queries, K = 4 basis vectors.  Each warp owns
 // one query tile (its E fragments stay in registers) and runs two node tiles
@@ -531,12 +608,6 @@ __global__ void __launch_bounds__(kFlat, 2) k_gs(GSArgs a) {
 // Requires Bp <= 32.
 // ---------------------------------------------------------------------------
 
-// the general edge coefficients (block interfaces, face operators) out of line: keeps the
-// register footprint of the common uniform-block path small
-__device__ __noinline__ void node_kappa3_call(const Geo& g, const double* th, int ldb, int b, int I, int J,
-                                              int K, double* k) {
-    node_kappa<3>(g, th, ldb, b, I, J, K, k);
-}
 
 template <bool LAST, int kGsSeg, bool FACES>
 __global__ void __launch_bounds__(kFlat, kGsSeg <= 2 ? 2 : 1) k_gs3r(GSArgs a) {

@@ -163,6 +163,13 @@ __device__ __forceinline__ void node_kappa(const Geo& g, const double* th, int l
     }
 }
 
+// the general edge coefficients (block interfaces, face operators) out of line: keeps the
+// register footprint of the common uniform-block path small
+__device__ __noinline__ void node_kappa3_call(const Geo& g, const double* th, int ldb, int b, int I, int J,
+                                              int K, double* k) {
+    node_kappa<3>(g, th, ldb, b, I, J, K, k);
+}
+
 // 2D edge coefficients from precomputed cell blocks (bx of cells I-1, I; by*px of
 // cells J-1, J): bitwise the same values as node_kappa<2>.
 __device__ __forceinline__ void kappa2_blocks(const double* th, int ldb, int b, int bx0, int bx1,
