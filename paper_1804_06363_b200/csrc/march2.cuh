@@ -894,3 +894,132 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
 }
 
 }  // namespace rbs
+
+namespace rbs {
+// ===========================================================================
+// k_wtr<BP>: the projection W^T v and ||v||^2 as a stream over a contiguous node
+// range per CTA (any dimension; the 3D second half of K2, eq5).
+// Chunks of kWtCH nodes of W (ldw doubles per node) and v (BP per node) arrive by
+// TMA bulk copies into a kWtD-slot ring (mbarriers); warps own (8-basis x 8-query)
+// tiles and split the chunk's k-steps when there are fewer tiles than warps; the
+// k-parts and the per-thread ||v||^2 terms are summed in a fixed order.  Partials
+// go to part[b][j][col] exactly like k_proj (stage 2: k_reduce_solve).
+// ===========================================================================
+constexpr int kWtCH = 64, kWtD = 3;
+
+inline size_t wtr_smem_bytes(int Bp, int ldw) {
+    return (size_t)kWtD * kWtCH * (ldw + Bp) * 8 + 256;
+}
+
+template <int BP>
+__global__ void __launch_bounds__(kMT, 2) k_wtr(ProjArgs a) {
+    if (a.done && ld_flag(a.done)) return;
+    extern __shared__ __align__(128) double smd[];
+    __shared__ __align__(8) uint64_t bars[kWtD];
+    __shared__ double s_red[kNW * 64];
+    __shared__ double s_rr[kMT];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int npad = a.npad, ldw = a.ldw, ntile = npad >> 3;
+    constexpr int NBT = BP / 8;
+    const int T = ntile * NBT;                                // output tiles
+    const int KP = T >= kNW ? 1 : min(kWtCH / 4, kNW / T);   // k-parts per tile (k-steps split)
+    const int64_t N = a.g.N;
+    const int64_t n0 = N * blockIdx.x / gridDim.x, n1 = N * (blockIdx.x + 1) / gridDim.x;
+    const int nch = (int)((n1 - n0 + kWtCH - 1) / kWtCH);
+    const int slotW = kWtCH * ldw, slotV = kWtCH * BP;
+    double* wr = smd;
+    double* vr = smd + kWtD * slotW;
+    if (tid == 0) {
+        for (int k = 0; k < kWtD; ++k) mbar_init(&bars[k], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int c) {             // chunk c -> slot c % kWtD (thread 0)
+        const int64_t i0 = n0 + (int64_t)c * kWtCH;
+        const int cnt = (int)(n1 - i0 < (int64_t)kWtCH ? n1 - i0 : (int64_t)kWtCH);
+        const int sl = c % kWtD;
+        uint64_t* bar = &bars[sl];
+        fence_async_smem();
+        const uint32_t bw = (uint32_t)cnt * ldw * 8, bv = (uint32_t)cnt * BP * 8;
+        mbar_expect_tx(bar, bw + bv);
+        bulk_g2s(wr + sl * slotW, a.W + i0 * ldw, bw, bar);
+        bulk_g2s(vr + sl * slotV, a.V + i0 * BP, bv, bar);
+    };
+    if (tid == 0)
+        for (int c = 0; c < kWtD - 1 && c < nch; ++c) issue(c);
+    // this warp's tiles: t = warp % T' ... with k-part kp
+    const int tslot = warp % (T * KP >= kNW ? kNW : T * KP);
+    const bool wact = warp < T * KP || T >= kNW;
+    const int kp = T >= kNW ? 0 : tslot / T;
+    double acc[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = 0.0;
+    double rr = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        if (tid == 0 && c + kWtD - 1 < nch) issue(c + kWtD - 1);
+        const int sl = c % kWtD;
+        mbar_wait(&bars[sl], (uint32_t)((c / kWtD) & 1));
+        const int64_t i0 = n0 + (int64_t)c * kWtCH;
+        const int cnt = (int)(n1 - i0 < (int64_t)kWtCH ? n1 - i0 : (int64_t)kWtCH);
+        const double* W = wr + sl * slotW;
+        const double* V = vr + sl * slotV;
+        // ||v||^2: element tid of the chunk (fixed node/query per thread)
+        for (int e = tid; e < kWtCH * BP; e += kMT)     // fixed element set per thread
+            if (e / BP < cnt) {
+                const double v = V[e];
+                rr = fma(v, v, rr);
+            }
+        if (wact) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {      // T <= 32 tiles: at most two per warp
+                const int t = T >= kNW ? warp + u * kNW : (u == 0 ? tslot % T : T);
+                if (t >= T) continue;
+                const int jt = t / NBT, bt = t - jt * NBT;
+                for (int ks = kp; ks < kWtCH / 4; ks += KP) {
+                    const int nd = ks * 4 + (lane & 3);           // node of this lane's k
+                    const bool in = nd < cnt;
+                    const double wa = in ? W[nd * ldw + jt * 8 + (lane >> 2)] : 0.0;   // A: basis x node
+                    const double vb = in ? V[nd * BP + bt * 8 + (lane >> 2)] : 0.0;    // B: node x query
+                    dmma_8x8x4(acc[u][0], acc[u][1], wa, vb);
+                }
+            }
+        }
+        __syncthreads();   // slot sl is reissued kWtD - 1 chunks later
+    }
+    // ---- fixed-order combine: k-parts of each tile, then partial columns -----
+    const int rows = npad + 1;
+    if (T >= kNW) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int t = warp + u * kNW;
+            if (t >= T) continue;
+            const int jt = t / NBT, bt = t - jt * NBT;
+            const int j = jt * 8 + (lane >> 2), bb = bt * 8 + 2 * (lane & 3);
+            a.part[((int64_t)bb * rows + j) * a.nct + a.col0 + blockIdx.x] = acc[u][0];
+            a.part[((int64_t)(bb + 1) * rows + j) * a.nct + a.col0 + blockIdx.x] = acc[u][1];
+        }
+    } else {
+        if (wact) {
+            s_red[warp * 64 + 2 * lane] = acc[0][0];
+            s_red[warp * 64 + 2 * lane + 1] = acc[0][1];
+        }
+        __syncthreads();
+        for (int idx = tid; idx < T * 64; idx += kMT) {
+            const int t = idx >> 6, w = idx & 63;
+            double s = 0.0;
+            for (int k = 0; k < KP; ++k) s += s_red[(k * T + t) * 64 + w];
+            const int ln = w >> 1, h = w & 1;
+            const int jt = t / NBT, bt = t - jt * NBT;
+            const int j = jt * 8 + (ln >> 2), bb = bt * 8 + 2 * (ln & 3) + h;
+            a.part[((int64_t)bb * rows + j) * a.nct + a.col0 + blockIdx.x] = s;
+        }
+    }
+    s_rr[tid] = rr;
+    __syncthreads();
+    if (tid < BP) {
+        double v = 0.0;
+        for (int u = tid; u < kMT; u += BP) v += s_rr[u];
+        a.part[((int64_t)tid * rows + npad) * a.nct + a.col0 + blockIdx.x] = v;
+    }
+}
+}  // namespace rbs

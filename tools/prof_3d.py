@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=127)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--faces", action="store_true")
+ap.add_argument("--n", type=int, default=20)
 a = ap.parse_args()
 blocks = (2, 2, 2)
 rng = np.random.default_rng(5)
@@ -25,7 +26,7 @@ if a.faces:
     s = rbs.Solver(3, a.m, faces=cases.faces_from_blocks(3, a.m, blocks))
 else:
     s = rbs.Solver(3, a.m, blocks)
-s.build_greedy(tr, 20)
+s.build_greedy(tr, a.n)
 mus = 0.1 * 100 ** rng.random((16, 8))
 out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False)
 torch.cuda.synchronize()
