@@ -916,7 +916,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         int nl = 1;
         if (mode == MODE_CG && g.dim == 3 && use_active && Bp <= 32 && !(v2off & 8)) {
             // two passes: x, r update in row segments, then W^T r, ||r||^2 on the new r
-            k_xr3r<4><<<nctf, kFlat, fsm, st>>>(a, lgB);
+            if (g.faces) k_xr3r<4, true><<<nctf, kFlat, fsm, st>>>(a, lgB);
+            else k_xr3r<4, false><<<nctf, kFlat, fsm, st>>>(a, lgB);
             ProjArgs b2 = a;
             b2.V = L.R;
             const size_t wsm = wtr_smem_bytes(Bp, ctx->ldw);
@@ -955,7 +956,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             const int64_t nb2 = (int64_t)g.N * Bp / 2;
             k_pnew3<<<(unsigned)std::min<int64_t>((nb2 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(
                 a.Y, a.Pold, a.Pnew, a.beta, a.active, nb2, Bp, a.done);
-            k_sigma3r<4><<<nctf, kFlat, fsm, st>>>(a);
+            if (g.faces) k_sigma3r<4, true><<<nctf, kFlat, fsm, st>>>(a);
+            else k_sigma3r<4, false><<<nctf, kFlat, fsm, st>>>(a);
             nl = 2;
         } else k_cgp<3><<<nctf, kFlat, fsm, st>>>(a);
         pe();

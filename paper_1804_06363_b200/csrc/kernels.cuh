@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
 // in k_proj<MODE_PLAIN> on the updated r.  Per node the same arithmetic as
 // k_proj<MODE_CG, 3>.  Requires Bp <= 32; no mesh slabs (all planes owned).
 // ---------------------------------------------------------------------------
-template <int SEG>
+template <int SEG, bool FACES>
 __global__ void __launch_bounds__(kFlat, 1) k_xr3r(ProjArgs a, int lgB) {
     if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
@@ -369,7 +369,9 @@ __global__ void __launch_bounds__(kFlat, 1) k_xr3r(ProjArgs a, int lgB) {
             if (x > m) break;
             double k[6];
             const int bxl = axis_block(g, x - 1, g.px), bxr = axis_block(g, x, g.px);
-            if (rowu && bxl == bxr) {
+            if (FACES) {
+                node_kappa_faces<3>(g, s_th, Bp, b, x, J, K, k);
+            } else if (rowu && bxl == bxr) {
                 const double c = s_th[(bxr + by0 + bz0) * Bp + b];
 #pragma unroll
                 for (int e = 0; e < 6; ++e) k[e] = c;
@@ -894,7 +896,7 @@ __global__ void __launch_bounds__(256) k_pnew3(const double* __restrict__ Y, con
     }
 }
 
-template <int SEG>
+template <int SEG, bool FACES>
 __global__ void __launch_bounds__(kFlat, 1) k_sigma3r(CGPArgs a) {
     if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
@@ -948,7 +950,9 @@ __global__ void __launch_bounds__(kFlat, 1) k_sigma3r(CGPArgs a) {
                 if (x > m) break;
                 double k[6];
                 const int bxl = axis_block(g, x - 1, g.px), bxr = axis_block(g, x, g.px);
-                if (rowu && bxl == bxr) {
+                if (FACES) {
+                    node_kappa_faces<3>(g, s_th, Bp, b, x, J, K, k);
+                } else if (rowu && bxl == bxr) {
                     const double c = s_th[(bxr + by0 + bz0) * Bp + b];
 #pragma unroll
                     for (int e = 0; e < 6; ++e) k[e] = c;
