@@ -224,9 +224,12 @@ void set_attrs() {
     cudaFuncSetAttribute(k_resid_march<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_resid_march<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(k_cgp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_wtr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_wtr<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_wtr<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_wtr<8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_wtr<16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_wtr<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_wtr<8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_wtr<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_wtr<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     set_attrs_v2<8>();
     set_attrs_v2<16>();
     set_attrs_v2<32>();
@@ -920,11 +923,19 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             else k_xr3r<4, false><<<nctf, kFlat, fsm, st>>>(a, lgB);
             ProjArgs b2 = a;
             b2.V = L.R;
-            const size_t wsm = wtr_smem_bytes(Bp, ctx->ldw);
-            if (!(v2off & 32) && wsm <= (size_t)110 * 1024 && npad <= 64) {   // streamed W^T r, 2 CTAs/SM (small n)
-                if (Bp == 8) k_wtr<8><<<a.nct, kMT, wsm, st>>>(b2);
-                else if (Bp == 16) k_wtr<16><<<a.nct, kMT, wsm, st>>>(b2);
-                else k_wtr<32><<<a.nct, kMT, wsm, st>>>(b2);
+            // streamed W^T r with two CTAs per SM: 64-node chunks, 32 when W rows are long
+            const int ch = wtr_smem_bytes(Bp, ctx->ldw, 64) <= (size_t)110 * 1024 ? 64 : 32;
+            const size_t wsm = wtr_smem_bytes(Bp, ctx->ldw, ch);
+            if (!(v2off & 32) && wsm <= (size_t)110 * 1024 && npad <= 64) {
+                if (ch == 64) {
+                    if (Bp == 8) k_wtr<8, 64><<<a.nct, kMT, wsm, st>>>(b2);
+                    else if (Bp == 16) k_wtr<16, 64><<<a.nct, kMT, wsm, st>>>(b2);
+                    else k_wtr<32, 64><<<a.nct, kMT, wsm, st>>>(b2);
+                } else {
+                    if (Bp == 8) k_wtr<8, 32><<<a.nct, kMT, wsm, st>>>(b2);
+                    else if (Bp == 16) k_wtr<16, 32><<<a.nct, kMT, wsm, st>>>(b2);
+                    else k_wtr<32, 32><<<a.nct, kMT, wsm, st>>>(b2);
+                }
             } else {
                 launch_proj<MODE_PLAIN>(g, a.nct, psm, st, b2);
             }

@@ -905,13 +905,13 @@ namespace rbs {
 // k-parts and the per-thread ||v||^2 terms are summed in a fixed order.  Partials
 // go to part[b][j][col] exactly like k_proj (stage 2: k_reduce_solve).
 // ===========================================================================
-constexpr int kWtCH = 64, kWtD = 3;
+constexpr int kWtD = 3;
 
-inline size_t wtr_smem_bytes(int Bp, int ldw) {
-    return (size_t)kWtD * kWtCH * (ldw + Bp) * 8 + 256;
+inline size_t wtr_smem_bytes(int Bp, int ldw, int ch) {
+    return (size_t)kWtD * ch * (ldw + Bp) * 8 + 256;
 }
 
-template <int BP>
+template <int BP, int kWtCH>
 __global__ void __launch_bounds__(kMT, 2) k_wtr(ProjArgs a) {
     if (a.done && ld_flag(a.done)) return;
     extern __shared__ __align__(128) double smd[];
