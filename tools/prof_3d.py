@@ -28,7 +28,9 @@ else:
     s = rbs.Solver(3, a.m, blocks)
 s.build_greedy(tr, a.n)
 mus = 0.1 * 100 ** rng.random((16, 8))
+torch.cuda.nvtx.range_push("solve")      # ncu --nvtx --nvtx-include "solve/" captures only this
 out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False)
+torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 prof = {k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]] for k, v in out["profile"].items() if v[1]}
 # graph-mode iteration time (the way bench.py runs): a fixed 200-iteration solve
