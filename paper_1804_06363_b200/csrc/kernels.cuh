@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_proj(ProjArgs a) {
 // k_proj<MODE_CG, 3>.  Requires Bp <= 32; no mesh slabs (all planes owned).
 // ---------------------------------------------------------------------------
 template <int SEG, bool FACES>
-__global__ void __launch_bounds__(kFlat, 1) k_xr3r(ProjArgs a, int lgB) {
+__global__ void __launch_bounds__(kFlat, SEG <= 2 ? 2 : 1) k_xr3r(ProjArgs a, int lgB) {
     if (a.done && ld_flag(a.done)) return;
     extern __shared__ double smem[];
     double* s_th = smem;
