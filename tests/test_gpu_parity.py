@@ -523,3 +523,22 @@ def test_gpu_basis_from_samples_matches_oracle(orc, rbs):
     assert np.abs(W - ref["W"]).max() <= 1e-8
     assert np.abs(res["ANq"] - ref["ANq"]).max() <= 1e-8 * np.abs(ref["ANq"]).max()
     assert np.abs(res["fn"] - ref["fn"]).max() <= 1e-8 * np.abs(ref["fn"]).max()
+
+
+@pytest.mark.parametrize("dim,m,blocks,n,B", [
+    (3, 13, (2, 2, 2), 20, 16),   # Bp 16: two rows per warp in the row-segment passes, k_wtr<16>
+    (3, 12, (2, 3, 2), 24, 32),   # Bp 32: one row per warp, k_wtr<32>, ragged segments (12 = 3 x 4)
+    (3, 10, (2, 2, 2), 60, 9),    # npad 64 with Bp 16 -> k_wtr with 32-node chunks
+])
+@pytest.mark.parametrize("method", ["rbcg", "rbi"])
+def test_3d_row_segment_passes(orc, rbs, dim, m, blocks, n, B, method):
+    """The 3D RBCG passes (k_pnew3 + k_sigma3r, k_xr3r + k_wtr, k_gs3r) and the RBI path
+    against the oracle at the batch widths they specialise on."""
+    g, res = oracle_basis(orc, dim, m, blocks, n, max(30, n + 20), 3)
+    s = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    rng = np.random.default_rng(700 + B)
+    mus = 0.1 * 100 ** rng.random((B, g.Q))
+    mi = 20000 if method == "rbcg" else 500000
+    out = s.solve_batch(mus, method=rbs.RBS_RBCG if method == "rbcg" else rbs.RBS_RBI,
+                        max_iter=mi, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, method, max_iter=mi)
