@@ -56,13 +56,15 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-iters", type=int, default=30)
     p.add_argument("--streams", type=int, default=2, help="concurrent batch streams (1 = one batch at a time)")
+    p.add_argument("--method", default="rbcg", choices=["rbcg", "rbi"],
+                   help="RBCG (PAPER.md:260-279, default) or the stand-alone RB iteration (PAPER.md:155-169)")
     return p.parse_args()
 
 
-def workload_desc(c):
+def workload_desc(c, method="rbcg"):
     return (f"{c.name}: {c.dim}D {c.m}^{c.dim} (N={c.N}), {'x'.join(map(str, c.blocks))} blocks, "
             f"mu logU[{c.lo},{c.hi}]^{c.P}, f=1, greedy n={c.n} from {c.n_train} train mu, "
-            f"{c.n_queries} queries/GPU, B={c.B}, RBCG sym-RBGS nu=1, tol 1e-10")
+            f"{c.n_queries} queries/GPU, B={c.B}, {method.upper()} sym-RBGS nu=1, tol 1e-10")
 
 
 def peaks():
@@ -349,9 +351,12 @@ def main():
     sts = [torch.cuda.Stream(device=s.device) for _ in range(S)]
     Xs = [torch.empty((c.B, c.N), dtype=torch.float64, device=s.device) for _ in range(S)]
 
+    mkw = (dict(method=rbs.RBS_RBI, max_iter=500000) if a.method == "rbi" else dict(method=rbs.RBS_RBCG))
+
     def step(t, k, **kw):
         b = k % nb
-        return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xs[t], stream=sts[t], want_a_n=False, **kw)
+        return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xs[t], stream=sts[t], want_a_n=False,
+                                 **{**mkw, **kw})
 
     def run(nsteps, fn, nvtx=None):
         outs = [[] for _ in range(S)]
@@ -411,7 +416,7 @@ def main():
     def step_host(t, k):
         b = k % nb
         return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xh[t], x_location=rbs.RBS_MEM_HOST,
-                                 stream=sts[t], want_a_n=True)
+                                 stream=sts[t], want_a_n=True, **mkw)
 
     run(S, step_host)      # warm-up: host-output workspace and its iteration graph per context
     torch.cuda.synchronize()
@@ -438,7 +443,9 @@ def main():
     alg = {"k_cgp": 24 * Bq * N,                    # y, p_old read; p_new written
            "k_proj": 40 * Bq * N + 8 * N * n,       # p, x, r read; x, r written; W
            "k_gs": 16 * Bq * N + 8 * N * n}         # 2D fused smoother: r read, y written; W
-    if c.dim == 3:   # separate prolongation pass; k_gs is one red-black half-sweep per launch
+    if a.method == "rbi":   # RBI: K3' x_new = S(x_old + W e) (x_old, W read; x written), resid f - A x + W^T (x, W)
+        alg = {"k_gs": 16 * Bq * N + 8 * N * n, "k_proj": 8 * Bq * N + 8 * N * n}
+    elif c.dim == 3:   # separate prolongation pass; k_gs is one red-black half-sweep per launch
         alg["k_prolong"] = 8 * Bq * N + 8 * N * n   # W read, y0 written
         alg["k_gs"] = 16 * Bq * N                   # y read, r and y of one colour
     flops = {"k_proj": 2.0 * N * n * Bq, "k_gs": 2.0 * N * n * Bq}   # W^T r / W e on DMMA
@@ -456,7 +463,7 @@ def main():
     top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
     kt = kernels[top]
     iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bq queries
-    iter_bytes = (80 * Bq + 16 * n) * N     # RBCG minimum per batch-iteration
+    iter_bytes = ((24 * Bq + 16 * n) if a.method == "rbi" else (80 * Bq + 16 * n)) * N   # minimum per batch-iteration
     traffic, traffic_src = ncu_traffic(a.config, top)
     roof = {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": kt["GBps"] / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
@@ -472,11 +479,11 @@ def main():
     l2 = (f"inputs larger than L2 (W {wbytes / 1e6:.0f} MB + 4 x {sbytes / 4e6:.0f} MB state > 126 MB)"
           if wbytes + sbytes > 126e6 else
           f"inputs fit in L2 (W {wbytes / 1e6:.1f} MB + state {sbytes / 1e6:.1f} MB): warm-L2 figure")
-    metric = METRIC.replace("(c2,", f"({c.name},")
+    metric = METRIC.replace("(c2,", f"({c.name},").replace("RBCG", a.method.upper())
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(c), "queries_per_gpu": nq, "B": c.B, "n": c.n,
+            "config": {"workload": workload_desc(c, a.method), "queries_per_gpu": nq, "B": c.B, "n": c.n,
                        "parallelism": f"query-shard x{world}" if world > 1 else "1 GPU",
                        "concurrent_batches": S,
                        "l2": l2,
@@ -484,7 +491,7 @@ def main():
                        "offline_greedy_s": round(offline_s, 2), "snapshot_its": snap[:6]},
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "kernels": kernels}
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.method == "rbcg":
         try:
             nq_cpu = min(os.cpu_count() or 1, 8)
             v, cores, wall, oits = cpu_oracle_run(c, nq_cpu)
