@@ -156,21 +156,23 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
 
 // k_smooth2 dynamic shared memory cap: 227 KB per CTA minus its static part
 constexpr int kSmooth2MaxDyn = 225 * 1024;
-template <int BP, bool R, int TX>
+template <int BP, bool R, int TX, int WR>
 void set_attrs_smooth2() {
     const int mx = kSmooth2MaxDyn;
-    cudaFuncSetAttribute(k_smooth2<BP, 0, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 1, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 2, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth2<BP, 3, R, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 0, R, TX, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 1, R, TX, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 2, R, TX, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_smooth2<BP, 3, R, TX, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 template <int BP>
 void set_attrs_v2() {
     const int mx = 214 * 1024;
-    set_attrs_smooth2<BP, false, 32>();
-    set_attrs_smooth2<BP, true, 32>();
-    set_attrs_smooth2<BP, false, 24>();
-    set_attrs_smooth2<BP, true, 24>();
+    set_attrs_smooth2<BP, false, 32, 3>();
+    set_attrs_smooth2<BP, true, 32, 3>();
+    set_attrs_smooth2<BP, false, 32, 2>();
+    set_attrs_smooth2<BP, true, 32, 2>();
+    set_attrs_smooth2<BP, false, 24, 3>();
+    set_attrs_smooth2<BP, true, 24, 3>();
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_resid2<BP, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -178,23 +180,27 @@ void set_attrs_v2() {
     cudaFuncSetAttribute(k_resid2<BP, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
-template <int BP, bool R, int TX>
+template <int BP, bool R, int TX, int WR>
 void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
     switch (S) {
-        case 0: k_smooth2<BP, 0, R, TX><<<grid, kMT, smem, st>>>(a); break;
-        case 1: k_smooth2<BP, 1, R, TX><<<grid, kMT, smem, st>>>(a); break;
-        case 2: k_smooth2<BP, 2, R, TX><<<grid, kMT, smem, st>>>(a); break;
-        default: k_smooth2<BP, 3, R, TX><<<grid, kMT, smem, st>>>(a); break;
+        case 0: k_smooth2<BP, 0, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
+        case 1: k_smooth2<BP, 1, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
+        case 2: k_smooth2<BP, 2, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
+        default: k_smooth2<BP, 3, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
     }
 }
+// variant: 0 = strip 32 / W ring 3, 1 = strip 32 / W ring 2, 2 = strip 24 / W ring 3
 template <int BP>
-void launch_smooth2(int TX, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
-    if (TX == 32) {
-        if (a.Rhs) launch_smooth2t<BP, true, 32>(S, grid, smem, st, a);
-        else launch_smooth2t<BP, false, 32>(S, grid, smem, st, a);
+void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+    if (var == 0) {
+        if (a.Rhs) launch_smooth2t<BP, true, 32, 3>(S, grid, smem, st, a);
+        else launch_smooth2t<BP, false, 32, 3>(S, grid, smem, st, a);
+    } else if (var == 1) {
+        if (a.Rhs) launch_smooth2t<BP, true, 32, 2>(S, grid, smem, st, a);
+        else launch_smooth2t<BP, false, 32, 2>(S, grid, smem, st, a);
     } else {
-        if (a.Rhs) launch_smooth2t<BP, true, 24>(S, grid, smem, st, a);
-        else launch_smooth2t<BP, false, 24>(S, grid, smem, st, a);
+        if (a.Rhs) launch_smooth2t<BP, true, 24, 3>(S, grid, smem, st, a);
+        else launch_smooth2t<BP, false, 24, 3>(S, grid, smem, st, a);
     }
 }
 template <int BP, int PF>
@@ -988,19 +994,28 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
         pb(RBS_K_GS);
         const size_t kMaxDyn = (size_t)kSmooth2MaxDyn;
-        int TX2 = 32;
-        size_t sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad).total;
+        // strip 32 with the 3-row W ring; else strip 32 with a 2-row ring (prefetch distance
+        // 1; keeps ~all SMs busy at large m, e.g. 2047: 64 strips x 2 segments against 86 x 1
+        // at strip 24); else strip 24
+        int var = 0, TX2 = 32;
+        const bool hr = rhs != nullptr, ax = Xold != nullptr;
+        size_t sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 3).total;
         if (sm2 > kMaxDyn) {
+            var = 1;
+            sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 2).total;
+        }
+        if (sm2 > kMaxDyn || (v2off & 128)) {
+            var = 2;
             TX2 = 24;
-            sm2 = Smooth2Smem(24, a.S, Bp, ctx->ldw, Q, rhs != nullptr, Xold != nullptr, npad).total;
+            sm2 = Smooth2Smem(24, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 3).total;
         }
         if (!(v2off & 1) && Bp <= 32 && a.S <= 3 && sm2 <= kMaxDyn) {
             // v2: lagged one-barrier-per-row pipeline (march2.cuh)
             a.part = march_part(g, TX2, ctx->num_sms);
             const int grid2 = a.part.nsx * a.part.nsy;
-            if (Bp == 8) launch_smooth2<8>(TX2, a.S, grid2, sm2, st, a);
-            else if (Bp == 16) launch_smooth2<16>(TX2, a.S, grid2, sm2, st, a);
-            else launch_smooth2<32>(TX2, a.S, grid2, sm2, st, a);
+            if (Bp == 8) launch_smooth2<8>(var, a.S, grid2, sm2, st, a);
+            else if (Bp == 16) launch_smooth2<16>(var, a.S, grid2, sm2, st, a);
+            else launch_smooth2<32>(var, a.S, grid2, sm2, st, a);
             pe();
             return 1;
         }

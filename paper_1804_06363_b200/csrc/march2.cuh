@@ -106,8 +106,8 @@ __device__ __forceinline__ void fill_rowinfo(const Geo& g, int Jfirst, int nr, i
 constexpr int kS2TX = 32;       // strip width (24 when the rings of 32 do not fit)
 constexpr int kS2YR = 8;         // y ring rows (lags 0 .. 2S+1 <= 7)
 constexpr int kS2RR = 8;         // r ring rows (issued at lag 0, last read at lag 2S+1)
-constexpr int kS2WR = 3;         // W / x_old ring rows (prefetch distance 2)
-constexpr int kS2D = 2;
+// W / x_old ring rows: template parameter WR of k_smooth2 (3: prefetch distance 2;
+// 2: distance 1, when the 3-row ring would push the strip width down to 24)
 constexpr int kS2NTW = 4;                 // tensor warps
 constexpr int kS2NVT = kMT - 32 * kS2NTW; // vector threads (384)
 
@@ -117,14 +117,15 @@ constexpr int kS2NVT = kMT - 32 * kS2NTW; // vector threads (384)
 struct Smooth2Smem {
     int vrow, xo, eo, wo, tho, cho, wrow;
     size_t total;
-    __host__ __device__ Smooth2Smem(int TX, int S, int Bp, int ldw, int Q, bool has_rhs, bool acc, int npad) {
+    __host__ __device__ Smooth2Smem(int TX, int S, int Bp, int ldw, int Q, bool has_rhs, bool acc, int npad,
+                                    int WR = 3) {
         const int TW = TX + 2 * S, tiles = (TW + 7) / 8;
         vrow = TW * Bp;
         wrow = tiles * 8 * ldw;
         xo = (kS2YR + (has_rhs ? kS2RR : 0)) * vrow;
-        eo = xo + (acc ? kS2WR * vrow : 0);
+        eo = xo + (acc ? WR * vrow : 0);
         wo = eo + ((npad * (Bp + 4) + 15) & ~15);
-        tho = wo + kS2WR * wrow;
+        tho = wo + WR * wrow;
         cho = tho + Q * Bp;
         total = (size_t)(cho + Q * Bp) * 8;
     }
@@ -136,8 +137,9 @@ struct Smooth2Smem {
 // half-sweep s (one column of every column pair has the sweep's colour), and
 // all 12 share the output row.  Every shared-memory load of a step is issued
 // before any update of that step.
-template <int BP, int S, bool HAS_RHS, int TX>
+template <int BP, int S, bool HAS_RHS, int TX, int WR>
 __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
+    constexpr int kS2WR = WR, kS2D = WR - 1;
     S2CLK_ENTRY
     if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     const int Jfirst = y0 - S;                               // row of step 0
     const int JlastP = y1 - 1 + S;                           // last prolongated row
     const int nsteps = (y1 - y0) + 3 * S + 1;                // last output row y1-1 at lag 2S+1
-    const Smooth2Smem L(TX, S, BP, ldw, a.g.Q, has_rhs, acc, npad);
+    const Smooth2Smem L(TX, S, BP, ldw, a.g.Q, has_rhs, acc, npad, WR);
     const int XO = L.xo, EO = L.eo, WO = L.wo, THO = L.tho, CHO = L.cho, WROW = L.wrow;
 
     // ---- init: zero the rings (Dirichlet columns/rows stay zero), tables ------
