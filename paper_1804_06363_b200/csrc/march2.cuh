@@ -151,7 +151,11 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     constexpr int GW = S > 0 ? (kS2NVT / 32) / S : 1;        // warps per sweep group
     constexpr int GT = GW * 32;                              // threads per sweep group
     constexpr int PPI = GT >> LGB;                           // pairs per slot round
-    constexpr int JO = (TX * BP + kS2NVT - 1) / kS2NVT;   // output slots per thread
+    // the output row is stored by the vector threads of groups >= OG: with three half-sweeps
+    // group 0 (the widest cone) skips it, so the per-row work of the groups evens out
+    constexpr int OG = S == 3 ? 1 : 0;
+    constexpr int NOT = kS2NVT - OG * GT;                   // output threads
+    constexpr int JO = (TX * BP + NOT - 1) / NOT;           // output slots per thread
     constexpr int YR = 0, RR = kS2YR * VROW;
     extern __shared__ __align__(128) double smd[];
     __shared__ int s_ci[TW], s_cu[TW];
@@ -369,12 +373,13 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
             S2CLK(2);
             // ---- output row Ro = Jb - (2S+1): stores + y^T r, y^T y -----------------
             const int Ro = Jb - (2 * S + 1);
-            if (Ro >= y0 && Ro < y1) {
+            const int ot = vtid - OG * GT;
+            if (ot >= 0 && Ro >= y0 && Ro < y1) {
                 const uint32_t yo = sbase + 8u * (YR + ((t - (2 * S + 1)) & (kS2YR - 1)) * VROW + S * BP);
                 const uint32_t ro = sbase + 8u * (RR + ((t - (2 * S + 1)) & (kS2RR - 1)) * VROW + S * BP);
 #pragma unroll
                 for (int j = 0; j < JO; ++j) {
-                    const int e = vtid + j * kS2NVT;
+                    const int e = ot + j * NOT;
                     if ((e >> LGB) >= nco) break;
                     const double v = ldsd(yo + 8u * e);
                     yg[e] = v;
