@@ -269,7 +269,15 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             a.g = q.g; a.Bp = Bp; a.lgB = lgB; a.NB = q.g.N * Bp; a.theta = L.theta; a.active = L.active;
             a.beta = L.beta; a.Y = q.Y; a.Pold = (it & 1) ? q.P1 : q.P0; a.Pnew = (it & 1) ? q.P0 : q.P1;
             a.s = S; a.done = done; a.col0 = q.colF; a.ext = 1;
-            k_cgp<3><<<q.nctf, kFlat, fsm, st>>>(a);
+            if (Bp <= 32 && !q.g.faces) {     // stream p_new, then sigma in row segments (kernels.cuh)
+                const int64_t nb2 = (int64_t)q.g.N * Bp / 2;
+                k_pnew3<<<(unsigned)std::min<int64_t>((nb2 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0,
+                          st>>>(a.Y, a.Pold, a.Pnew, a.beta, a.active, nb2, Bp, a.done);
+                k_sigma3r<4, false><<<q.nctf, kFlat, fsm, st>>>(a);
+                ++c;
+            } else {
+                k_cgp<3><<<q.nctf, kFlat, fsm, st>>>(a);
+            }
             ++c;
         }
         if (dist) {   // rank sum of the columns, allreduce over the ranks, Step 5
@@ -377,7 +385,11 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             if (cs.empty()) cs.push_back(-1);
             for (size_t t = 0; t < cs.size(); ++t) {
                 a.color = cs[t];
-                if (t + 1 == cs.size()) k_gs<3, true><<<q.nctf, kFlat, fsm, st>>>(a);
+                const bool l = t + 1 == cs.size();
+                if (Bp <= 32 && a.color >= 0 && !q.g.faces) {     // row segments (kernels.cuh)
+                    if (l) k_gs3r<true, 4, false><<<q.nctf, kFlat, fsm, st>>>(a);
+                    else k_gs3r<false, 4, false><<<q.nctf, kFlat, fsm, st>>>(a);
+                } else if (l) k_gs<3, true><<<q.nctf, kFlat, fsm, st>>>(a);
                 else k_gs<3, false><<<q.nctf, kFlat, fsm, st>>>(a);
                 ++c;
             }
