@@ -154,6 +154,7 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
+int g_v2off = 0;   // RBS_DISABLE_V2 bits of the current solve (launch helpers)
 // k_smooth2 dynamic shared memory cap: 227 KB per CTA minus its static part
 constexpr int kSmooth2MaxDyn = 225 * 1024;
 template <int BP, bool R, int TX, int WR>
@@ -167,6 +168,10 @@ void set_attrs_smooth2() {
 template <int BP>
 void set_attrs_v2() {
     const int mx = 214 * 1024;
+    if (BP == 32) {
+        cudaFuncSetAttribute(k_smooth2<32, 3, true, 32, 3, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmooth2MaxDyn);
+        cudaFuncSetAttribute(k_smooth2<32, 3, true, 32, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmooth2MaxDyn);
+    }
     set_attrs_smooth2<BP, false, 32, 3>();
     set_attrs_smooth2<BP, true, 32, 3>();
     set_attrs_smooth2<BP, false, 32, 2>();
@@ -192,6 +197,14 @@ void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const Smooth
 // variant: 0 = strip 32 / W ring 3, 1 = strip 32 / W ring 2, 2 = strip 24 / W ring 3
 template <int BP>
 void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+    if (BP == 32 && S == 3 && a.Rhs && a.npad == 40 && var == 0 && !(g_v2off & 1024)) {
+        k_smooth2<32, 3, true, 32, 3, 10><<<grid, kMT, smem, st>>>(a);     // n = 33..40 (c2)
+        return;
+    }
+    if (BP == 32 && S == 3 && a.Rhs && a.npad == 64 && var == 1 && !(g_v2off & 1024)) {
+        k_smooth2<32, 3, true, 32, 2, 16><<<grid, kMT, smem, st>>>(a);     // n = 57..64 (c3)
+        return;
+    }
     if (var == 0) {
         if (a.Rhs) launch_smooth2t<BP, true, 32, 3>(S, grid, smem, st, a);
         else launch_smooth2t<BP, false, 32, 3>(S, grid, smem, st, a);
@@ -704,6 +717,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     // RBS_DISABLE_V2 (debug / A-B): bit 0 smoother, bit 1 p-update, bit 2 projection v2 kernels
     const char* dv2 = getenv("RBS_DISABLE_V2");
     const int v2off = dv2 ? atoi(dv2) : 0;
+    g_v2off = v2off;
     const bool cg = o->method == RBS_RBCG;
     // 2D, B_pad <= 32: the projection pass is the row march (k_resid_march)
     const bool use_rmarch = g.dim == 2 && Bp <= 32 && !g.faces;   // row marches: block tables

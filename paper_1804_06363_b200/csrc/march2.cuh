@@ -137,8 +137,10 @@ struct Smooth2Smem {
 // half-sweep s (one column of every column pair has the sweep's colour), and
 // all 12 share the output row.  Every shared-memory load of a step is issued
 // before any update of that step.
-template <int BP, int S, bool HAS_RHS, int TX, int WR>
+template <int BP, int S, bool HAS_RHS, int TX, int WR, int NKC = 0>
 __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
+    // NKC > 0: the basis width npad / 4 fixed at compile time, so the k loop of the
+    // prolongation unrolls completely (no loop-carried branch; loads scheduled ahead)
     constexpr int kS2WR = WR, kS2D = WR - 1;
     S2CLK_ENTRY
     if (a.done && ld_flag(a.done)) return;
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     // ---- tensor warps: query tile bt, tiles tile0 + k*TSTEP ----------------------
     constexpr int LGNBT = LGB - 3;
     constexpr int TSTEP = kS2NTW >> LGNBT;
-    const int nk = npad >> 2;
+    const int nk = NKC > 0 ? NKC : npad >> 2;
     const int bt = warp & (NBT - 1), tile0 = warp >> LGNBT;
     constexpr int TPW = (TILES + TSTEP - 1) / TSTEP;                 // tiles per tensor warp
     const int eoff = EO + (lane & 3) * (BP + 4) + bt * 8 + (lane >> 2);   // B fragments (E)
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
                     double d0[TPW], d1[TPW];
 #pragma unroll
                     for (int i = 0; i < TPW; ++i) d0[i] = d1[i] = 0.0;
-#pragma unroll 1
+#pragma unroll (NKC > 0 ? NKC / 2 : 1)
                     for (int kk = 0; kk < nk; kk += 2, ea += 8u * 8 * (BP + 4)) {
                         const double e0 = ldsd(ea), e1 = ldsd(ea + 8u * 4 * (BP + 4));
                         double wa[TPW], wb2[TPW];
