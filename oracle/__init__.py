@@ -183,9 +183,17 @@ class Grid:
                          int(max_iter), _d(x), C.byref(its))
         return dict(x=x, its=its.value, status=STATUS[st])
 
-    def greedy(self, mu_train, n_max, adaptive=True, snapshot_tol=1e-12, drop_tol=1e-10):
+    def greedy(self, mu_train, n_max, adaptive=True, snapshot_tol=1e-12, drop_tol=1e-10, phi_train=None,
+               terms=None):
+        """phi_train (nt, R) + terms (R, N): affine right-hand sides (or_set_greedy_rhs); the
+        result's fnr is then (R, n) = W^T f_r."""
         mu_train = np.ascontiguousarray(mu_train, dtype=np.float64)
         nt = mu_train.shape[0]
+        R = 0 if phi_train is None else int(np.shape(phi_train)[1])
+        phi = np.ascontiguousarray(phi_train, dtype=np.float64) if R else None
+        tm = np.ascontiguousarray(terms, dtype=np.float64) if R else None
+        fnr = np.zeros((max(R, 1), n_max))
+        self._lib().or_set_greedy_rhs(R, _d(phi), _d(tm), _d(fnr) if R else None)
         W = np.zeros((self.N, n_max), order="F")
         ANq = np.zeros((self.Q, n_max, n_max))
         fn = np.zeros(n_max)
@@ -196,9 +204,13 @@ class Grid:
         n = self._lib().or_greedy(self.dim, C.c_int64(self.m), self._cb, nt, _d(mu_train), n_max,
                             int(adaptive), C.c_double(snapshot_tol), C.c_double(drop_tol),
                             _d(W), _d(ANq), _d(fn), _i(sel), _d(ind), _i(its), C.byref(rej))
-        return dict(W=np.asfortranarray(W[:, :n]), ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(),
-                    selected=sel[:n].copy(), indicator=ind[:n].copy(), snap_iters=its[:n].copy(),
-                    n_rejected=rej.value, n=n)
+        self._lib().or_set_greedy_rhs(0, None, None, None)
+        out = dict(W=np.asfortranarray(W[:, :n]), ANq=ANq[:, :n, :n].copy(), fn=fn[:n].copy(),
+                   selected=sel[:n].copy(), indicator=ind[:n].copy(), snap_iters=its[:n].copy(),
+                   n_rejected=rej.value, n=n)
+        if R:
+            out["fnr"] = fnr[:, :n].copy()
+        return out
 
     def basis_from_samples(self, mus, snapshot_tol=1e-12, drop_tol=1e-10):
         mus = np.ascontiguousarray(mus, dtype=np.float64)

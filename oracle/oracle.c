@@ -633,6 +633,39 @@ static int snapshot(int dim, int64_t m, const int* blocks, int n, const double* 
     return st;
 }
 
+/* affine right-hand sides for the greedy (NEXT(4), AMB-23): f(mu_t) = sum_r phi[t][r] f_r;
+ * set by or_set_greedy_rhs before or_greedy / or_basis_from_samples, R = 0 = f = 1 */
+static int g_rhs_R = 0;
+static const double* g_rhs_phi = NULL;    /* [n_train][R] */
+static const double* g_rhs_terms = NULL;  /* [R][N] */
+static double* g_rhs_fnr = NULL;          /* [R][n_max] out: f_{N,r} = W^T f_r */
+
+void or_set_greedy_rhs(int R, const double* phi, const double* terms, double* fnr_out)
+{
+    g_rhs_R = R;
+    g_rhs_phi = phi;
+    g_rhs_terms = terms;
+    g_rhs_fnr = fnr_out;
+}
+
+/* snapshot of RBCG (snapshot()) with an explicit right-hand side b */
+static int snapshot_b(int dim, int64_t m, const int* blocks, int n, const double* W,
+                      const double* ANq_ld, int ldA, const double* fn, const double* mu, const double* b,
+                      double tol, int max_iter, double* x, int* its)
+{
+    int Q = grid_Q(dim, blocks);
+    double* A = (double*)malloc(sizeof(double) * (size_t)(Q * n * n + 1));
+    for (int q = 0; q < Q; ++q)
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                A[(int64_t)q * n * n + i * n + j] = ANq_ld[(int64_t)q * ldA * ldA + i * ldA + j];
+    or_opts o = {tol, max_iter, OR_SMOOTH_SYM_RBGS, 1, 1.0, 1e-12};
+    double trr;
+    int st = or_rbcg(dim, m, blocks, n, W, A, fn, mu, b, &o, x, its, NULL, NULL, &trr);
+    free(A);
+    return st;
+}
+
 static int greedy_core(int dim, int64_t m, const int* blocks, int n_train,
                        const double* mu_train, int n_max, int adaptive,
                        double snapshot_tol, double drop_tol, double* W, double* ANq,
@@ -648,25 +681,35 @@ static int greedy_core(int dim, int64_t m, const int* blocks, int n_train,
     double* L = (double*)malloc(sizeof(double) * (size_t)n_max * n_max + 8);
     double* a = (double*)malloc(sizeof(double) * (size_t)n_max + 8);
     int n = 0, rej = 0, its_first = -1;
+    const int R = g_rhs_R;
+    double* bsnap = R > 0 ? (double*)malloc(sizeof(double) * (size_t)N) : NULL;
+    double* fn_t = R > 0 ? (double*)malloc(sizeof(double) * (size_t)n_max + 8) : NULL;
     /* Step 0/1: mu_1 = Xi_train[0] (AMB-13; Xi_train itself is seeded random) */
     int cand = 0;
     int list_pos = 0;
     while (n < n_max && cand >= 0) {
         const double* mu = mu_train + (int64_t)cand * P;
+        if (R > 0) {   /* f(mu_cand) = sum_r phi_r f_r */
+            for (int64_t i = 0; i < N; ++i) {
+                double v = 0.0;
+                for (int r = 0; r < R; ++r) v += g_rhs_phi[(int64_t)cand * R + r] * g_rhs_terms[(int64_t)r * N + i];
+                bsnap[i] = v;
+            }
+        }
         /* Step 3: solve the snapshot (adaptive: RBCG with W_{N-1}) */
         int its = 0, st;
         if (!adaptive || n == 0) {
             /* N = 1 (or plain greedy): the "standard solver" of PAPER.md:291 = SGS-PCG */
-            st = snapshot(dim, m, blocks, 0, W, ANq, n_max, fn, mu, snapshot_tol, 200000, x, &its);
+            st = snapshot_b(dim, m, blocks, 0, W, ANq, n_max, fn, mu, bsnap, snapshot_tol, 200000, x, &its);
             if (n == 0 && its_first < 0) its_first = its;
         } else {
             /* RBCG with W_{N-1}, guarded (AMB-22): if it has not
              * converged within 2*its_1 + 50 iterations (its_1 = the N = 1 snapshot),
              * fall back to the standard solver. */
-            st = snapshot(dim, m, blocks, n, W, ANq, n_max, fn, mu, snapshot_tol,
-                          2 * (its_first > 0 ? its_first : 1000) + 50, x, &its);
+            st = snapshot_b(dim, m, blocks, n, W, ANq, n_max, fn, mu, bsnap, snapshot_tol,
+                            2 * (its_first > 0 ? its_first : 1000) + 50, x, &its);
             if (st != OR_CONVERGED) {
-                st = snapshot(dim, m, blocks, 0, W, ANq, n_max, fn, mu, snapshot_tol, 200000, x, &its);
+                st = snapshot_b(dim, m, blocks, 0, W, ANq, n_max, fn, mu, bsnap, snapshot_tol, 200000, x, &its);
                 its = -its;   /* reported negative: fallback used */
             }
         }
@@ -680,6 +723,8 @@ static int greedy_core(int dim, int64_t m, const int* blocks, int n_train,
             selected[n] = cand;
             if (snap_iters) snap_iters[n] = its;
             offline_column(dim, m, blocks, n, W, ANq, n_max, fn);
+            for (int r = 0; r < R; ++r)   /* f_{N,r}[n] = w_n^T f_r */
+                g_rhs_fnr[(int64_t)r * n_max + n] = or_dot(N, W + (int64_t)n * N, g_rhs_terms + (int64_t)r * N);
             ++n;
         }
         if (from_list) {
@@ -697,7 +742,16 @@ static int greedy_core(int dim, int64_t m, const int* blocks, int n_train,
         for (int t = 0; t < n_train; ++t) {
             online_assemble(n, Q, ANq, n_max, mu_train + (int64_t)t * P, AN);
             if (or_cholesky(n, AN, L) >= 0) { ind[t] = -INFINITY; continue; }
-            or_chol_solve(n, L, fn, a);
+            if (R > 0) {   /* f_N(mu_t) = sum_r phi_r(mu_t) f_{N,r} */
+                for (int j = 0; j < n; ++j) {
+                    double v = 0.0;
+                    for (int r = 0; r < R; ++r) v += g_rhs_phi[(int64_t)t * R + r] * g_rhs_fnr[(int64_t)r * n_max + j];
+                    fn_t[j] = v;
+                }
+                or_chol_solve(n, L, fn_t, a);
+            } else {
+                or_chol_solve(n, L, fn, a);
+            }
             double sabs = 0.0;
             for (int j = 0; j < n; ++j) sabs += fabs(a[j]);
             ind[t] = sabs;
@@ -710,7 +764,7 @@ static int greedy_core(int dim, int64_t m, const int* blocks, int n_train,
         if (indicator) indicator[n - 1] = best;
     }
     if (n_rejected) *n_rejected = rej;
-    free(x); free(excluded); free(ind); free(AN); free(L); free(a);
+    free(x); free(excluded); free(ind); free(AN); free(L); free(a); free(bsnap); free(fn_t);
     return n;
 }
 

@@ -108,6 +108,12 @@ int or_greedy(int dim, int64_t m, const int* blocks, int n_train, const double* 
               double* W_out, double* ANq_out, double* fn_out, int* selected,
               double* indicator, int* snap_iters, int* n_rejected);
 
+/* Affine right-hand sides for the next or_greedy / or_basis_from_samples (NEXT(4)):
+ * snapshots solve with f(mu_t) = sum_r phi[t*R + r] terms[r*N + i]; the offline
+ * vectors f_{N,r} = W^T f_r go to fnr_out [R][n_max]; the indicator solves use
+ * f_N(mu_t) = sum_r phi_r f_{N,r}.  R = 0 restores f = 1.  Pointers are kept. */
+void or_set_greedy_rhs(int R, const double* phi, const double* terms, double* fnr_out);
+
 /* Build a basis from a given sample list (the fine-grid half of the
  * multi-fidelity approach): RBCG snapshots with the growing
  * basis, MGS, incremental offline blocks.  returns n_out. */

@@ -108,3 +108,16 @@ def test_case2_rhs_terms_are_the_bilinear_expansion(orc):
     direct = cases.source(3, m) + cases.lifting(3, m, Fb, g)[0]
     assert np.abs(rhs - direct).max() <= 1e-12 * np.abs(direct).max()
     assert np.allclose(P["phi"](np.array([1.0, 0.5])), [1, 0.5, 0.5, 0.5, 0.5])
+
+
+def test_affine_rhs_greedy_reduces_to_the_constant_rhs(orc):
+    """or_set_greedy_rhs with one term f_1 = 1, phi = 1 is the f = 1 greedy (same snapshots,
+    selections, basis); its f_{N,1} equals the offline fn = W^T 1."""
+    g = orc.Grid(2, 15, (2, 2))
+    rng = np.random.default_rng(4)
+    tr = 0.1 * 100 ** rng.random((12, g.Q))
+    a = g.greedy(tr, 4)
+    b = g.greedy(tr, 4, phi_train=np.ones((12, 1)), terms=np.ones((1, g.N)))
+    assert np.array_equal(a["selected"], b["selected"])
+    assert np.abs(a["W"] - b["W"]).max() <= 1e-13
+    assert np.abs(b["fnr"][0] - a["fn"]).max() <= 1e-12 * np.abs(a["fn"]).max()
