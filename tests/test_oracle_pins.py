@@ -462,3 +462,110 @@ def test_adaptive_n_grows_by_the_rule_and_converges(orc, small2d):
     A = refs.cellwise_fd(2, g.m, g.blocks, mu).toarray()
     xs = np.linalg.solve(A, np.ones(g.N))
     assert np.linalg.norm(out["x"] - xs) <= 1e-8 * np.linalg.norm(xs)
+
+
+# --------------------------------------------------------------------------- greedy Steps 5-6 (recomputed)
+def _recompute_selection(dim, m, blocks, tr, W, selected, n_out, rhs=None):
+    """Steps 5-6 of algorithm0/algorithm3 recomputed from
+    their definition with independent pieces: for N = 1..n-1, A_N(mu_t) = W_N^T A(mu_t)
+    W_N with A from the cell-wise assembly (refs.cellwise_fd), f_N = W_N^T f(mu_t),
+    a_N(mu_t) by numpy.linalg.solve, indicator = sum_j |a_N,j| (the L1 norm of
+    PAPER.md:87); mu_{N+1} = argmax over the parameters not selected yet, lowest index
+    on ties (AMB-13).  Returns, per step, (expected index, top-2 gap, max indicator)."""
+    out = []
+    As = [refs.cellwise_fd(dim, m, blocks, mu).tocsr() for mu in tr]
+    for N in range(1, n_out):
+        WN = W[:, :N]
+        ind = np.empty(len(tr))
+        for t, A in enumerate(As):
+            f = np.ones(W.shape[0]) if rhs is None else rhs(t)
+            ind[t] = np.abs(np.linalg.solve(WN.T @ (A @ WN), WN.T @ f)).sum()
+        ind[list(selected[:N])] = -np.inf
+        best = int(np.argmax(ind))          # numpy: first (lowest) index of the maximum
+        srt = np.sort(ind)[::-1]
+        out.append((best, (srt[0] - srt[1]) / srt[0], srt[0]))
+    return out
+
+
+@pytest.mark.parametrize("dim,m,blocks,nt,nmax", [(2, 15, (2, 2), 40, 7), (2, 11, (3, 3), 30, 6),
+                                                  (3, 5, (2, 2, 2), 24, 5)])
+def test_greedy_selection_rule_recomputed(orc, dim, m, blocks, nt, nmax):
+    """or_greedy Steps 5-6 against the paper's definition recomputed in numpy: a wrong
+    norm (L2 / max instead of L1), selected parameters not excluded, or ties broken
+    high all change the selected sequence."""
+    g = orc.Grid(dim, m, blocks)
+    tr = 0.1 * 100 ** np.random.default_rng(100 + m).random((nt, g.Q))
+    res = g.greedy(tr, nmax)
+    assert res["n"] == nmax and res["n_rejected"] == 0 and res["selected"][0] == 0
+    for N, (best, gap, top) in enumerate(_recompute_selection(dim, m, blocks, tr, res["W"],
+                                                              res["selected"], res["n"]), start=1):
+        if gap > 1e-10:
+            assert res["selected"][N] == best, (N, res["selected"], best)
+        else:   # a genuine near-tie: either candidate is the argmax to rounding
+            assert res["selected"][N] not in res["selected"][:N]
+        assert abs(res["indicator"][N - 1] - top) <= 1e-10 * top
+
+
+def test_greedy_tie_goes_to_lowest_index(orc):
+    """Exact ties (a training parameter listed twice gives bitwise-equal indicators):
+    AMB-13 takes the lowest index.  Put a copy of the parameter the greedy picks second
+    BEFORE it in the list: the copy (lower index) must be picked instead, and the
+    later duplicate is then dependent (same snapshot) -- rejected if ever chosen."""
+    g = orc.Grid(2, 13, (2, 2))
+    tr = 0.1 * 100 ** np.random.default_rng(31).random((20, 4))
+    r0 = g.greedy(tr, 3)
+    s1 = int(r0["selected"][1])
+    assert s1 >= 1
+    tr2 = np.vstack([tr[:1], tr[s1:s1 + 1], tr[1:]])      # copy at index 1; the original moves to s1+1
+    r1 = g.greedy(tr2, 3)
+    assert r1["selected"][1] == 1, r1["selected"]
+    assert np.array_equal(r1["W"][:, :2], r0["W"][:, :2])
+    assert (s1 + 1) not in list(r1["selected"])
+
+
+def test_greedy_linear_rhs_family(orc):
+    """Fixed operator, f(phi) = sum_r phi_r f_r with R = 3 (affine right-hand side,
+    PAPER.md:98-103): every snapshot is A^{-1} sum_r phi_r f_r, so the solution manifold
+    is 3-dimensional -- the greedy stops at n = 3 with the rest rejected -- and
+    a_N(phi) = A_N^{-1} sum_r phi_r f_{N,r} is linear in phi, so Step 6's argmax is the
+    largest |.|_1 of a linear map over the listed phi (recomputed in numpy)."""
+    m = 12
+    g = orc.Grid(2, m, (2, 2))
+    rng = np.random.default_rng(17)
+    theta = np.array([1.0, 3.0, 0.5, 2.0])
+    nt, R = 15, 3
+    tr = np.tile(theta, (nt, 1))
+    phi = rng.standard_normal((nt, R))
+    terms = rng.standard_normal((R, g.N))
+    res = g.greedy(tr, 6, phi_train=phi, terms=terms)
+    assert res["n"] == R and res["n_rejected"] == nt - R
+    A = refs.cellwise_fd(2, m, (2, 2), theta).tocsc()
+    X = spla.spsolve(A, terms.T)                              # A^{-1} f_r, columns
+    s = np.linalg.svd(res["W"].T @ np.linalg.qr(X)[0], compute_uv=False)
+    assert s.min() > 1 - 1e-10                                # span W = span A^{-1} f_r
+    assert np.abs(res["fnr"] - terms @ res["W"]).max() <= 1e-12 * np.abs(terms).max() * np.sqrt(g.N)
+    for N, (best, gap, top) in enumerate(_recompute_selection(2, m, (2, 2), tr, res["W"], res["selected"],
+                                                              res["n"], rhs=lambda t: phi[t] @ terms), start=1):
+        assert gap > 1e-10 and res["selected"][N] == best
+        assert abs(res["indicator"][N - 1] - top) <= 1e-10 * top
+
+
+# --------------------------------------------------------------------------- plain CG (context solver)
+@pytest.mark.parametrize("dim,m,blocks", [(2, 20, (3, 3)), (3, 7, (2, 2, 2))])
+def test_cg_matches_scipy(orc, dim, m, blocks):
+    """or_cg is textbook CG (the context baseline of PAPER.md:31, 417): the same
+    iteration count as scipy.sparse.linalg.cg on the independently assembled matrix
+    (+-1) and the same solution."""
+    g = orc.Grid(dim, m, blocks)
+    mu = rand_mu(g.Q, rng=np.random.default_rng(23))
+    A = refs.cellwise_fd(dim, m, blocks, mu).tocsr()
+    b = np.random.default_rng(24).standard_normal(g.N)
+    count = [0]
+    xs, info = spla.cg(A, b, rtol=1e-10, atol=0.0, maxiter=5000,
+                       callback=lambda xk: count.__setitem__(0, count[0] + 1))
+    assert info == 0
+    out = g.cg(mu, b=b, tol=1e-10)
+    assert out["status"] == "CONVERGED" and abs(out["its"] - count[0]) <= 1
+    xd = spla.spsolve(A.tocsc(), b)
+    assert np.linalg.norm(out["x"] - xd) <= 1e-8 * np.linalg.norm(xd)
+    assert np.linalg.norm(b - A @ out["x"]) <= 1e-10 * np.linalg.norm(b)
