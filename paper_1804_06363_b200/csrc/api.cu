@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -25,6 +26,7 @@ using namespace rbs;
 struct rbs_ctx {
     int device = 0;
     int num_sms = 148;
+    int v2off = 0;   // RBS_DISABLE_V2 debug bits (read once at rbs_create)
     std::string err;
     // operator
     bool has_op = false;
@@ -108,7 +110,7 @@ inline int flat_ctas(const Geo& g) {
 }
 // strip partition of the 2D row-marching passes (march.cuh): ~one CTA per SM
 inline int march_tx(int Bp) { return Bp <= 32 ? 32 : 16; }
-inline MarchPart march_part(const Geo& g, int TX, int sms = 148) {
+inline MarchPart march_part(const Geo& g, int TX, int sms) {
     MarchPart p;
     p.nsx = (g.m + TX - 1) / TX;
     int nsy = std::max(1, sms / p.nsx);
@@ -117,9 +119,9 @@ inline MarchPart march_part(const Geo& g, int TX, int sms = 148) {
     return p;
 }
 // columns of the per-CTA partial buffers of the flat / march passes
-inline int part_ctas(const Geo& g) {
-    const MarchPart a = march_part(g, 32), b = march_part(g, 16), c = march_part(g, 24);
-    const MarchPart d = march_part(g, 32, 2 * 148);    // k_cgp2: 2 CTAs per SM
+inline int part_ctas(const Geo& g, int sms) {
+    const MarchPart a = march_part(g, 32, sms), b = march_part(g, 16, sms), c = march_part(g, 24, sms);
+    const MarchPart d = march_part(g, 32, 2 * sms);    // k_cgp2: 2 CTAs per SM
     return std::max(std::max(flat_ctas(g), c.nsx * c.nsy),
                     std::max(std::max(a.nsx * a.nsy, b.nsx * b.nsy), d.nsx * d.nsy));
 }
@@ -154,7 +156,6 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
-int g_v2off = 0;   // RBS_DISABLE_V2 bits of the current solve (launch helpers)
 // k_smooth2 dynamic shared memory cap: 227 KB per CTA minus its static part
 constexpr int kSmooth2MaxDyn = 225 * 1024;
 template <int BP, bool R, int TX, int WR>
@@ -196,12 +197,12 @@ void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const Smooth
 }
 // variant: 0 = strip 32 / W ring 3, 1 = strip 32 / W ring 2, 2 = strip 24 / W ring 3
 template <int BP>
-void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
-    if (BP == 32 && S == 3 && a.Rhs && a.npad == 40 && var == 0 && !(g_v2off & 1024)) {
+void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a, int v2off) {
+    if (BP == 32 && S == 3 && a.Rhs && a.npad == 40 && var == 0 && !(v2off & 1024)) {
         k_smooth2<32, 3, true, 32, 3, 10><<<grid, kMT, smem, st>>>(a);     // n = 33..40 (c2)
         return;
     }
-    if (BP == 32 && S == 3 && a.Rhs && a.npad == 64 && var == 1 && !(g_v2off & 1024)) {
+    if (BP == 32 && S == 3 && a.Rhs && a.npad == 64 && var == 1 && !(v2off & 1024)) {
         k_smooth2<32, 3, true, 32, 2, 16><<<grid, kMT, smem, st>>>(a);     // n = 57..64 (c3)
         return;
     }
@@ -222,9 +223,12 @@ void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMa
     else k_resid2<BP, 1, PF><<<grid, kMT, smem, st>>>(r);
 }
 
-bool g_attr_done = false;
-void set_attrs() {
-    if (g_attr_done) return;
+// cudaFuncSetAttribute applies to the current device only: once per device
+std::mutex g_attr_mu;
+bool g_attr_done[64] = {false};
+void set_attrs(int dev) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (dev < 0 || dev >= 64 || g_attr_done[dev]) return;
     const int big = 200 * 1024;
     cudaFuncSetAttribute(k_proj<MODE_CG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_proj<MODE_CG, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -252,7 +256,7 @@ void set_attrs() {
     set_attrs_v2<8>();
     set_attrs_v2<16>();
     set_attrs_v2<32>();
-    g_attr_done = true;
+    g_attr_done[dev] = true;
 }
 
 // storage of a basis of dimension n
@@ -284,7 +288,7 @@ struct SolveLayout {
 SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool rhs, void* base) {
     const int Bp = pow2_batch(B), npad = c->npad;
     const size_t vec = (size_t)c->N8 * Bp;
-    const int nct = proj_ctas(c->g), nctf = part_ctas(c->g);
+    const int nct = proj_ctas(c->g), nctf = part_ctas(c->g, c->num_sms);
     Carve cv(base);
     SolveLayout L{};
     const bool cg = o->method == RBS_RBCG;
@@ -304,7 +308,7 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.Ainv = cv.take<double>((size_t)Bp * npad * npad + 8);
     L.E = cv.take<double>((size_t)std::max(npad, 8) * Bp);
     L.a_n = cv.take<double>((size_t)Bp * npad + 8);
-    const MarchPart rp = march_part(c->g, kRmTX);
+    const MarchPart rp = march_part(c->g, kRmTX, c->num_sms);
     L.partP = cv.take<double>((size_t)Bp * (npad + 1) * std::max(nct, rp.nsx * rp.nsy));
     L.partF = cv.take<double>((size_t)Bp * 2 * nctf);
     L.alpha = cv.take<double>(Bp);
@@ -409,7 +413,9 @@ rbs_status rbs_create(int cuda_device, rbs_ctx** out) {
         delete ctx;
         return RBS_E_CUDA;
     }
-    set_attrs();
+    set_attrs(cuda_device);
+    const char* dv2 = getenv("RBS_DISABLE_V2");   // debug / A-B bits, read once per context
+    ctx->v2off = dv2 ? atoi(dv2) : 0;
     *out = ctx;
     return RBS_OK;
 }
@@ -714,15 +720,13 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     cudaStream_t st = (cudaStream_t)stream;
     const Geo& g = ctx->g;
     const int Bp = pow2_batch(B), lgB = ilog2(Bp), n = ctx->n, npad = ctx->npad, Q = g.Q;
-    // RBS_DISABLE_V2 (debug / A-B): bit 0 smoother, bit 1 p-update, bit 2 projection v2 kernels
-    const char* dv2 = getenv("RBS_DISABLE_V2");
-    const int v2off = dv2 ? atoi(dv2) : 0;
-    g_v2off = v2off;
+    // RBS_DISABLE_V2 (debug / A-B, read at rbs_create): bit 0 smoother, bit 1 p-update, bit 2 projection
+    const int v2off = ctx->v2off;
     const bool cg = o->method == RBS_RBCG;
     // 2D, B_pad <= 32: the projection pass is the row march (k_resid_march)
     const bool use_rmarch = g.dim == 2 && Bp <= 32 && !g.faces;   // row marches: block tables
     const MarchPart rpart = march_part(g, kRmTX, ctx->num_sms);
-    const int nct = use_rmarch ? rpart.nsx * rpart.nsy : proj_ctas(g), nctf = part_ctas(g);
+    const int nct = use_rmarch ? rpart.nsx * rpart.nsy : proj_ctas(g), nctf = part_ctas(g, ctx->num_sms);
     const int nct_plain = proj_ctas(g);
     const int64_t vecN = ctx->N8 * Bp;
     const size_t psm = proj_smem(g, Bp, npad), fsm = flat_smem(g, Bp);
@@ -1027,9 +1031,9 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             // v2: lagged one-barrier-per-row pipeline (march2.cuh)
             a.part = march_part(g, TX2, ctx->num_sms);
             const int grid2 = a.part.nsx * a.part.nsy;
-            if (Bp == 8) launch_smooth2<8>(var, a.S, grid2, sm2, st, a);
-            else if (Bp == 16) launch_smooth2<16>(var, a.S, grid2, sm2, st, a);
-            else launch_smooth2<32>(var, a.S, grid2, sm2, st, a);
+            if (Bp == 8) launch_smooth2<8>(var, a.S, grid2, sm2, st, a, v2off);
+            else if (Bp == 16) launch_smooth2<16>(var, a.S, grid2, sm2, st, a, v2off);
+            else launch_smooth2<32>(var, a.S, grid2, sm2, st, a, v2off);
             pe();
             return 1;
         }
@@ -1099,10 +1103,14 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
     const int chunk = o->graph_chunk;
     char keybuf[512];
-    snprintf(keybuf, sizeof keybuf, "%p|%p|%d|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%d|%.17g|%d|%.17g|%.17g",
+    // the key names every carved pointer the graph holds (the layout moves with
+    // x_location / rhs / history), so a reused workspace never replays stale pointers
+    snprintf(keybuf, sizeof keybuf, "%p|%p|%d|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%d|%.17g|%d|%.17g|%.17g"
+             "|%d|%p|%p|%p|%p|%p",
              workspace_dev, (void*)Fv, B, Bp, o->method, o->smoother, o->sweeps, o->max_iter, chunk,
              o->tol, o->delta, o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist,
-             rhs_dev ? 1 : 0, n, npad, ctx->fconst, o->n_active, o->gamma, o->omega);
+             rhs_dev ? 1 : 0, n, npad, ctx->fconst, o->n_active, o->gamma, o->omega,
+             o->x_location, (void*)L.theta, (void*)L.partP, (void*)L.partF, (void*)L.ints, (void*)L.X);
     const std::string key(keybuf);
     if (prof) {
         // eager launches, one iteration at a time, events on the launching stream

@@ -215,6 +215,16 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     const int64_t plane = (int64_t)g.m * g.m;
     SolveLayout& L = P.L;
     int64_t launches = 0;
+    // NCCL calls are enqueued inside lambdas (and inside graph capture): the first
+    // failure is kept here and turned into RBS_E_CUDA (with ncclGetErrorString)
+    ncclResult_t nres = ncclSuccess;
+    std::string nwhere;
+    auto nck = [&](ncclResult_t r, const char* what) {
+        if (r != ncclSuccess && nres == ncclSuccess) { nres = r; nwhere = what; }
+    };
+    auto nfail = [&]() {
+        return fail(ctx, RBS_E_CUDA, nwhere + ": " + ncclGetErrorString(nres));
+    };
 
     std::vector<double> th((size_t)Q * Bp, 1.0);
     for (int b = 0; b < B; ++b)
@@ -285,7 +295,8 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             S1.partF = P.colF;
             S1.nctf = 1;
             k_reduce_rows<<<Bp, 128, 0, st>>>(L.partF, 2, P.totF, P.colF);
-            ncclAllReduce(P.colF, P.colF, (size_t)Bp * 2, ncclDouble, ncclSum, ctx->comm, st);
+            nck(ncclAllReduce(P.colF, P.colF, (size_t)Bp * 2, ncclDouble, ncclSum, ctx->comm, st),
+                "ncclAllReduce(sigma)");
             k_slab_alpha<<<1, 512, 0, st>>>(S1, 1);
             return c + 2;
         }
@@ -308,7 +319,8 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             S1.partP = P.colP;
             S1.nct = 1;
             k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, P.totP, P.colP);
-            ncclAllReduce(P.colP, P.colP, (size_t)Bp * (npad + 1), ncclDouble, ncclSum, ctx->comm, st);
+            nck(ncclAllReduce(P.colP, P.colP, (size_t)Bp * (npad + 1), ncclDouble, ncclSum, ctx->comm, st),
+                "ncclAllReduce(W^T r, ||r||^2)");
             k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S1);
             return c + 2;
         }
@@ -322,18 +334,22 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             Slab& q = P.sl[0];
             double* v = which == 0 ? q.R : which == 1 ? q.Y : q.X;
             const size_t pe = (size_t)plane * Bp;          // doubles per plane
-            ncclGroupStart();
+            nck(ncclGroupStart(), "ncclGroupStart");
             if (ctx->rank > 0) {
                 const int d = std::min(depth, q.z0 - q.g0);
-                ncclSend(v + (size_t)(q.z0 - q.g0) * pe, d * pe, ncclDouble, ctx->rank - 1, ctx->comm, st);
-                ncclRecv(v + (size_t)(q.z0 - d - q.g0) * pe, d * pe, ncclDouble, ctx->rank - 1, ctx->comm, st);
+                nck(ncclSend(v + (size_t)(q.z0 - q.g0) * pe, d * pe, ncclDouble, ctx->rank - 1, ctx->comm, st),
+                    "ncclSend(halo, lower)");
+                nck(ncclRecv(v + (size_t)(q.z0 - d - q.g0) * pe, d * pe, ncclDouble, ctx->rank - 1, ctx->comm, st),
+                    "ncclRecv(halo, lower)");
             }
             if (ctx->rank + 1 < ctx->nranks) {
                 const int d = std::min(depth, q.g1 - q.z1);
-                ncclSend(v + (size_t)(q.z1 - d - q.g0) * pe, d * pe, ncclDouble, ctx->rank + 1, ctx->comm, st);
-                ncclRecv(v + (size_t)(q.z1 - q.g0) * pe, d * pe, ncclDouble, ctx->rank + 1, ctx->comm, st);
+                nck(ncclSend(v + (size_t)(q.z1 - d - q.g0) * pe, d * pe, ncclDouble, ctx->rank + 1, ctx->comm, st),
+                    "ncclSend(halo, upper)");
+                nck(ncclRecv(v + (size_t)(q.z1 - q.g0) * pe, d * pe, ncclDouble, ctx->rank + 1, ctx->comm, st),
+                    "ncclRecv(halo, upper)");
             }
-            ncclGroupEnd();
+            nck(ncclGroupEnd(), "ncclGroupEnd");
             return 0;
         }
         for (int s = 0; s < G; ++s) {
@@ -399,7 +415,8 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             S1.partF = P.colF;
             S1.nctf = 1;
             k_reduce_rows<<<Bp, 128, 0, st>>>(L.partF, 2, P.totF, P.colF);
-            ncclAllReduce(P.colF, P.colF, (size_t)Bp * 2, ncclDouble, ncclSum, ctx->comm, st);
+            nck(ncclAllReduce(P.colF, P.colF, (size_t)Bp * 2, ncclDouble, ncclSum, ctx->comm, st),
+                "ncclAllReduce(y^T r, y^T y)");
             k_slab_beta<<<1, 512, 0, st>>>(S1, 1, init);
             return c + 2;
         }
@@ -411,6 +428,7 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     launches += k3(1);
     halo(1, 1);
     CKL();
+    if (nres != ncclSuccess) return nfail();
     int per_iter = 0;
     auto body = [&](int it) {
         int c = k1(it);
@@ -422,10 +440,11 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     };
     const int chunk = o->graph_chunk;
     char keybuf[512];
-    snprintf(keybuf, sizeof keybuf, "slab|%d|%d|%p|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%.17g|%d|%.17g",
+    snprintf(keybuf, sizeof keybuf, "slab|%d|%d|%p|%d|%d|%d|%d|%d|%d|%.17g|%.17g|%d|%p|%p|%p|%d|%d|%.17g|%d|%.17g"
+             "|%d|%p|%p|%p|%p",
              G, (int)dist, workspace_dev, B, Bp, o->smoother, o->sweeps, o->max_iter, chunk, o->tol, o->delta,
              o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist, n, npad, ctx->fconst, o->n_active,
-             o->gamma);
+             o->gamma, o->x_location, (void*)L.theta, (void*)L.partP, (void*)L.ints, (void*)P.colP);
     const std::string key(keybuf);
     if (!ctx->gexec || ctx->gkey != key) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
@@ -437,7 +456,13 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
         st = cap;
         for (int it = 0; it < chunk; ++it) per_iter += body(it);
         st = keep;
-        CK(cudaStreamEndCapture(cap, &graph));
+        const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+        if (nres != ncclSuccess || ce != cudaSuccess) {   // end the capture cleanly before returning
+            if (ce == cudaSuccess) cudaGraphDestroy(graph);
+            cudaStreamDestroy(cap);
+            if (nres != ncclSuccess) return nfail();
+            return fail(ctx, RBS_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+        }
         CK(cudaGraphInstantiate(&ctx->gexec, graph, 0));
         cudaGraphDestroy(graph);
         cudaStreamDestroy(cap);
@@ -484,8 +509,11 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
     }
     k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, P.totP, L.fproj);
     ++launches;
-    if (dist) ncclAllReduce(L.fproj, L.fproj, (size_t)Bp * (npad + 1), ncclDouble, ncclSum, ctx->comm, st);
+    if (dist)
+        nck(ncclAllReduce(L.fproj, L.fproj, (size_t)Bp * (npad + 1), ncclDouble, ncclSum, ctx->comm, st),
+            "ncclAllReduce(true residual)");
     CKL();
+    if (nres != ncclSuccess) return nfail();
     {
         std::vector<double> rows((size_t)Bp * (npad + 1));
         CK(cudaMemcpyAsync(rows.data(), L.fproj, rows.size() * 8, cudaMemcpyDeviceToHost, st));
