@@ -127,7 +127,9 @@ inline MarchPart march_part3(const Geo& g, int S, int sms) {
     int64_t bcost = -1;
     const int nsx = (g.m + TX - 1) / TX;
     for (int nsy = 1; nsy <= std::max(1, g.m / 8); ++nsy) {
-        const int rows = (g.m + nsy - 1) / nsy;
+        // even segments: every segment origin has the parity of row 1 (k_smooth3's
+        // compile-time colour pattern)
+        const int rows = ((g.m + nsy - 1) / nsy + 1) & ~1;
         const int ny = (g.m + rows - 1) / rows;
         const int64_t waves = ((int64_t)nsx * ny + sms - 1) / sms;
         const int64_t cost = waves * (rows + 3 * S + 1);
@@ -145,7 +147,7 @@ inline int part_ctas(const Geo& g, int sms) {
     const MarchPart a = march_part(g, 32, sms), b = march_part(g, 16, sms), c = march_part(g, 24, sms);
     const MarchPart d = march_part(g, 32, 2 * sms);    // k_cgp2: 2 CTAs per SM
     int v3 = 0;
-    for (int S = 1; S <= 3; ++S) {
+    for (int S = 2; S <= 3; ++S) {
         const MarchPart e = march_part3(g, S, sms);
         v3 = std::max(v3, e.nsx * e.nsy);
     }
@@ -282,6 +284,8 @@ void set_attrs_s3all() {
     set_attrs_s3<S, false, true>();
     set_attrs_s3<S, true, true>();
 }
+// k_smooth3 covers alternating colour sequences starting red (every symmetric / forward
+// red-black sweep: color_seq drops repeats) of 2 or 3 half-sweeps
 template <int BP, int PF>
 void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r) {
     if (md == 0) k_resid2<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
@@ -321,7 +325,6 @@ void set_attrs(int dev) {
     set_attrs_v2<8>();
     set_attrs_v2<16>();
     set_attrs_v2<32>();
-    set_attrs_s3all<1>();
     set_attrs_s3all<2>();
     set_attrs_s3all<3>();
     g_attr_done[dev] = true;
@@ -1077,7 +1080,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         a.W = ctx->Wi; a.E = L.E; a.Xold = Xold; a.Rhs = rhs; a.rconst = rconst; a.Y = Yv;
         a.theta = L.theta; a.active = L.active; a.S = (int)seq.size();
         for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
-        a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done; a.dbg = v2off >> 12;
+        a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
         pb(RBS_K_GS);
         const size_t kMaxDyn = (size_t)kSmooth2MaxDyn;
         // strip 32 with the 3-row W ring; else strip 32 with a 2-row ring (prefetch distance
@@ -1096,7 +1099,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             sm2 = Smooth2Smem(24, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 3).total;
         }
         const bool has_rhs_rows = rhs != nullptr;
-        if (!(v2off & 2048) && Bp == 32 && a.S >= 1 && a.S <= 3 && npad > 0 && npad <= 64 &&
+        if (!(v2off & 2048) && Bp == 32 && a.S >= 2 && a.S <= 3 && a.seq[0] == 0 && npad > 0 && npad <= 64 &&
             (has_rhs_rows || Xold != nullptr) &&
             Smooth3Smem(ctx->ldw, Q, has_rhs_rows, Xold != nullptr).total <= kMaxDyn) {
             // v3: register windows, all warps on the DMMA prolongation (march3.cuh)
@@ -1104,8 +1107,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             const int grid3 = a.part.nsx * a.part.nsy;
             const size_t sm3 = Smooth3Smem(ctx->ldw, Q, has_rhs_rows, Xold != nullptr).total;
             const int nkc = npad / 4;
-            if (a.S == 1) launch_s3<1>(has_rhs_rows, Xold != nullptr, nkc, grid3, sm3, st, a);
-            else if (a.S == 2) launch_s3<2>(has_rhs_rows, Xold != nullptr, nkc, grid3, sm3, st, a);
+            if (a.S == 2) launch_s3<2>(has_rhs_rows, Xold != nullptr, nkc, grid3, sm3, st, a);
             else launch_s3<3>(has_rhs_rows, Xold != nullptr, nkc, grid3, sm3, st, a);
             pe();
             return 1;

@@ -98,7 +98,6 @@ struct SmoothMarchArgs {
     int has_e;                // npad > 0
     int last;                 // LAST: y^T rhs, y^T y partials + Step 10 in the last CTA
     int init;
-    int dbg;                  // debug / A-B bits (RBS_DISABLE_V2 >> 12): k_smooth3 ablations
     SolveState s;
     const int* done;
 };
