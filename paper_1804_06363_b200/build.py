@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "librbs.so")
 SOURCES = [os.path.join(HERE, "csrc", "api.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in (
-    "kernels.cuh", "rbs_internal.cuh", "greedy.inc.cu", "march.cuh", "march2.cuh", "march3.cuh", "slab.inc.cu")] + [
+    "kernels.cuh", "rbs_internal.cuh", "greedy.inc.cu", "march.cuh", "march2.cuh", "slab.inc.cu")] + [
     os.path.join(ROOT, "include", "rbs.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -19,7 +19,7 @@
 #include <nccl.h>
 
 #include "../../include/rbs.h"
-#include "march3.cuh"
+#include "march2.cuh"
 
 using namespace rbs;
 
@@ -118,40 +118,11 @@ inline MarchPart march_part(const Geo& g, int TX, int sms) {
     p.nsy = (g.m + p.rows_per_seg - 1) / p.rows_per_seg;
     return p;
 }
-// k_smooth3 partition (one CTA per SM, strip TX = 32 - 2S): the number of row segments
-// minimises waves x (rows per segment + the 3S+1 lag steps), so a grid with more
-// strips than SMs (m = 2047: 79 strips) still fills every SM
-inline MarchPart march_part3(const Geo& g, int S, int sms) {
-    const int TX = 32 - 2 * S;
-    MarchPart best{};
-    int64_t bcost = -1;
-    const int nsx = (g.m + TX - 1) / TX;
-    for (int nsy = 1; nsy <= std::max(1, g.m / 8); ++nsy) {
-        // even segments: every segment origin has the parity of row 1 (k_smooth3's
-        // compile-time colour pattern)
-        const int rows = ((g.m + nsy - 1) / nsy + 1) & ~1;
-        const int ny = (g.m + rows - 1) / rows;
-        const int64_t waves = ((int64_t)nsx * ny + sms - 1) / sms;
-        const int64_t cost = waves * (rows + 3 * S + 1);
-        if (bcost < 0 || cost < bcost) {
-            bcost = cost;
-            best.nsx = nsx;
-            best.nsy = ny;
-            best.rows_per_seg = rows;
-        }
-    }
-    return best;
-}
 // columns of the per-CTA partial buffers of the flat / march passes
 inline int part_ctas(const Geo& g, int sms) {
     const MarchPart a = march_part(g, 32, sms), b = march_part(g, 16, sms), c = march_part(g, 24, sms);
     const MarchPart d = march_part(g, 32, 2 * sms);    // k_cgp2: 2 CTAs per SM
-    int v3 = 0;
-    for (int S = 2; S <= 3; ++S) {
-        const MarchPart e = march_part3(g, S, sms);
-        v3 = std::max(v3, e.nsx * e.nsy);
-    }
-    return std::max(std::max(std::max(flat_ctas(g), c.nsx * c.nsy), v3),
+    return std::max(std::max(flat_ctas(g), c.nsx * c.nsy),
                     std::max(std::max(a.nsx * a.nsy, b.nsx * b.nsy), d.nsx * d.nsy));
 }
 inline int grid_for(int64_t work, int per, int cap) {
@@ -246,46 +217,6 @@ void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, cons
         else launch_smooth2t<BP, false, 24, 3>(S, grid, smem, st, a);
     }
 }
-// k_smooth3 (march3.cuh): S half-sweeps, RBCG (rhs rows) or RBI (x_old + W e, constant rhs)
-template <int S, bool R, bool A>
-void set_attrs_s3() {
-    const int mx = kSmooth2MaxDyn;
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_smooth3<S, R, A, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-}
-template <int S, bool R, bool A>
-void launch_s3t(int nkc, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
-    switch (nkc) {
-        case 2: k_smooth3<S, R, A, 2><<<grid, kMT, smem, st>>>(a); break;
-        case 4: k_smooth3<S, R, A, 4><<<grid, kMT, smem, st>>>(a); break;
-        case 6: k_smooth3<S, R, A, 6><<<grid, kMT, smem, st>>>(a); break;
-        case 8: k_smooth3<S, R, A, 8><<<grid, kMT, smem, st>>>(a); break;
-        case 10: k_smooth3<S, R, A, 10><<<grid, kMT, smem, st>>>(a); break;
-        case 12: k_smooth3<S, R, A, 12><<<grid, kMT, smem, st>>>(a); break;
-        case 14: k_smooth3<S, R, A, 14><<<grid, kMT, smem, st>>>(a); break;
-        default: k_smooth3<S, R, A, 16><<<grid, kMT, smem, st>>>(a); break;
-    }
-}
-template <int S>
-void launch_s3(bool rhs, bool acc, int nkc, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
-    if (rhs && !acc) launch_s3t<S, true, false>(nkc, grid, smem, st, a);
-    else if (!rhs && acc) launch_s3t<S, false, true>(nkc, grid, smem, st, a);
-    else launch_s3t<S, true, true>(nkc, grid, smem, st, a);
-}
-template <int S>
-void set_attrs_s3all() {
-    set_attrs_s3<S, true, false>();
-    set_attrs_s3<S, false, true>();
-    set_attrs_s3<S, true, true>();
-}
-// k_smooth3 covers alternating colour sequences starting red (every symmetric / forward
-// red-black sweep: color_seq drops repeats) of 2 or 3 half-sweeps
 template <int BP, int PF>
 void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r) {
     if (md == 0) k_resid2<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
@@ -325,8 +256,6 @@ void set_attrs(int dev) {
     set_attrs_v2<8>();
     set_attrs_v2<16>();
     set_attrs_v2<32>();
-    set_attrs_s3all<2>();
-    set_attrs_s3all<3>();
     g_attr_done[dev] = true;
 }
 
@@ -1097,20 +1026,6 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             var = 2;
             TX2 = 24;
             sm2 = Smooth2Smem(24, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 3).total;
-        }
-        const bool has_rhs_rows = rhs != nullptr;
-        if (!(v2off & 2048) && Bp == 32 && a.S >= 2 && a.S <= 3 && a.seq[0] == 0 && npad > 0 && npad <= 64 &&
-            (has_rhs_rows || Xold != nullptr) &&
-            Smooth3Smem(ctx->ldw, Q, has_rhs_rows, Xold != nullptr).total <= kMaxDyn) {
-            // v3: register windows, all warps on the DMMA prolongation (march3.cuh)
-            a.part = march_part3(g, a.S, ctx->num_sms);
-            const int grid3 = a.part.nsx * a.part.nsy;
-            const size_t sm3 = Smooth3Smem(ctx->ldw, Q, has_rhs_rows, Xold != nullptr).total;
-            const int nkc = npad / 4;
-            if (a.S == 2) launch_s3<2>(has_rhs_rows, Xold != nullptr, nkc, grid3, sm3, st, a);
-            else launch_s3<3>(has_rhs_rows, Xold != nullptr, nkc, grid3, sm3, st, a);
-            pe();
-            return 1;
         }
         if (!(v2off & 1) && Bp <= 32 && a.S <= 3 && sm2 <= kMaxDyn) {
             // v2: lagged one-barrier-per-row pipeline (march2.cuh)
