@@ -304,3 +304,59 @@ def interpolated_basis(dim, m, blocks, mu_train, n, m_coarse):
     g = Grid(dim, m, blocks)
     ANq, fn = g.offline_blocks(W)
     return np.asfortranarray(W), ANq, fn
+
+
+def _interp_axis(v, axis, m_c, m_f):
+    """linear interpolation of nodal values along one axis from the coarse grid
+    (m_c interior nodes, zero boundary) to the fine grid (m_f interior nodes); exact
+    refinement: (m_f + 1) is a multiple of (m_c + 1).  Input generation only."""
+    r = (m_f + 1) // (m_c + 1)
+    v = np.moveaxis(v, axis, 0)
+    pad = np.zeros((m_c + 2,) + v.shape[1:])
+    pad[1:m_c + 1] = v
+    I = np.arange(1, m_f + 1)
+    lo, fr = I // r, (I % r) / r                                # coarse cell and fraction
+    out = pad[lo] * (1.0 - fr)[(slice(None),) + (None,) * (v.ndim - 1)] + \
+        pad[np.minimum(lo + 1, m_c + 1)] * fr[(slice(None),) + (None,) * (v.ndim - 1)]
+    return np.moveaxis(out, 0, axis)
+
+
+def offline_blocks_blas(g, W):
+    """A_{n,q} = W^T A_q W and f_n = W^T 1 (eq12c) with the oracle's
+    matrix-free operator for A_q w_j (or_apply_A, one column at a time) and a library
+    matmul for W^T Z (numpy/BLAS; a library primitive as one step); (i <= j) mirrored
+    as or_offline_blocks (O-3).  For full-size inputs, where or_offline_blocks' plain
+    loops take minutes; pinned against it (tests/test_oracle_pins.py)."""
+    W = np.asfortranarray(W, dtype=np.float64)
+    n = W.shape[1]
+    ANq = np.empty((g.Q, n, n))
+    for q in range(g.Q):
+        e = np.zeros(g.Q)
+        e[q] = 1.0
+        Z = np.empty_like(W)
+        for j in range(n):
+            Z[:, j] = g.apply_A(e, W[:, j])
+        M = W.T @ Z
+        ANq[q] = np.triu(M) + np.triu(M, 1).T
+    return ANq, W.T @ np.ones(W.shape[0])
+
+
+def fullsize_basis(dim, m, blocks, mu_train, n, m_coarse):
+    """Full-size test input at the bench's RB dimension (DESIGN.md input recipe): greedy
+    (algorithm3, or_greedy) on the coarse grid m_coarse, separable linear interpolation
+    of its basis to the fine grid, orthonormalised by a library QR (input generation:
+    the span matters, not the MGS rounding), offline blocks by offline_blocks_blas.
+    Returns (W, ANq, fn)."""
+    gc = Grid(dim, m_coarse, blocks)
+    res = gc.greedy(mu_train, n)
+    assert res["n"] == n, res["n"]
+    cols = []
+    for j in range(n):
+        v = res["W"][:, j].reshape((m_coarse,) * dim, order="F")   # axis 0 = x
+        for ax in range(dim):
+            v = _interp_axis(v, ax, m_coarse, m)
+        cols.append(v.reshape(-1, order="F"))
+    W = np.linalg.qr(np.stack(cols, axis=1))[0]
+    W = np.asfortranarray(W * np.sign(np.diag(W.T @ np.stack(cols, axis=1)))[None, :])
+    ANq, fn = offline_blocks_blas(Grid(dim, m, blocks), W)
+    return W, ANq, fn

@@ -445,6 +445,11 @@ int or_rbi(int dim, int64_t m, const int* blocks, int n, const double* W,
     memset(x, 0, sizeof(double) * (size_t)N);
     if (setup_reduced(&s, ANq) >= 0) { status = OR_REDUCED_NOT_SPD; goto done; }
     double bnorm = norm2(N, b);
+    if (!isfinite(bnorm)) {   /* AMB-11: NONFINITE (before the b = 0 shortcut below) */
+        if (hist) hist[0] = NAN;
+        status = OR_NONFINITE;
+        goto done;
+    }
     for (int it = 0;; ++it) {
         /* Step 2: r = b - A x */
         or_apply_A(dim, m, blocks, mu, x, Ax);
@@ -521,8 +526,10 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
     /* Step 1: r_0 = f - A x_0 = f */
     memcpy(r, f, sizeof(double) * (size_t)N);
     if (hist) hist[0] = fnorm > 0.0 ? 1.0 : 0.0;
-    if (!(fnorm > 0.0)) { status = OR_CONVERGED; goto final; }
+    /* AMB-11: NaN / Inf anywhere is NONFINITE -- tested before the f = 0 shortcut,
+     * which a NaN norm would otherwise take (!(NaN > 0) holds) */
     if (!isfinite(fnorm)) { status = OR_NONFINITE; goto final; }
+    if (!(fnorm > 0.0)) { status = OR_CONVERGED; goto final; }
     /* Step 2: y_0 = RBI(A, r_0, W, 1);  W^T r_0 = W^T f = f_n when b = f */
     if (o->active_n) o->active_n[0] = s.na;
     rbi_precond(&s, r, b_in == NULL ? fn : NULL, y, a_n);

@@ -1168,8 +1168,8 @@ __global__ void __launch_bounds__(128) k_setup_reduced(SolveState s, int rbi) {
         if (s.hist) s.hist[(int64_t)b * (s.maxit + 1)] = fnorm > 0.0 ? 1.0 : 0.0;
         int act = 1, st = Q_MAXIT;
         if (s_fail >= 0) { act = 0; st = Q_NOT_SPD; }
+        else if (!isfinite(fnorm)) { act = 0; st = Q_NONFINITE; }   // before f = 0 (AMB-11)
         else if (!(fnorm > 0.0)) { act = 0; st = Q_CONVERGED; }
-        else if (!isfinite(fnorm)) { act = 0; st = Q_NONFINITE; }
         else if (rbi && 1.0 < s.tol) { act = 0; st = Q_CONVERGED; }
         else if (rbi && s.maxit <= 0) { act = 0; st = Q_MAXIT; }
         s.active[b] = act;

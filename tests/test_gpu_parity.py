@@ -6,6 +6,8 @@ Same seeded inputs (synth/), same basis (built by the oracle).  Criteria
   reduced coefficients a_n to relative 1e-10, residual histories to 1e-6
   relative (+1e-13 absolute rounding floor) at every common k.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -49,13 +51,22 @@ def c1_basis(orc):
     return _BASES[key]
 
 
-def compare(gout, g_or, W, ANq, fn, mus, method, check_hist=True, **kw):
-    """run the oracle on each mu and compare with the GPU result dict."""
+def oracle_refs(g_or, W, ANq, fn, mus, method, **kw):
+    """oracle solves of every mu, in threads (ctypes releases the GIL in the C oracle)."""
+    from concurrent.futures import ThreadPoolExecutor
+    solve = g_or.rbcg if method == "rbcg" else g_or.rbi
+    with ThreadPoolExecutor(max(1, min(len(mus), os.cpu_count() or 1))) as ex:
+        return list(ex.map(lambda mu: solve(W, ANq, fn, mu, **kw), list(mus)))
+
+
+def compare(gout, g_or, W, ANq, fn, mus, method, check_hist=True, refs=None, **kw):
+    """run the oracle on each mu (or take its precomputed results `refs`) and compare
+    with the GPU result dict."""
     X = gout["X"].cpu().numpy()
     worst = dict(x=0.0, a=0.0, h=0.0, dits=0)
     for b, mu in enumerate(mus):
         solve = g_or.rbcg if method == "rbcg" else g_or.rbi
-        ref = solve(W, ANq, fn, mu, **kw)
+        ref = refs[b] if refs is not None else solve(W, ANq, fn, mu, **kw)
         assert gout["status"][b] == ref["status"], (b, gout["status"][b], ref["status"])
         d = abs(int(gout["its"][b]) - ref["its"])
         assert d <= 1, (b, gout["its"][b], ref["its"])
@@ -298,9 +309,11 @@ def test_c2_full_size_sampled(orc, rbs):
         t = np.linalg.norm(1.0 - g.apply_A(mus[b], X[b])) / np.sqrt(g.N)
         assert abs(t - out["true_relres"][b]) <= 1e-3 * t + 1e-13, b
         assert t < 1e-9, b
-    compare(dict(out, X=out["X"][[5]], status=[out["status"][5]], its=out["its"][[5]],
-                 a_n=out["a_n"][[5]], history=[out["history"][5]]),
-            g, W, ANq, fn, mus[[5]], "rbcg")
+    idx = [0, 5, 9, 13, 18, 22, 27, 31]       # 8 of the 32, in full at convergence
+    refs = oracle_refs(g, W, ANq, fn, mus[idx], "rbcg")
+    compare(dict(out, X=out["X"][idx], status=[out["status"][i] for i in idx], its=out["its"][idx],
+                 a_n=out["a_n"][idx], history=[out["history"][i] for i in idx]),
+            g, W, ANq, fn, mus[idx], "rbcg", refs=refs)
 
 
 # ----------------------------------------------------------------------------- full size c3 / c4
@@ -344,6 +357,46 @@ def test_c4_full_size_sampled(orc, rbs):
     """c4: 3D 255^3 (N = 16.6M), 2x2x2 blocks, B = 16."""
     out = _full_size_sampled(orc, rbs, "c4", 8, 31, 5, [0, 15])
     assert len(out["its"]) == 16
+
+
+_FULL = {}
+
+
+def _fullsize(orc, cname, m_coarse):
+    """full-size input at the bench's RB dimension (oracle.fullsize_basis: coarse oracle
+    greedy, interpolated, orthonormalised, oracle offline blocks); built once per session"""
+    if cname not in _FULL:
+        c = CONFIGS[cname]
+        _FULL[cname] = orc.fullsize_basis(c.dim, c.m, c.blocks, train_set(c), c.n, m_coarse)
+    return _FULL[cname]
+
+
+def _n_full_fixed(orc, rbs, cname, m_coarse, idx, K):
+    """BASELINE configs at full size AND the bench's n (npad 64 kernels, the explicit
+    A_n^{-1}): K fixed RBCG iterations of the config's batch (tol = 0), the oracle on
+    sampled queries."""
+    c = CONFIGS[cname]
+    W, ANq, fn = _fullsize(orc, cname, m_coarse)
+    assert W.shape[1] == c.n
+    g = orc.Grid(c.dim, c.m, c.blocks)
+    s = rbs.Solver(c.dim, c.m, c.blocks).load_basis(W, ANq, fn)
+    mus = query_set(c)[:c.B]
+    out = s.solve_batch(mus, tol=0.0, max_iter=K, record_history=1)
+    assert all(st == "MAXIT" for st in out["status"]) and np.all(out["its"] == K)
+    refs = oracle_refs(g, W, ANq, fn, mus[idx], "rbcg", tol=0.0, max_iter=K)
+    return compare(dict(out, X=out["X"][idx], status=[out["status"][i] for i in idx], its=out["its"][idx],
+                        a_n=out["a_n"][idx], history=[out["history"][i] for i in idx]),
+                   g, W, ANq, fn, mus[idx], "rbcg", refs=refs, tol=0.0, max_iter=K)
+
+
+def test_c3_full_size_n60(orc, rbs):
+    """c3: 2047^2, n = 60, B = 64 (two 32-query passes), 20 fixed iterations, 3 queries."""
+    _n_full_fixed(orc, rbs, "c3", 63, [0, 37, 63], 20)
+
+
+def test_c4_full_size_n60(orc, rbs):
+    """c4: 255^3, n = 60, B = 16, 20 fixed iterations, 2 queries."""
+    _n_full_fixed(orc, rbs, "c4", 31, [0, 15], 20)
 
 
 # ----------------------------------------------------------------------------- mesh slabs

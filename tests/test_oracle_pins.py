@@ -569,3 +569,52 @@ def test_cg_matches_scipy(orc, dim, m, blocks):
     xd = spla.spsolve(A.tocsc(), b)
     assert np.linalg.norm(out["x"] - xd) <= 1e-8 * np.linalg.norm(xd)
     assert np.linalg.norm(b - A @ out["x"]) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_nonfinite_rhs_is_reported(orc, small2d):
+    """AMB-11: a NaN / Inf right-hand side is NONFINITE, not the f = 0
+    shortcut (a NaN norm fails every comparison, so the finiteness test comes first)."""
+    g, tr, res = small2d
+    for bad in (np.nan, np.inf, -np.inf):
+        b = np.ones(g.N)
+        b[5] = bad
+        for solve in (g.rbcg, g.rbi):
+            out = solve(res["W"], res["ANq"], res["fn"], tr[0], b=b, max_iter=50)
+            assert out["status"] == "NONFINITE" and out["its"] == 0, (bad, solve)
+    out = g.rbcg(res["W"], res["ANq"], res["fn"], tr[0], b=np.zeros(g.N))
+    assert out["status"] == "CONVERGED" and out["its"] == 0 and not np.any(out["x"])
+
+
+def test_offline_blocks_blas_equals_plain(orc, small2d):
+    """The full-size helper (or_apply_A per column + a BLAS matmul) equals or_offline_blocks."""
+    g, _, res = small2d
+    A1, f1 = g.offline_blocks(res["W"])
+    A2, f2 = orc.offline_blocks_blas(g, res["W"])
+    assert np.abs(A1 - A2).max() <= 1e-13 * np.abs(A1).max() and np.abs(f1 - f2).max() <= 1e-13 * np.abs(f1).max()
+    for q in range(g.Q):
+        assert np.array_equal(A2[q], A2[q].T)
+
+
+@pytest.mark.parametrize("dim,mc,mf", [(2, 7, 31), (3, 3, 15)])
+def test_fullsize_basis_interpolates_linearly(orc, dim, mc, mf):
+    """The input recipe's prolongation reproduces a linear field exactly at fine nodes that
+    are not next to the boundary ramp, and the result is orthonormal."""
+    v = np.arange(1, mc + 1, dtype=float)
+    f = v.copy()
+    for ax in range(1, dim):
+        f = f[..., None] * np.ones(mc)
+    fine = f
+    for ax in range(dim):
+        fine = orc._interp_axis(fine, ax, mc, mf)
+    hc, hf = 1.0 / (mc + 1), 1.0 / (mf + 1)
+    xf = np.arange(1, mf + 1) * hf / hc                    # coarse index coordinate
+    exp = np.where(xf <= mc, xf, mc * (mc + 1 - xf))       # linear, then the ramp to the zero boundary
+    sl = (slice(None),) + (slice(4, 5),) * (dim - 1)
+    got = fine[sl].reshape(-1)
+    assert np.abs(got - exp).max() <= 1e-12
+    g = orc.Grid(dim, mf, (2,) * dim)
+    tr = 0.1 * 100 ** np.random.default_rng(3).random((12, g.Q))
+    W, A, fn = orc.fullsize_basis(dim, mf, (2,) * dim, tr, 3, mc)
+    assert np.abs(W.T @ W - np.eye(3)).max() < 1e-12
+    A2, f2 = g.offline_blocks(W)
+    assert np.abs(A - A2).max() <= 1e-12 * np.abs(A2).max()
