@@ -12,8 +12,11 @@ hot path: reduced assembly + Cholesky, residual, projection, reduced solve,
 prolongation, smoothing, CG recurrences, stop test).  Batches are independent:
 --streams S (default 2) runs S of them at a time on S CUDA streams, each with
 its own context, so one batch's latency-bound passes overlap another's.  N > 1: one process per
-GPU (torchrun), queries sharded (rank r solves its own 256), no collective on
-the data path: weak scaling.  Timing: CUDA events on the solve stream after a
+GPU (torchrun; `--gpus N` without WORLD_SIZE re-launches itself under
+torch.distributed.run), no collective on the data path.  c1/c2: every rank its
+own query set (weak scaling); c3/c4: one fixed query set (`--queries`) split into
+contiguous shards (strong scaling); c5: one 511^3 system, z-slabs over the ranks
+(rbs_dist_init, NCCL halos + 3 small allreduces per iteration; strong scaling).  Timing: CUDA events on the solve stream after a
 barrier + synchronize, max over ranks.  The working set (W 84 MB + four 67 MB
 state vectors) exceeds the 126 MB L2, so no explicit flush is needed.
 
@@ -58,6 +61,11 @@ def parse():
     p.add_argument("--streams", type=int, default=2, help="concurrent batch streams (1 = one batch at a time)")
     p.add_argument("--method", default="rbcg", choices=["rbcg", "rbi"],
                    help="RBCG (PAPER.md:260-279, default) or the stand-alone RB iteration (PAPER.md:155-169)")
+    p.add_argument("--shard", default=None, choices=["weak", "strong"],
+                   help="weak: every rank its own query set (c1/c2 default); strong: one fixed set split "
+                        "over the ranks (c3/c4 default)")
+    p.add_argument("--queries", type=int, default=0,
+                   help="strong shards / c5: size of the fixed query set (0 = the config's)")
     return p.parse_args()
 
 
@@ -119,10 +127,10 @@ class Clocks:
 
 # ----------------------------------------------------------------------------- oracle (CPU)
 def _oracle_worker(args):
-    path, idx, mu = args
+    path, idx, mu, cname = args
     import oracle
     from synth import CONFIGS as CF
-    c = CF["c2"]
+    c = CF[cname]
     d = np.load(path)
     g = oracle.Grid(c.dim, c.m, c.blocks)
     t = time.perf_counter()
@@ -136,37 +144,59 @@ def oracle_basis_file(c):
     offline blocks.  Cached per process in /tmp (rebuilt if absent)."""
     import oracle
     path = os.path.join(tempfile.gettempdir(), f"rbs_oracle_basis_{c.name}_{c.n}.npz")
+    if not os.path.exists(path) and c.m <= 63:     # small grids: the oracle greedy itself
+        res = oracle.Grid(c.dim, c.m, c.blocks).greedy(train_set(c), c.n)
+        np.savez(path, W=res["W"], ANq=res["ANq"], fn=res["fn"])
     if not os.path.exists(path):
         W, ANq, fn = oracle.interpolated_basis(c.dim, c.m, c.blocks, train_set(c), c.n, 63)
         np.savez(path, W=W, ANq=ANq, fn=fn)
     return path
 
 
+def host_info():
+    """CPU model, logical cores and RAM of this host (the cpu_baseline's machine)."""
+    model, ram = "unknown", None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                ram = round(int(ln.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count(), "ram_gib": ram}
+
+
 def cpu_oracle_run(c, nq, offset=0):
-    """solve nq queries with the oracle, one process per core; returns q/s, details."""
+    """solve nq queries with the oracle, one process per core (all host cores); returns
+    q/s, cores, wall, its, seconds per iteration per query."""
     import multiprocessing as mp
     path = oracle_basis_file(c)
     mus = query_set(c, offset + nq)[offset:]
     cores = min(nq, os.cpu_count() or 1)
     t = time.perf_counter()
     with mp.get_context("fork").Pool(cores) as pool:
-        res = pool.map(_oracle_worker, [(path, i, mus[i]) for i in range(nq)])
+        res = pool.map(_oracle_worker, [(path, i, mus[i], c.name) for i in range(nq)])
     wall = time.perf_counter() - t
     its = [r[2] for r in res]
-    return nq / wall, cores, wall, its
+    s_per_it = statistics.median(r[1] / max(r[2], 1) for r in res)
+    return nq / wall, cores, wall, its, s_per_it
 
 
 def run_reference(a):
     c = CONFIGS[a.config]
     ncpu = os.cpu_count() or 1
-    nq = min(ncpu, 8)
+    nq = ncpu                  # one query per host core per step (all cores)
     oracle_basis_file(c)
     for w in range(a.warmup):
         cpu_oracle_run(c, nq, offset=w * nq)
     t0 = time.perf_counter()
     tot_q, its_all, cores = 0, [], 1
     for s in range(a.steps):
-        _, cores, _, its = cpu_oracle_run(c, nq, offset=(a.warmup + s) * nq)
+        _, cores, _, its, _ = cpu_oracle_run(c, nq, offset=(a.warmup + s) * nq)
         tot_q += nq
         its_all += its
     el = time.perf_counter() - t0
@@ -179,7 +209,7 @@ def run_reference(a):
                        "interpolated, n=40", "oracle_its": [int(min(its_all)), int(max(its_all))]},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{nq} queries per step, one oracle process per core, "
-                                       f"RBCG to 1e-10 (host has {ncpu} cores)"},
+                                       f"RBCG to 1e-10 (host has {ncpu} cores)", "host": host_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -188,16 +218,24 @@ def run_reference(a):
 # Case 1 with RB dimension 1 and 5, Case 2 with 2 and 10 (AMB-17: the
 # text's 10 over the caption's 20), 100 random parameters per case (96 = 6 batches of 16 here)
 CASE_M, CASE_B, CASE_TRAIN, CASE_QUERIES = 127, 16, 64, 96
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r1_final_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2_traffic.json")
+# the exact instantiation each kernel class runs as at each config (what the committed
+# ncu capture must name; a capture of another instantiation is not reported)
+TIMED_KERNEL = {("c2", "k_gs"): "void k_smooth2<32, 3, 1, 32, 3, 10>(SmoothMarchArgs)",
+                ("c2", "k_proj"): "void k_resid2<32, 0, 2>(ResidMarchArgs)",
+                ("c2", "k_cgp"): "void k_cgp2<32>(CGP2Args)"}
 
 
 def ncu_traffic(config, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
-    ncu --set full capture of the same kernel and configuration (profiles/), else None."""
+    ncu --set full capture of the same configuration AND the same kernel instantiation
+    (profiles/), else None."""
     try:
         d = json.load(open(TRAFFIC_FILE))
-        if d.get("config") == config and kernel in d:
-            return d[kernel]["dram_bytes_per_launch"], f"{os.path.relpath(TRAFFIC_FILE, ROOT)}: {d[kernel]['kernel']}"
+        want = TIMED_KERNEL.get((config, kernel))
+        e = d.get("config") == config and d.get(kernel)
+        if e and want and e["kernel"] == want:
+            return e["dram_bytes_per_launch"], f"{os.path.relpath(TRAFFIC_FILE, ROOT)}: {e['kernel']}"
     except (OSError, ValueError, KeyError):
         pass
     return None, None
@@ -290,30 +328,200 @@ def run_case(a, case):
     print(json.dumps(line), flush=True)
 
 
+def spawn(a):
+    """`--gpus N` (N > 1) outside torchrun: re-launch under torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def run_c5(a, world, rank, local):
+    """BASELINE configs[4]: one 3D 511^3 system (N = 133,432,831), 2x2x2 blocks, mu logU
+    [0.01, 100]^8, n = 40, B = 8 queries per solve, RBCG.  N = 1: the unpartitioned
+    one-GPU reference solve; N > 1: z-slabs over the ranks (rbs_dist_init; NCCL halos and
+    3 small allreduces per iteration).  Basis (offline, untimed): the
+    multi-fidelity GPU builder of PAPER.md:310 -- GPU greedy on the 127^3 grid selects the
+    parameters, adaptive snapshots at them on the fine grid (RBS_GREEDY_SAMPLES).  A step =
+    one batch of B queries to convergence on all ranks (the whole job: strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1804_06363_b200 as rbs
+    c = CONFIGS["c5"]
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    plane = c.m * c.m
+    t0 = time.perf_counter()
+    n = c.n
+    if rank == 0:
+        coarse = rbs.Solver(3, 127, c.blocks, device=local)
+        grc = coarse.build_greedy(train_set(c), c.n, load=False)
+        sel = train_set(c)[grc["selected"]]
+        del coarse, grc
+        torch.cuda.empty_cache()
+        fine = rbs.Solver(3, c.m, c.blocks, device=local)
+        gr = fine.build_greedy(sel, c.n, load=False, samples=True)
+        W, ANq, fn, n = gr["W"], np.asarray(gr["ANq"]), np.asarray(gr["fn"]), gr["n"]
+        snap = [int(x) for x in gr["snap_iters"]]
+        del fine
+        torch.cuda.empty_cache()
+    if world > 1:
+        meta = torch.tensor([n], device=dev)
+        dist.broadcast(meta, 0)
+        n = int(meta.item())
+        At = torch.tensor(ANq, device=dev) if rank == 0 else torch.empty((c.P, n, n), dtype=torch.float64, device=dev)
+        ft = torch.tensor(fn, device=dev) if rank == 0 else torch.empty((n,), dtype=torch.float64, device=dev)
+        dist.broadcast(At, 0)
+        dist.broadcast(ft, 0)
+        ANq, fn = At.cpu().numpy(), ft.cpu().numpy()
+        uid = [rbs.rbs_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, 0)
+        s = rbs.Solver(3, c.m, c.blocks, device=local).dist_init(uid[0], world, rank, 3)
+        lr = s.local
+        spans = [None] * world
+        dist.all_gather_object(spans, (lr["g0"], lr["g1"]))
+        rows = torch.empty((lr["n_stored"], n), dtype=torch.float64, device=dev)
+        if rank == 0:       # each rank gets the basis rows of its stored planes
+            for r, (g0, g1) in enumerate(spans):
+                blk = W[(g0 - 1) * plane:(g1 - 1) * plane].contiguous()
+                if r == 0:
+                    rows.copy_(blk)
+                else:
+                    dist.send(blk, r)
+                del blk
+            del W
+        else:
+            dist.recv(rows, 0)
+        s.load_basis(rows, ANq, fn)
+        del rows
+        snap = snap if rank == 0 else []
+    else:
+        s = rbs.Solver(3, c.m, c.blocks, device=local).load_basis(W, ANq, fn)
+        del W
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    offline_s = time.perf_counter() - t0
+    nq = a.queries or c.n_queries
+    mus_all = query_set(c, nq)
+    nb = max(1, nq // c.B)
+    nx = s.local["n_owned"] if world > 1 else c.N
+    X = torch.empty((c.B, nx), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(k, **kw):
+        b = k % nb
+        return s.solve_batch(mus_all[b * c.B:(b + 1) * c.B], X=X, want_a_n=False, **kw)
+
+    for w in range(max(a.warmup, 1)):
+        step(w)
+    clocks = Clocks(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches, its, trr = 0, [], []
+    for k in range(a.steps):
+        out = step(k)
+        launches += out["launches"]
+        its += [int(i) for i in out["its"]]
+        trr += [float(v) for v in out["true_relres"]]
+        assert all(st == "CONVERGED" for st in out["status"]), out["status"]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop()
+    # e2e: host mu in, X (this rank's owned planes) out to pinned host memory, every step
+    Xh = torch.empty((c.B, nx), dtype=torch.float64, pin_memory=True)
+    s.solve_batch(mus_all[:c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False)
+    if world > 1:
+        dist.barrier()
+    te = time.perf_counter()
+    for k in range(a.steps):
+        b = k % nb
+        s.solve_batch(mus_all[b * c.B:(b + 1) * c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - te
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    prof = None
+    if world == 1:
+        prof = step(0, profile=1, tol=0.0, max_iter=min(a.profile_iters, 10))["profile"]
+    hbm, hbm_src = peaks()
+    line = {"metric": f"parameter queries solved/sec to rel. residual 1e-10 (c5, RBCG, {world} GPU)",
+            "value": a.steps * c.B / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(c), "B": c.B, "n": n,
+                       "parallelism": f"mesh z-slabs x{world} (NCCL)" if world > 1 else "1 GPU (reference solve)",
+                       "queries": nq, "its_min_med_max": [min(its), int(np.median(its)), max(its)],
+                       "true_relres_max": max(trr), "offline_s": round(offline_s, 1),
+                       "basis": "multi-fidelity GPU builder (127^3 greedy selects, 511^3 snapshots)",
+                       "snapshot_its": snap[:6] if rank == 0 else [],
+                       "l2": "inputs larger than L2 (W 47 GB + 4 x 8.5 GB state)"},
+            "clocks": clk, "gpu_launches": launches,
+            "e2e": {"value": a.steps * c.B / e2e_s, "unit": UNIT, "h2d_bytes_per_step": c.B * c.P * 8,
+                    "d2h_bytes_per_step": c.B * nx * 8 * world}}
+    if prof is not None:
+        tot_ms = sum(v[0] for v in prof.values())
+        line["kernels"] = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
+                               "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
+        iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)
+        iter_bytes = (80 * c.B + 16 * n) * c.N
+        line["roofline"] = {"bound": "hbm", "kernel": "iteration", "achieved": iter_bytes / (iter_us * 1e-6) / 1e9,
+                            "peak": hbm, "unit": "GB/s", "frac": iter_bytes / (iter_us * 1e-6) / 1e9 / hbm,
+                            "traffic": None, "peak_source": hbm_src, "alg_bytes_per_launch": iter_bytes,
+                            "avg_launch_us": iter_us}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl == "ours":
+        spawn(a)           # does not return
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.config in ("case1", "case2"):
         if a.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "case workloads: GPU measurement only"}))
-        elif int(os.environ.get("RANK", "0")) == 0:
+        elif rank == 0:
             run_case(a, int(a.config[-1]))
         return
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         if rank == 0:
             run_reference(a)
         return
+    if a.config == "c5":
+        run_c5(a, world, rank, local)
+        return
     import torch
     import torch.distributed as dist
     import paper_1804_06363_b200 as rbs
-    from paper_1804_06363_b200.dist import broadcast_basis, gather_counts
+    from paper_1804_06363_b200.dist import broadcast_basis, gather_counts, query_shard
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[a.config]
+    shard = a.shard or ("strong" if a.config in ("c3", "c4") else "weak")
     s = rbs.Solver(c.dim, c.m, c.blocks, device=local)
     stream = torch.cuda.current_stream()
 
@@ -336,11 +544,21 @@ def main():
     torch.cuda.synchronize()
     offline_s = time.perf_counter() - t0
 
-    # ---- queries: rank r owns its own n_queries (weak scaling) ---------------
-    nq = c.n_queries
-    mus_all = query_set(c, nq * world)
-    mus = mus_all[rank * nq:(rank + 1) * nq]
-    nb = nq // c.B
+    # ---- queries ------------------------------------------------------------
+    # weak: rank r owns its own n_queries; strong: one fixed set, contiguous shards
+    if shard == "weak":
+        nq = c.n_queries
+        mus_all = query_set(c, nq * world)
+        mus = mus_all[rank * nq:(rank + 1) * nq]
+        Bq = c.B
+    else:
+        nq_tot = a.queries or c.n_queries
+        q0, q1 = query_shard(nq_tot, world, rank)
+        mus = query_set(c, nq_tot)[q0:q1]
+        nq = q1 - q0
+        Bq = min(c.B, nq)
+    batches = [mus[i:i + Bq] for i in range(0, nq, Bq)]
+    nb = len(batches)
     # S concurrent batch streams (DESIGN.md §7 "Concurrent batches"): batch k runs on stream
     # k mod S, each stream with its own context (same basis) and buffers; the batches are
     # independent, so this is a scheduling choice that lets one batch's latency-bound
@@ -349,16 +567,15 @@ def main():
     ss = [s] + [rbs.Solver(c.dim, c.m, c.blocks, device=local).load_basis(W, ANq.cpu().numpy(), fn.cpu().numpy())
                 for _ in range(S - 1)]
     sts = [torch.cuda.Stream(device=s.device) for _ in range(S)]
-    Xs = [torch.empty((c.B, c.N), dtype=torch.float64, device=s.device) for _ in range(S)]
+    Xs = [torch.empty((Bq, c.N), dtype=torch.float64, device=s.device) for _ in range(S)]
 
     mkw = (dict(method=rbs.RBS_RBI, max_iter=500000) if a.method == "rbi" else dict(method=rbs.RBS_RBCG))
 
     def step(t, k, **kw):
-        b = k % nb
-        return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xs[t], stream=sts[t], want_a_n=False,
-                                 **{**mkw, **kw})
+        mb = batches[k % nb]
+        return ss[t].solve_batch(mb, X=Xs[t][:len(mb)], stream=sts[t], want_a_n=False, **{**mkw, **kw})
 
-    def run(nsteps, fn, nvtx=None):
+    def run(nsteps, fn_, nvtx=None):
         outs = [[] for _ in range(S)]
 
         def worker(t):
@@ -366,7 +583,7 @@ def main():
             if nvtx:
                 torch.cuda.nvtx.range_push(nvtx)
             for k in range(t, nsteps, S):
-                outs[t].append(fn(t, k))
+                outs[t].append(fn_(t, k))
             if nvtx:
                 torch.cuda.nvtx.range_pop()
 
@@ -377,7 +594,9 @@ def main():
             x.join()
         return [o for ol in outs for o in ol]
 
-    run(max(a.warmup, S), step)
+    # strong: a step = one pass over this rank's shard (the fixed set over all ranks)
+    steps_per = nb if shard == "strong" else 1
+    run(max(a.warmup * steps_per, S), step)
     # ---- timed region (device events, max over ranks) ------------------------
     clocks = Clocks(local)
     clocks.start()
@@ -387,35 +606,47 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")   # ncu --nvtx --nvtx-include "timed/" profiles only this
     ev0.record(stream)
-    outs = run(a.steps, step, nvtx="timed")     # every worker thread marks its launches too
+    outs = run(a.steps * steps_per, step, nvtx="timed")     # every worker thread marks its launches too
     torch.cuda.synchronize()
     ev1.record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    launches, its = 0, []
+    launches, its, trr, nsolved = 0, [], [], 0
     for out in outs:
         launches += out["launches"]
         its += [int(i) for i in out["its"]]
+        trr += [float(v) for v in out["true_relres"]]
+        nsolved += len(out["its"])
         assert all(st == "CONVERGED" for st in out["status"]), out["status"]
     if world > 1:
         t = torch.tensor([ms], device=s.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        tq = torch.tensor([nsolved], device=s.device)
+        dist.all_reduce(tq)
+        nsolved = int(tq.item())
+        tr = torch.tensor([max(trr)], device=s.device)
+        dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+        trr = [float(tr.item())]
         dist.barrier()
     clk = clocks.stop()
-    value = a.steps * c.B * world / (ms / 1e3)
+    value = nsolved / (ms / 1e3)
     if world > 1:   # per-query iteration counts of every rank, for the its statistics
-        t_its = torch.tensor(its, dtype=torch.int32, device=s.device)
+        L = torch.tensor([len(its)], device=s.device)
+        Lmax = L.clone()
+        dist.all_reduce(Lmax, op=dist.ReduceOp.MAX)
+        t_its = torch.full((int(Lmax.item()),), -1, dtype=torch.int32, device=s.device)
+        t_its[:len(its)] = torch.tensor(its, dtype=torch.int32, device=s.device)
         all_its, _ = gather_counts(t_its, torch.zeros_like(t_its))
-        its = [int(v) for v in all_its.cpu()]
+        its = [int(v) for v in all_its.cpu() if v >= 0]
 
     # ---- e2e: public API with host buffers (pinned X, host mu) --------------
-    Xh = [torch.empty((c.B, c.N), dtype=torch.float64, pin_memory=True) for _ in range(S)]
+    Xh = [torch.empty((Bq, c.N), dtype=torch.float64, pin_memory=True) for _ in range(S)]
 
     def step_host(t, k):
-        b = k % nb
-        return ss[t].solve_batch(mus[b * c.B:(b + 1) * c.B], X=Xh[t], x_location=rbs.RBS_MEM_HOST,
+        mb = batches[k % nb]
+        return ss[t].solve_batch(mb, X=Xh[t][:len(mb)], x_location=rbs.RBS_MEM_HOST,
                                  stream=sts[t], want_a_n=True, **mkw)
 
     run(S, step_host)      # warm-up: host-output workspace and its iteration graph per context
@@ -423,32 +654,37 @@ def main():
     if world > 1:
         dist.barrier()
     t = time.perf_counter()
-    run(a.steps, step_host)
+    eo = run(a.steps * steps_per, step_host)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t
+    ne = sum(len(o["its"]) for o in eo)
     if world > 1:
         tt = torch.tensor([e2e_s], device=s.device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e = {"value": a.steps * c.B * world / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": c.B * c.P * 8,
-           "d2h_bytes_per_step": c.B * c.N * 8 + c.B * (4 + 4 + 8 + 8 + 8 * c.n)}
+        tq = torch.tensor([ne], device=s.device)
+        dist.all_reduce(tq)
+        ne = int(tq.item())
+    e2e = {"value": ne / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": Bq * c.P * 8,
+           "d2h_bytes_per_step": Bq * c.N * 8 + Bq * (4 + 4 + 8 + 8 + 8 * c.n)}
 
     # ---- per-kernel device times (eager, events on the launching stream) -----
     prof = step(0, 0, profile=1, tol=0.0, max_iter=a.profile_iters)["profile"]
     hbm, hbm_src = peaks()
     # queries per pass: 2D batches above 32 run as 32-query sub-batches
-    Bq, N, n = (min(c.B, 32) if c.dim == 2 else c.B), c.N, c.n
+    Bp_ = min(Bq, 32) if c.dim == 2 else Bq
+    N, n = c.N, c.n
     # algorithmic bytes per launch (each vector once, W once per batch)
-    alg = {"k_cgp": 24 * Bq * N,                    # y, p_old read; p_new written
-           "k_proj": 40 * Bq * N + 8 * N * n,       # p, x, r read; x, r written; W
-           "k_gs": 16 * Bq * N + 8 * N * n}         # 2D fused smoother: r read, y written; W
+    alg = {"k_cgp": 24 * Bp_ * N,                    # y, p_old read; p_new written
+           "k_proj": 40 * Bp_ * N + 8 * N * n,       # p, x, r read; x, r written; W
+           "k_gs": 16 * Bp_ * N + 8 * N * n}         # 2D fused smoother: r read, y written; W
     if a.method == "rbi":   # RBI: K3' x_new = S(x_old + W e) (x_old, W read; x written), resid f - A x + W^T (x, W)
-        alg = {"k_gs": 16 * Bq * N + 8 * N * n, "k_proj": 8 * Bq * N + 8 * N * n}
+        alg = {"k_gs": 16 * Bp_ * N + 8 * N * n, "k_proj": 8 * Bp_ * N + 8 * N * n}
     elif c.dim == 3:   # separate prolongation pass; k_gs is one red-black half-sweep per launch
-        alg["k_prolong"] = 8 * Bq * N + 8 * N * n   # W read, y0 written
-        alg["k_gs"] = 16 * Bq * N                   # y read, r and y of one colour
-    flops = {"k_proj": 2.0 * N * n * Bq, "k_gs": 2.0 * N * n * Bq}   # W^T r / W e on DMMA
+        alg["k_prolong"] = 8 * Bp_ * N + 8 * N * n   # W read, y0 written
+        alg["k_gs"] = 16 * Bp_ * N                   # y read, r and y of one colour
+    flops = {"k_proj": 2.0 * N * n * Bp_, "k_gs": 2.0 * N * n * Bp_}   # W^T r / W e on DMMA
     tot_ms = sum(v[0] for v in prof.values())
     kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
                    "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
@@ -462,43 +698,62 @@ def main():
                 kernels[k]["fp64_tensor_TFs"] = flops[k] / d / 1e12
     top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
     kt = kernels[top]
-    iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bq queries
-    iter_bytes = ((24 * Bq + 16 * n) if a.method == "rbi" else (80 * Bq + 16 * n)) * N   # minimum per batch-iteration
+    iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bp_ queries
+    iter_bytes = ((24 * Bp_ + 16 * n) if a.method == "rbi" else (80 * Bp_ + 16 * n)) * N   # minimum per batch-iteration
     traffic, traffic_src = ncu_traffic(a.config, top)
-    roof = {"bound": "hbm", "kernel": top, "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
+    roof = {"bound": "hbm", "kernel": top, "timed_instantiation": TIMED_KERNEL.get((a.config, top)),
+            "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": kt["GBps"] / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
             "alg_bytes_per_launch": kt["alg_bytes"], "avg_launch_us": kt["avg_us"],
             "share_of_iteration": kt["share"],
             "iteration": {"us": iter_us, "alg_bytes": iter_bytes,
                           "GBps": iter_bytes / (iter_us * 1e-6) / 1e9,
                           "frac": iter_bytes / (iter_us * 1e-6) / 1e9 / hbm},
+            "solve_level": None,
             "fp64_tensor_peak_tflops": FP64_TENSOR_MEASURED_TFS,
             "fp64_tensor_peak_source": "measured, tools/fp64_peak.cu (DMMA m8n8k4, all SMs)"}
+    # solve level: the whole timed region against the per-iteration minimum bytes
+    # (queries x iterations x (80 + 16 n / B) B per node), concurrency included
+    it_q = sum(its) / max(len(its), 1)
+    per_q = (iter_bytes / Bp_) * it_q
+    roof["solve_level"] = {"GBps": value * per_q / 1e9, "frac": value * per_q / 1e9 / hbm / max(world, 1),
+                           "mean_its": it_q}
 
-    wbytes, sbytes = c.N * (((c.n + 7) // 8) * 8 + 4) * 8, 4 * c.N * c.B * 8
+    wbytes, sbytes = c.N * (((c.n + 7) // 8) * 8 + 4) * 8, 4 * c.N * Bq * 8
     l2 = (f"inputs larger than L2 (W {wbytes / 1e6:.0f} MB + 4 x {sbytes / 4e6:.0f} MB state > 126 MB)"
           if wbytes + sbytes > 126e6 else
           f"inputs fit in L2 (W {wbytes / 1e6:.1f} MB + state {sbytes / 1e6:.1f} MB): warm-L2 figure")
     metric = METRIC.replace("(c2,", f"({c.name},").replace("RBCG", a.method.upper())
+    if world > 1:
+        metric = metric.replace("1 GPU)", f"{world} GPUs)")
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(c, a.method), "queries_per_gpu": nq, "B": c.B, "n": c.n,
-                       "parallelism": f"query-shard x{world}" if world > 1 else "1 GPU",
+            "scaling": shard, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(c, a.method), "B": Bq, "n": c.n,
+                       "queries_per_gpu": nq,
+                       "queries_total": (a.queries or c.n_queries) if shard == "strong" else nq * world,
+                       "step": "one pass over the rank's query shard" if shard == "strong" else "one batch of B queries",
+                       "parallelism": f"query-shard x{world} ({shard})" if world > 1 else "1 GPU",
                        "concurrent_batches": S,
                        "l2": l2,
                        "its_min_med_max": [min(its), int(np.median(its)), max(its)],
+                       "true_relres_max": max(trr),
                        "offline_greedy_s": round(offline_s, 2), "snapshot_its": snap[:6]},
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "kernels": kernels}
-    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.method == "rbcg":
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.method == "rbcg" and c.name in ("c1", "c2"):
         try:
-            nq_cpu = min(os.cpu_count() or 1, 8)
-            v, cores, wall, oits = cpu_oracle_run(c, nq_cpu)
+            nq_cpu = min(os.cpu_count() or 1, 32)
+            v, cores, wall, oits, spi = cpu_oracle_run(c, nq_cpu)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                    "sample": f"{nq_cpu} c2 queries, one oracle process per core, "
-                                              f"RBCG to 1e-10, oracle-built interpolated basis "
-                                              f"n=40 (its {min(oits)}-{max(oits)}), wall {wall:.1f}s"}
+                                    "sample": f"{nq_cpu} {c.name} queries, one oracle process per host core, "
+                                              f"RBCG to 1e-10, oracle-built interpolated basis n={c.n} "
+                                              f"(its {min(oits)}-{max(oits)}; the GPU arm's basis comes from its own "
+                                              f"builder: the oracle takes no input from the CUDA path), "
+                                              f"wall {wall:.1f}s",
+                                    "s_per_iteration_per_query": spi,
+                                    "gpu_s_per_iteration_per_query": (ms / 1e3) / max(sum(its), 1),
+                                    "host": host_info()}
         except Exception as e:  # reported, never silently dropped
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle",
                                     "sample": f"failed: {e!r}"}
