@@ -123,8 +123,49 @@ rbs_status rbs_set_operator_faces(rbs_ctx* ctx, int dim, int64_t m, int Q, const
 rbs_status rbs_affine_rhs(rbs_ctx* ctx, int B, int R, const double* phi_host, const double* terms_dev,
                           double* out_dev, void* stream);
 
-/* R = 1, f_1 = value * ones(N), phi_1 = 1 (the BASELINE configs use 1.0). */
+/* R = 1, f_1 = value * ones(N), phi_1 = 1 (the BASELINE configs use 1.0).  Drops affine
+ * rhs terms set by rbs_set_rhs_terms (then the basis must be loaded again). */
 rbs_status rbs_set_rhs_constant(rbs_ctx* ctx, double value);
+
+/* Affine right-hand side f(mu) = sum_r phi_r(mu) f_r (eq12; the online
+ * f_N(mu) = sum_r phi_r(mu) f_{N,r} of eq12b):
+ *  f_dev: R device pointers to vectors of length N (node order of the header), BORROWED
+ *  until the next rbs_set_rhs_terms / rbs_set_rhs_constant / operator change.  R = 0
+ *  returns to the constant right-hand side.  The next rbs_load_basis (required: the
+ *  basis state is invalidated) packs the terms into the basis storage (its size grows by
+ *  N8 (round8(R)+4) doubles) and computes the offline f_{N,r} = W^T f_r and the Gram
+ *  matrix f_r^T f_s.  rbs_solve_batch with rhs_dev == NULL then forms f(mu_b) on the
+ *  device (one pass over the packed terms), f_N(mu) = sum_r phi_r f_{N,r} and
+ *  ||f(mu)||^2 = phi^T G phi without any N-length projection.  phi(mu) comes from the
+ *  parameter map (rbs_set_param_map; default: all ones).  Not with mesh slabs.
+ *  The operator change and rbs_build_greedy* drop the terms.
+ *  Errors: RBS_E_STATE (no operator), RBS_E_DIM (R > RBS_MAX_R), RBS_E_ARG (NULL pointer),
+ *  RBS_E_UNSUPPORTED (mesh slabs). */
+rbs_status rbs_set_rhs_terms(rbs_ctx* ctx, int R, const double* const* f_dev);
+
+/* Parameter map (theta_q(mu), phi_r(mu)), affine in the P parameters:
+ *   theta_q(mu) = theta_aff[q][0] + sum_p theta_aff[q][p+1] mu_p   (Q x (P+1), row-major)
+ *   phi_r(mu)   = phi_aff[r][0]   + sum_p phi_aff[r][p+1]   mu_p   (R x (P+1), row-major)
+ * theta_aff NULL = identity (P == Q); phi_aff NULL = all ones.  Set after rbs_set_rhs_terms
+ * (new terms drop phi_aff).  From then on mu_host of rbs_solve_batch is B x P.  A
+ * non-affine dependence is written with derived parameters (e.g. Case 2 of PAPER.md
+ * Table 1: mu' = (mu_1, mu_2, mu_1 mu_2), DESIGN.md AMB-23).  Copied (not borrowed).
+ * Errors: RBS_E_STATE (no operator; phi_aff without terms), RBS_E_DIM (P out of range or
+ * identity with P != Q), RBS_E_ARG (non-finite entries). */
+rbs_status rbs_set_param_map(rbs_ctx* ctx, int P, const double* theta_aff, const double* phi_aff);
+
+/* Cell-label operator: cell (a,b[,c]) (a,b,c in 0..m, x fastest) carries
+ * label cell_label_dev[a + (m+1)(b + (m+1)c)] in 0..Q-1; A(theta) is the cell-averaged
+ * stencil with kappa_cell = theta_label(cell) (AMB-1).  Realised as the face operator of
+ * rbs_set_operator_faces (DESIGN.md AMB-24): a face's coefficient for term q is the
+ * fraction of its 2^(dim-1) cells labelled q, written by a device kernel into
+ * faces_storage_dev (caller-owned, RETAINED as the face operator; size from
+ * rbs_operator_labels_size = Q dim (m+1) m^(dim-1) doubles).  labels are read once
+ * (borrowed for the call).  Synchronises `stream`.  Q <= 255.
+ * Errors: RBS_E_ARG (NULL), RBS_E_DIM, RBS_E_NOMEM (storage too small), RBS_E_CUDA. */
+rbs_status rbs_operator_labels_size(int dim, int64_t m, int Q, size_t* bytes);
+rbs_status rbs_set_operator_labels(rbs_ctx* ctx, int dim, int64_t m, int Q, const uint8_t* cell_label_dev,
+                                   void* faces_storage_dev, size_t storage_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Basis W (N x n, orthonormal columns) and offline blocks
@@ -184,10 +225,11 @@ rbs_status rbs_solve_workspace_size(const rbs_ctx* ctx, int B, const rbs_solve_o
 /*
  * rbs_solve_batch:
  *  B         1..RBS_MAX_BATCH queries.
- *  mu_host   B x P host array (P = Q), theta_q = mu_q.  Values outside the
+ *  mu_host   B x P host array: theta_q = mu_q (P = Q) or, after rbs_set_param_map,
+ *            theta(mu) and phi(mu) of the map.  Values outside the
  *            sampling box are accepted; A(mu) must be SPD for convergence.
- *  rhs_dev   NULL (use f of rbs_set_rhs_constant) or a B x N device array of
- *            per-query right-hand sides (e.g. Lemma-1 tests).
+ *  rhs_dev   NULL (use f of rbs_set_rhs_terms, else of rbs_set_rhs_constant) or a
+ *            B x N device array of per-query right-hand sides (e.g. Lemma-1 tests).
  *  X         B x N output (device, or host when opts->x_location == HOST).
  *  iters, qstatus, relres (last recurrence/true residual ratio), true_relres
  *            (||f - A x||/||f|| recomputed after exit): host arrays of B
@@ -244,6 +286,24 @@ rbs_status rbs_nccl_unique_id(void* id_out, size_t bytes);
 rbs_status rbs_dist_init(rbs_ctx* ctx, const void* nccl_id, int nranks, int rank, int ghost);
 rbs_status rbs_local_range(const rbs_ctx* ctx, int64_t* z0, int64_t* z1, int64_t* g0, int64_t* g1,
                            int64_t* n_stored, int64_t* n_owned);
+
+/* Query sharding over ranks: every rank keeps the full
+ * grid and solves its own queries with no collective on the hot path.
+ * rbs_comm_init: join an NCCL communicator (id from rbs_nccl_unique_id on one rank,
+ *   distributed by the caller) without changing the geometry.  Errors: RBS_E_ARG,
+ *   RBS_E_STATE (a mesh-slab context), RBS_E_CUDA (NCCL failure, detail in rbs_last_error).
+ * rbs_broadcast_basis: collective; the packed W, the offline blocks A_{n,q} and f_n
+ *   (eq12c) go from `root` to every rank by one ncclBroadcast of the
+ *   storage prefix that holds them.  root: the basis of dimension n must be loaded
+ *   (storage_dev ignored); other ranks: storage_dev (caller-owned, >=
+ *   rbs_basis_storage_size(n), RETAINED) becomes their basis storage, the host copies of
+ *   the blocks are rebuilt from it, and affine rhs terms (rbs_set_rhs_terms, set on every
+ *   rank) get their offline quantities locally.  Synchronises `stream`.
+ *   Errors: RBS_E_STATE (no communicator; root without that basis), RBS_E_ARG, RBS_E_DIM,
+ *   RBS_E_NOMEM, RBS_E_CUDA (NCCL failure). */
+rbs_status rbs_comm_init(rbs_ctx* ctx, const void* nccl_id, int nranks, int rank);
+rbs_status rbs_broadcast_basis(rbs_ctx* ctx, int root, int n, void* storage_dev, size_t storage_bytes,
+                               void* stream);
 
 /* Active RB dimension of every query at the end of the last rbs_solve_batch
  * (host array of B; n unless opts.n_active / opts.gamma were used). */

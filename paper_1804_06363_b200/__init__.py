@@ -56,6 +56,13 @@ _SIGS = {
     "rbs_set_operator_faces": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p]),
     "rbs_affine_rhs": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p]),
+    "rbs_set_rhs_terms": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "rbs_set_param_map": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "rbs_operator_labels_size": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.POINTER(C.c_size_t)]),
+    "rbs_set_operator_labels": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.c_size_t, C.c_void_p]),
+    "rbs_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "rbs_broadcast_basis": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]),
     "rbs_set_virtual_slabs": (C.c_int, [C.c_void_p, C.c_int]),
     "rbs_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
     "rbs_dist_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]),
@@ -150,6 +157,43 @@ def rbs_affine_rhs(ctx, B, R, phi_host, terms_dev, out_dev, stream=None):
 
 def rbs_set_rhs_constant(ctx, value):
     _check(ctx, lib().rbs_set_rhs_constant(ctx, float(value)), "rbs_set_rhs_constant")
+
+
+def rbs_set_rhs_terms(ctx, terms):
+    """terms: list of (N,) cuda float64 tensors (borrowed: keep them alive)."""
+    R = len(terms)
+    arr = (C.c_void_p * max(R, 1))(*[t.data_ptr() for t in terms])
+    _check(ctx, lib().rbs_set_rhs_terms(ctx, R, arr if R else None), "rbs_set_rhs_terms")
+
+
+def rbs_set_param_map(ctx, P, theta_aff=None, phi_aff=None):
+    ta = None if theta_aff is None else np.ascontiguousarray(theta_aff, dtype=np.float64)
+    pa = None if phi_aff is None else np.ascontiguousarray(phi_aff, dtype=np.float64)
+    _check(ctx, lib().rbs_set_param_map(ctx, int(P), _ptr(ta), _ptr(pa)), "rbs_set_param_map")
+
+
+def rbs_operator_labels_size(dim, m, Q):
+    b = C.c_size_t(0)
+    _check(None, lib().rbs_operator_labels_size(int(dim), C.c_int64(m), int(Q), C.byref(b)),
+           "rbs_operator_labels_size")
+    return b.value
+
+
+def rbs_set_operator_labels(ctx, dim, m, Q, labels_dev, storage, stream=None):
+    _check(ctx, lib().rbs_set_operator_labels(ctx, int(dim), C.c_int64(m), int(Q), _ptr(labels_dev),
+                                              _ptr(storage), storage.numel(), _stream(stream)),
+           "rbs_set_operator_labels")
+
+
+def rbs_comm_init(ctx, nccl_id: bytes, nranks, rank):
+    buf = C.create_string_buffer(nccl_id, 128)
+    _check(ctx, lib().rbs_comm_init(ctx, buf, int(nranks), int(rank)), "rbs_comm_init")
+
+
+def rbs_broadcast_basis(ctx, root, n, storage, stream=None):
+    _check(ctx, lib().rbs_broadcast_basis(ctx, int(root), int(n), _ptr(storage),
+                                          0 if storage is None else storage.numel(), _stream(stream)),
+           "rbs_broadcast_basis")
 
 
 def rbs_set_virtual_slabs(ctx, G):
@@ -331,6 +375,48 @@ class Solver:
         out = torch.empty((B, self.N), dtype=torch.float64, device=self.device)
         rbs_affine_rhs(self.ctx, B, R, phi, t, out, stream)
         return out
+
+    def set_rhs_terms(self, terms):
+        """Affine right-hand side f(mu) = sum_r phi_r(mu) f_r (rbs_set_rhs_terms): terms (R, N)
+        array or tensor; the rows are kept on the device (borrowed by the library).  Load
+        the basis afterwards."""
+        torch = self.torch
+        t = terms if torch.is_tensor(terms) else torch.as_tensor(np.ascontiguousarray(terms))
+        self._terms = t.to(device=self.device, dtype=torch.float64).contiguous()
+        rbs_set_rhs_terms(self.ctx, [self._terms[r] for r in range(self._terms.shape[0])])
+        self._ws.clear()
+        return self
+
+    def set_param_map(self, P, theta_aff=None, phi_aff=None):
+        """theta(mu) = theta_aff [1; mu], phi(mu) = phi_aff [1; mu] (rbs_set_param_map)."""
+        rbs_set_param_map(self.ctx, P, theta_aff, phi_aff)
+        self.P = int(P)
+        return self
+
+    def set_labels(self, labels):
+        """Cell-label operator (rbs_set_operator_labels): labels (m+1)^dim uint8, x fastest."""
+        torch = self.torch
+        lab = torch.as_tensor(np.ascontiguousarray(labels, dtype=np.uint8)).to(self.device)
+        Q = int(lab.max().item()) + 1
+        self._faces = self._bytes(rbs_operator_labels_size(self.dim, self.m, Q))
+        rbs_set_operator_labels(self.ctx, self.dim, self.m, Q, lab, self._faces)
+        self.Q, self.blocks, self.n = Q, None, None
+        self._ws.clear()
+        return self
+
+    def comm_init(self, nccl_id: bytes, nranks, rank):
+        """Query sharding: an NCCL communicator over the ranks (rbs_comm_init)."""
+        rbs_comm_init(self.ctx, nccl_id, nranks, rank)
+        return self
+
+    def broadcast_basis(self, root, n, stream=None):
+        """Collective: the basis of `root` to every rank (rbs_broadcast_basis)."""
+        if self._storage is None or self.n != n:
+            self._storage = self._bytes(rbs_basis_storage_size(self.ctx, n))
+        rbs_broadcast_basis(self.ctx, root, n, self._storage, stream)
+        self.n = n
+        self._ws.clear()
+        return self
 
     def set_slabs(self, G):
         """Mesh-slab mode (3D, RBCG): solve slab by slab with G z-slabs (1 = off)."""

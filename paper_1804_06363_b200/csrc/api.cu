@@ -40,6 +40,17 @@ struct rbs_ctx {
     double* dANq = nullptr;  // [Q][npad][npad]
     double* scratch = nullptr;
     std::vector<double> hANq, hfn;  // Q*n*n, n (fn = W^T 1)
+    // affine right-hand side f(phi) = sum_r phi_r f_r (rbs_set_rhs_terms; R = 0: constant):
+    // borrowed term vectors, their packed copy T [N8][ldt] in the basis storage, and the
+    // offline quantities f_{n,r} = W^T f_r (R x n) and the Gram matrix f_r^T f_s (R x R)
+    int R = 0, ldt = 0;
+    std::vector<const double*> fr;
+    double* T = nullptr;
+    std::vector<double> hfNr, hG;
+    // parameter map (rbs_set_param_map): theta = Ta [1; mu], phi = Pa [1; mu]
+    int P = 0;
+    std::vector<double> Ta, Pa;      // Q x (P+1) / R x (P+1); empty = identity / all ones
+    bool qcomm = false;              // communicator for query sharding (rbs_comm_init)
     // mesh slabs (virtual, one process): 1 = off
     int nslab = 1;
     // mesh slabs over ranks (rbs_dist_init): this rank's slab, NCCL communicator
@@ -261,18 +272,23 @@ void set_attrs(int dev) {
 
 // storage of a basis of dimension n
 struct BasisLayout {
-    double *Wi, *ANq, *Z, *part, *rows;
+    double *Wi, *ANq, *Z, *part, *rows, *T;
     size_t bytes;
 };
+// terms: packed row stride (R rounded to 8, + 4 like W)
+inline int terms_ld(int R) { return R > 0 ? (int)round_up(R, 8) + 4 : 0; }
 BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
     const int npad = (int)round_up(n, 8);
+    const int rpad = (int)round_up(c->R, 8), mpad = std::max(npad, rpad);
     Carve cv(base);
     BasisLayout L;
     L.Wi = cv.take<double>((size_t)c->N8 * w_ld(npad));
-    L.ANq = cv.take<double>((size_t)c->g.Q * npad * npad + 8);
+    // offline blocks [Q][npad][npad], then f_n (npad): the region rbs_broadcast_basis sends
+    L.ANq = cv.take<double>((size_t)c->g.Q * npad * npad + npad + 8);
     L.Z = cv.take<double>((size_t)c->N8 * 8);
-    L.part = cv.take<double>((size_t)8 * (npad + 1) * proj_ctas(c->g));
-    L.rows = cv.take<double>((size_t)8 * (npad + 1));
+    L.part = cv.take<double>((size_t)8 * (mpad + 1) * proj_ctas(c->g));
+    L.rows = cv.take<double>((size_t)8 * (mpad + 1));
+    L.T = c->R > 0 ? cv.take<double>((size_t)c->N8 * terms_ld(c->R)) : nullptr;
     L.bytes = cv.off + 256;
     return L;
 }
@@ -280,7 +296,7 @@ BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
 // solve workspace
 struct SolveLayout {
     double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout, *T;
-    double *theta, *fproj, *L, *Ainv, *E, *a_n, *partP, *partF;
+    double *theta, *fproj, *L, *Ainv, *E, *a_n, *partP, *partF, *phi;
     double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist;
     int *active, *status, *its, *pivot, *ints, *na;
     size_t bytes;
@@ -303,6 +319,7 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.F = rhs ? cv.take<double>(vec) : nullptr;
     L.Xout = o->x_location == RBS_MEM_HOST ? cv.take<double>((size_t)B * c->g.N) : nullptr;
     L.theta = cv.take<double>((size_t)c->g.Q * Bp);
+    L.phi = c->R > 0 ? cv.take<double>((size_t)Bp * c->R) : nullptr;
     L.fproj = cv.take<double>((size_t)Bp * (npad + 1));
     L.L = cv.take<double>((size_t)Bp * npad * npad + 8);
     L.Ainv = cv.take<double>((size_t)Bp * npad * npad + 8);
@@ -368,6 +385,62 @@ std::vector<int> color_seq(int smoother, int sweeps) {
             if (s.empty() || s.back() != seq[t]) s.push_back(seq[t]);
     }
     return s;
+}
+
+}  // namespace
+
+namespace {
+// affine right-hand side terms (rbs_set_rhs_terms) of a loaded basis: packed copy T,
+// f_{n,r} = W^T f_r and the Gram matrix (rbs_load_basis, rbs_broadcast_basis)
+rbs_status terms_offline(rbs_ctx* ctx, const BasisLayout& L, cudaStream_t st) {
+    // affine right-hand side terms (rbs_set_rhs_terms): packed copy T, f_{n,r} = W^T f_r
+    // (eq12c) and the Gram matrix f_r^T f_s for ||f(mu)||^2 = phi^T G phi --
+    // both by the projection pass, 8 terms at a time (a term chunk is the projected vector V;
+    // for G, T itself plays W)
+    const Geo& g = ctx->g;
+    const int n = ctx->n, npad = ctx->npad;
+    ctx->T = L.T;
+    ctx->ldt = terms_ld(ctx->R);
+    ctx->hfNr.assign((size_t)ctx->R * n, 0.0);
+    ctx->hG.assign((size_t)ctx->R * ctx->R, 0.0);
+    if (ctx->R > 0) {
+        TermPtrs tp{};
+        for (int r = 0; r < ctx->R; ++r) tp.p[r] = ctx->fr[r];
+        k_pack_terms<<<grid_for(ctx->N8 * ctx->ldt, 256, 4 * ctx->num_sms * 8), 256, 0, st>>>(
+            tp, ctx->R, g.N, ctx->N8, ctx->ldt, L.T);
+        CKL();
+        const int nct = proj_ctas(g), rpad = (int)round_up(ctx->R, 8);
+        std::vector<double> rows((size_t)8 * (std::max(npad, rpad) + 1));
+        for (int r0 = 0; r0 < ctx->R; r0 += 8) {
+            k_take8<<<grid_for(ctx->N8 * 8, 256, 4 * ctx->num_sms * 8), 256, 0, st>>>(L.T, ctx->ldt, r0, ctx->R,
+                                                                                   ctx->N8, L.Z);
+            CKL();
+            for (int pass = 0; pass < 2; ++pass) {     // 0: W^T f_r, 1: T^T f_r (Gram)
+                const int np_ = pass == 0 ? npad : rpad;
+                if (np_ == 0) continue;
+                ProjArgs a{};
+                a.g = g; a.Bp = 8; a.npad = np_; a.nct = nct; a.ngroups = (g.N + 3) / 4;
+                a.ldw = pass == 0 ? ctx->ldw : ctx->ldt;
+                a.W = pass == 0 ? L.Wi : L.T; a.V = L.Z; a.part = L.part;
+                launch_proj<MODE_PLAIN>(g, nct, proj_smem(g, 8, np_), st, a);
+                CKL();
+                k_reduce_rows<<<8, 128, 0, st>>>(L.part, np_ + 1, nct, L.rows);
+                CKL();
+                CK(cudaMemcpyAsync(rows.data(), L.rows, (size_t)8 * (np_ + 1) * 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (int k = 0; k < 8 && r0 + k < ctx->R; ++k) {
+                    const int r = r0 + k;
+                    if (pass == 0)
+                        for (int j = 0; j < n; ++j) ctx->hfNr[(size_t)r * n + j] = rows[(size_t)k * (np_ + 1) + j];
+                    else
+                        for (int j = 0; j < ctx->R; ++j) ctx->hG[(size_t)j * ctx->R + r] = rows[(size_t)k * (np_ + 1) + j];
+                }
+            }
+        }
+        for (int i = 0; i < ctx->R; ++i)          // exactly symmetric (i <= j mirrored)
+            for (int j = 0; j < i; ++j) ctx->hG[(size_t)i * ctx->R + j] = ctx->hG[(size_t)j * ctx->R + i];
+    }
+    return RBS_OK;
 }
 
 }  // namespace
@@ -501,6 +574,12 @@ rbs_status rbs_set_operator_blocks(rbs_ctx* ctx, int dim, const int64_t m[3], co
     ctx->N8 = round_up(N, 8);
     ctx->has_op = true;
     ctx->has_basis = false;
+    ctx->R = 0;                 // a new operator drops the affine rhs terms and the parameter map
+    ctx->fr.clear();
+    ctx->T = nullptr;
+    ctx->P = 0;
+    ctx->Ta.clear();
+    ctx->Pa.clear();
     ctx->dist = false;
     ctx->nslab = 1;
     return RBS_OK;
@@ -550,7 +629,77 @@ rbs_status rbs_set_rhs_constant(rbs_ctx* ctx, double value) {
     ctx->err.clear();
     if (!std::isfinite(value)) return fail(ctx, RBS_E_ARG, "rhs constant must be finite");
     ctx->fconst = value;
+    if (ctx->R > 0) {           // back to the constant right-hand side: the basis layout changes
+        ctx->R = 0;
+        ctx->fr.clear();
+        ctx->T = nullptr;
+        ctx->Pa.clear();
+        ctx->has_basis = false;
+    }
     return RBS_OK;
+}
+
+rbs_status rbs_set_rhs_terms(rbs_ctx* ctx, int R, const double* const* f_dev) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
+    if (ctx->dist || ctx->nslab > 1) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: affine rhs terms not supported");
+    if (R < 0 || R > RBS_MAX_R) return fail(ctx, RBS_E_DIM, "R must be in 0..RBS_MAX_R");
+    if (R > 0 && !f_dev) return fail(ctx, RBS_E_ARG, "f_dev is NULL");
+    for (int r = 0; r < R; ++r)
+        if (!f_dev[r]) return fail(ctx, RBS_E_ARG, "a term pointer is NULL");
+    ctx->R = R;
+    ctx->fr.assign(f_dev, f_dev + R);
+    ctx->T = nullptr;
+    ctx->Pa.clear();            // phi map (R rows) refers to the old terms
+    ctx->has_basis = false;     // f_{n,r}, the Gram matrix and the storage layout are per basis
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+    return RBS_OK;
+}
+
+rbs_status rbs_set_param_map(rbs_ctx* ctx, int P, const double* theta_aff, const double* phi_aff) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
+    if (P < 1 || P > RBS_MAX_Q) return fail(ctx, RBS_E_DIM, "P must be in 1..RBS_MAX_Q");
+    const int Q = ctx->g.Q, R = ctx->R;
+    if (!theta_aff && P != Q) return fail(ctx, RBS_E_DIM, "identity theta map needs P == Q");
+    if (phi_aff && R == 0) return fail(ctx, RBS_E_STATE, "phi map without rhs terms (rbs_set_rhs_terms)");
+    ctx->P = P;
+    ctx->Ta.clear();
+    ctx->Pa.clear();
+    if (theta_aff) ctx->Ta.assign(theta_aff, theta_aff + (size_t)Q * (P + 1));
+    if (phi_aff) ctx->Pa.assign(phi_aff, phi_aff + (size_t)R * (P + 1));
+    for (double v : ctx->Ta)
+        if (!std::isfinite(v)) return fail(ctx, RBS_E_ARG, "theta map not finite");
+    for (double v : ctx->Pa)
+        if (!std::isfinite(v)) return fail(ctx, RBS_E_ARG, "phi map not finite");
+    return RBS_OK;
+}
+
+rbs_status rbs_operator_labels_size(int dim, int64_t m, int Q, size_t* bytes) {
+    if (!bytes || (dim != 2 && dim != 3) || m < 1 || Q < 1 || Q > RBS_MAX_Q) return RBS_E_ARG;
+    *bytes = (size_t)Q * dim * (size_t)(m + 1) * (size_t)(dim == 3 ? m * m : m) * 8;
+    return RBS_OK;
+}
+
+rbs_status rbs_set_operator_labels(rbs_ctx* ctx, int dim, int64_t m, int Q, const uint8_t* cell_label_dev,
+                                   void* faces_storage_dev, size_t storage_bytes, void* stream) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!cell_label_dev || !faces_storage_dev) return fail(ctx, RBS_E_ARG, "labels / storage is NULL");
+    size_t need = 0;
+    if (rbs_operator_labels_size(dim, m, Q, &need) != RBS_OK) return fail(ctx, RBS_E_DIM, "bad dim/m/Q");
+    if (storage_bytes < need) return fail(ctx, RBS_E_NOMEM, "face storage too small");
+    if (Q > 255) return fail(ctx, RBS_E_DIM, "labels are uint8: Q <= 255");
+    CK(cudaSetDevice(ctx->device));
+    const cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nfd = (int64_t)dim * (m + 1) * (dim == 3 ? m * m : m);
+    k_labels_to_faces<<<grid_for(nfd, 256, ctx->num_sms * 8), 256, 0, st>>>(cell_label_dev, dim, (int)m, Q,
+                                                                          (double*)faces_storage_dev);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    return rbs_set_operator_faces(ctx, dim, m, Q, (const double*)faces_storage_dev);
 }
 
 rbs_status rbs_basis_storage_size(const rbs_ctx* c, int n, size_t* bytes) {
@@ -643,12 +792,14 @@ rbs_status rbs_load_basis(rbs_ctx* ctx, int n, const double* W_dev, int64_t ldw,
         CK(cudaStreamSynchronize(st));
         for (int j = 0; j < n; ++j) ctx->hfn[j] = rows[j];
     }
-    // padded device copy of the blocks
-    std::vector<double> pad((size_t)Q * npad * npad + 8, 0.0);
+    if (rbs_status ts = terms_offline(ctx, L, st); ts != RBS_OK) return ts;
+    // padded device copy of the blocks, then f_n (the broadcast region)
+    std::vector<double> pad((size_t)Q * npad * npad + npad + 8, 0.0);
     for (int q = 0; q < Q; ++q)
         for (int i = 0; i < n; ++i)
             for (int j = 0; j < n; ++j)
                 pad[((size_t)q * npad + i) * npad + j] = ctx->hANq[((size_t)q * n + i) * n + j];
+    for (int j = 0; j < n; ++j) pad[(size_t)Q * npad * npad + j] = ctx->hfn[j];
     CK(cudaMemcpyAsync(L.ANq, pad.data(), pad.size() * 8, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     ctx->has_basis = true;
@@ -693,7 +844,10 @@ rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opt
     return RBS_OK;
 }
 
-static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, const rbs_solve_opts* o,
+// mu_host here is theta (B x Q, the parameter map already applied); phi_host (B x R)
+// the right-hand-side coefficients when affine terms are set
+static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, const double* phi_host,
+                                   const rbs_solve_opts* o,
                                    const double* rhs_dev, double* X, int* iters, int* qstatus,
                                    double* relres, double* true_relres, double* a_n, double* history,
                                    void* workspace_dev, size_t workspace_bytes, void* stream) {
@@ -705,16 +859,18 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     if (!mu_host || !X || !workspace_dev) return fail(ctx, RBS_E_ARG, "mu_host/X/workspace is NULL");
     rbs_status s0 = check_opts(ctx, o);
     if (s0 != RBS_OK) return s0;
+    const bool terms = ctx->R > 0 && rhs_dev == nullptr;   // f(mu) = sum_r phi_r f_r online
     if (ctx->nslab > 1 || ctx->dist) {
         if (rhs_dev) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: rhs override not supported");
+        if (ctx->R > 0) return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: affine rhs terms not supported");
         if (o->smoother == RBS_SMOOTH_JACOBI)
             return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: Jacobi smoother not supported");
         CK(cudaSetDevice(ctx->device));
         return solve_slabs(ctx, B, mu_host, o, X, iters, qstatus, relres, true_relres, a_n, history,
                            workspace_dev, workspace_bytes, (cudaStream_t)stream);
     }
-    SolveLayout L = solve_layout(ctx, B, o, rhs_dev != nullptr, workspace_dev);
-    if (workspace_bytes < solve_layout(ctx, B, o, rhs_dev != nullptr, nullptr).bytes)
+    SolveLayout L = solve_layout(ctx, B, o, rhs_dev != nullptr || terms, workspace_dev);
+    if (workspace_bytes < solve_layout(ctx, B, o, rhs_dev != nullptr || terms, nullptr).bytes)
         return fail(ctx, RBS_E_NOMEM, "workspace too small");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
@@ -767,6 +923,34 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         k_reduce_rows<<<Bp, 128, 0, st>>>(L.partP, npad + 1, nct_plain, L.fproj);
         CKL();
         launches += 2;
+    } else if (terms) {
+        // affine right-hand side, online (eq12b): F = sum_r phi_r f_r on the
+        // device (one pass over the packed terms), f_n(mu) = sum_r phi_r f_{n,r} and
+        // ||f(mu)||^2 = phi^T G phi from the offline quantities -- no projection pass
+        const int R = ctx->R;
+        std::vector<double> ph((size_t)Bp * R, 0.0), fp((size_t)Bp * (npad + 1), 0.0);
+        for (int b = 0; b < B; ++b) {
+            const double* pb = phi_host + (size_t)b * R;
+            for (int r = 0; r < R; ++r) ph[(size_t)b * R + r] = pb[r];
+            for (int j = 0; j < n; ++j) {
+                double v = 0.0;
+                for (int r = 0; r < R; ++r) v += pb[r] * ctx->hfNr[(size_t)r * n + j];
+                fp[(size_t)b * (npad + 1) + j] = v;
+            }
+            double ff = 0.0;
+            for (int r = 0; r < R; ++r) {
+                double gr = 0.0;
+                for (int t2 = 0; t2 < R; ++t2) gr += ctx->hG[(size_t)r * R + t2] * pb[t2];
+                ff += pb[r] * gr;
+            }
+            fp[(size_t)b * (npad + 1) + npad] = ff;
+        }
+        CK(cudaMemcpyAsync(L.phi, ph.data(), ph.size() * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(L.fproj, fp.data(), fp.size() * 8, cudaMemcpyHostToDevice, st));
+        k_fill_terms<<<fgrid, 256, 0, st>>>(L.F, g.N, ctx->N8, Bp, B, ctx->T, ctx->ldt, R, L.phi);
+        CKL();
+        ++launches;
+        Fv = L.F;
     } else {
         std::vector<double> fp((size_t)Bp * (npad + 1), 0.0);
         for (int b = 0; b < Bp; ++b) {
@@ -780,9 +964,13 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     if (cg) {
         CK(cudaMemsetAsync(L.P0, 0, vecN * 8, st));
         CK(cudaMemsetAsync(L.P1, 0, vecN * 8, st));
-        k_fill_batch<<<fgrid, 256, 0, st>>>(L.R, g.N, ctx->N8, Bp, B, rhs_dev, ctx->fconst);
-        CKL();
-        ++launches;
+        if (terms) {
+            CK(cudaMemcpyAsync(L.R, L.F, vecN * 8, cudaMemcpyDeviceToDevice, st));   // r_0 = f
+        } else {
+            k_fill_batch<<<fgrid, 256, 0, st>>>(L.R, g.N, ctx->N8, Bp, B, rhs_dev, ctx->fconst);
+            CKL();
+            ++launches;
+        }
     }
 
     SolveState S{};
@@ -1248,17 +1436,49 @@ rbs_status rbs_solve_batch(rbs_ctx* ctx, int B, const double* mu_host, const rbs
                            const double* rhs_dev, double* X, int* iters, int* qstatus,
                            double* relres, double* true_relres, double* a_n, double* history,
                            void* workspace_dev, size_t workspace_bytes, void* stream) {
-    if (!ctx || !ctx->has_op || ctx->g.dim != 2 || B <= 32 || B > RBS_MAX_BATCH || !mu_host || !X || !o)
-        return solve_batch_impl(ctx, B, mu_host, o, rhs_dev, X, iters, qstatus, relres, true_relres, a_n,
+    if (!ctx) return RBS_E_ARG;
+    // parameter map: theta_q(mu) and phi_r(mu) per query, on the host
+    std::vector<double> th, ph;
+    const double* thp = mu_host;
+    const double* php = nullptr;
+    if (ctx->has_op && mu_host && B >= 1 && B <= RBS_MAX_BATCH) {
+        const int Q = ctx->g.Q, R = ctx->R, P = ctx->P > 0 ? ctx->P : Q;
+        if (!ctx->Ta.empty()) {
+            th.assign((size_t)B * Q, 0.0);
+            for (int b = 0; b < B; ++b)
+                for (int q = 0; q < Q; ++q) {
+                    const double* row = ctx->Ta.data() + (size_t)q * (P + 1);
+                    double v = row[0];
+                    for (int k = 0; k < P; ++k) v += row[k + 1] * mu_host[(size_t)b * P + k];
+                    th[(size_t)b * Q + q] = v;
+                }
+            thp = th.data();
+        }
+        if (R > 0) {
+            ph.assign((size_t)B * R, 1.0);
+            if (!ctx->Pa.empty())
+                for (int b = 0; b < B; ++b)
+                    for (int r = 0; r < R; ++r) {
+                        const double* row = ctx->Pa.data() + (size_t)r * (P + 1);
+                        double v = row[0];
+                        for (int k = 0; k < P; ++k) v += row[k + 1] * mu_host[(size_t)b * P + k];
+                        ph[(size_t)b * R + r] = v;
+                    }
+            php = ph.data();
+        }
+    }
+    if (!ctx->has_op || ctx->g.dim != 2 || B <= 32 || B > RBS_MAX_BATCH || !mu_host || !X || !o)
+        return solve_batch_impl(ctx, B, thp, php, o, rhs_dev, X, iters, qstatus, relres, true_relres, a_n,
                                 history, workspace_dev, workspace_bytes, stream);
     const int64_t N = ctx->g.N;
-    const int P = ctx->g.Q, nb = ctx->n, hl = o->max_iter + 1;
+    const int P = ctx->g.Q, nb = ctx->n, hl = o->max_iter + 1, Rr = ctx->R;
     int64_t total = 0;
     std::vector<int> na_all;
     for (int c0 = 0; c0 < B; c0 += 32) {
         const int b = std::min(32, B - c0);
         rbs_status s = solve_batch_impl(
-            ctx, b, mu_host + (size_t)c0 * P, o, rhs_dev ? rhs_dev + (size_t)c0 * N : nullptr,
+            ctx, b, thp + (size_t)c0 * P, php ? php + (size_t)c0 * Rr : nullptr, o,
+            rhs_dev ? rhs_dev + (size_t)c0 * N : nullptr,
             X + (size_t)c0 * N, iters ? iters + c0 : nullptr, qstatus ? qstatus + c0 : nullptr,
             relres ? relres + c0 : nullptr, true_relres ? true_relres + c0 : nullptr,
             a_n ? a_n + (size_t)c0 * nb : nullptr, history ? history + (size_t)c0 * hl : nullptr,

@@ -131,6 +131,14 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
     if (mode != RBS_GREEDY_PLAIN && mode != RBS_GREEDY_ADAPTIVE && mode != RBS_GREEDY_SAMPLES)
         return fail(ctx, RBS_E_ARG, "bad mode");
     const bool from_list = mode == RBS_GREEDY_SAMPLES;   // multi-fidelity fine half
+    // the greedy works in theta space with its own right-hand side: the context's affine
+    // rhs terms and parameter map are dropped (set them again before loading a basis)
+    ctx->R = 0;
+    ctx->fr.clear();
+    ctx->T = nullptr;
+    ctx->P = 0;
+    ctx->Ta.clear();
+    ctx->Pa.clear();
     GreedyLayout L = greedy_layout(ctx, n_train, n_max, workspace);
     if (ws_bytes < L.bytes) return fail(ctx, RBS_E_NOMEM, "workspace too small");
     CK(cudaSetDevice(ctx->device));

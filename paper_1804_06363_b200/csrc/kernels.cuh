@@ -502,6 +502,99 @@ __global__ void k_affine_rhs(const double* phi, int R, const double* terms, int6
     }
 }
 
+// affine right-hand side of a batch in the internal layout (rbs_set_rhs_terms):
+// v[i][b] = sum_r phi[b][r] T[i][r] (r ascending) for i < N, b < B; 0 in the padding.
+// T: the packed terms [N8][ldt] (node-major, one read per solve)
+__global__ void k_fill_terms(double* __restrict__ v, int64_t N, int64_t N8, int Bp, int B,
+                             const double* __restrict__ T, int ldt, int R, const double* __restrict__ phi) {
+    const int64_t tot = N8 * Bp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / Bp;
+        const int b = (int)(t - i * Bp);
+        double x = 0.0;
+        if (i < N && b < B) {
+            const double* Ti = T + i * ldt;
+            for (int r = 0; r < R; ++r) x = fma(phi[b * R + r], __ldg(Ti + r), x);
+        }
+        v[t] = x;
+    }
+}
+
+// terms f_r (R borrowed device vectors of length N) -> packed node-major T[N8][ldt]
+struct TermPtrs {
+    const double* p[64];
+};
+__global__ void k_pack_terms(TermPtrs f, int R, int64_t N, int64_t N8, int ldt, double* __restrict__ T) {
+    const int64_t tot = N8 * ldt;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ldt;
+        const int r = (int)(t - i * ldt);
+        T[t] = (i < N && r < R) ? f.p[r][i] : 0.0;
+    }
+}
+
+// columns j0 .. j0+7 of a node-major [N8][ld] matrix -> [N8][8] (zero beyond ncol)
+__global__ void k_take8(const double* __restrict__ A, int ld, int j0, int ncol, int64_t N8,
+                        double* __restrict__ Z) {
+    const int64_t tot = N8 * 8;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t >> 3;
+        const int k = (int)(t & 7);
+        Z[t] = j0 + k < ncol ? A[i * ld + j0 + k] : 0.0;
+    }
+}
+
+// Cell-label operator (rbs_set_operator_labels) as face coefficients: a face's
+// coefficient for term q is the fraction of the 2^(dim-1) cells sharing it that carry
+// label q, so kappa_e = sum_q theta_q F_q[e] is the cell average of theta_label(cell)
+// (DESIGN.md AMB-1, AMB-24).  labels: (m+1)^dim cells, x fastest; F: [Q][dim][nf].
+__global__ void k_labels_to_faces(const uint8_t* __restrict__ lab, int dim, int m, int Q,
+                                  double* __restrict__ F) {
+    const int64_t M = m, M1 = m + 1;
+    const int64_t nf = M1 * (dim == 3 ? M * M : M);
+    const int64_t tot = (int64_t)dim * nf;
+    const double w = dim == 3 ? 0.25 : 0.5;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (int)(t / nf);
+        const int64_t idx = t - d * nf;
+        // decode the face (layout in include/rbs.h): the cell index along d is a (0..m);
+        // the two transverse node coordinates u, v (1..m) give cells u-1, u (and v-1, v)
+        int64_t a, u, v = 1;
+        if (d == 0) {             // idx = a + (m+1)((J-1) + m(K-1))
+            a = idx % M1;
+            const int64_t r = idx / M1;
+            u = r % M + 1;        // J
+            v = r / M + 1;        // K
+        } else if (d == 1) {      // idx = (I-1) + m(a + (m+1)(K-1))
+            u = idx % M + 1;      // I
+            const int64_t r = idx / M;
+            a = r % M1;
+            v = r / M1 + 1;       // K
+        } else {                  // idx = (I-1) + m((J-1) + m a)
+            u = idx % M + 1;      // I
+            const int64_t r = idx / M;
+            v = r % M + 1;        // J
+            a = r / M;
+        }
+        for (int q = 0; q < Q; ++q) F[((int64_t)q * dim + d) * nf + idx] = 0.0;
+        const int nv = dim == 3 ? 2 : 1;
+        for (int du = 0; du < 2; ++du)
+            for (int dv = 0; dv < nv; ++dv) {
+                int64_t c[3];
+                const int64_t cu = u - 1 + du, cv = dim == 3 ? v - 1 + dv : 0;
+                if (d == 0) { c[0] = a; c[1] = cu; c[2] = cv; }
+                else if (d == 1) { c[0] = cu; c[1] = a; c[2] = cv; }
+                else { c[0] = cu; c[1] = cv; c[2] = a; }
+                const int q = lab[c[0] + M1 * (c[1] + M1 * c[2])];
+                if (q < Q) F[((int64_t)q * dim + d) * nf + idx] += w;
+            }
+    }
+}
+
 // LAST pass of the smoother: y^T r, y^T y partials of this CTA and RBCG Step 10
 // (beta = y_{k+1}^T r_{k+1} / y_k^T r_k) in the last CTA (AMB-11)
 __device__ __forceinline__ void gs_step10(GSArgs& a, double yr, double yy) {

@@ -178,6 +178,71 @@ extern "C" rbs_status rbs_dist_init(rbs_ctx* ctx, const void* nccl_id, int nrank
     return RBS_OK;
 }
 
+// Query sharding: a communicator over the ranks without any change of
+// geometry -- every rank keeps the full grid and solves its own queries; the only
+// collective is rbs_broadcast_basis (off the hot path).
+extern "C" rbs_status rbs_comm_init(rbs_ctx* ctx, const void* nccl_id, int nranks, int rank) {
+    if (!ctx || !nccl_id) return RBS_E_ARG;
+    ctx->err.clear();
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, RBS_E_ARG, "bad nranks/rank");
+    if (ctx->dist) return fail(ctx, RBS_E_STATE, "context is a mesh slab (rbs_dist_init)");
+    CK(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    if (ctx->comm) { ncclCommDestroy(ctx->comm); ctx->comm = nullptr; }
+    const ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+    if (r != ncclSuccess) return fail(ctx, RBS_E_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    ctx->qcomm = true;
+    return RBS_OK;
+}
+
+// W (packed), the offline blocks A_{n,q} and f_n from `root` to every rank: one
+// ncclBroadcast of the storage prefix that holds them (basis_layout: Wi, then ANq, f_n).
+// Non-root ranks adopt `storage_dev` as their basis storage and rebuild the host copies;
+// affine rhs terms (set on every rank) get their offline quantities locally.
+extern "C" rbs_status rbs_broadcast_basis(rbs_ctx* ctx, int root, int n, void* storage_dev,
+                                          size_t storage_bytes, void* stream) {
+    if (!ctx) return RBS_E_ARG;
+    ctx->err.clear();
+    if (!ctx->comm || !ctx->qcomm) return fail(ctx, RBS_E_STATE, "no query communicator (rbs_comm_init)");
+    if (root < 0 || root >= ctx->nranks) return fail(ctx, RBS_E_ARG, "bad root");
+    if (n < 0 || n > RBS_MAX_N) return fail(ctx, RBS_E_DIM, "n out of range");
+    const bool is_root = ctx->rank == root;
+    if (is_root && (!ctx->has_basis || ctx->n != n)) return fail(ctx, RBS_E_STATE, "root: load the basis (dimension n) first");
+    BasisLayout L = basis_layout(ctx, n, is_root ? (void*)ctx->Wi : storage_dev);
+    if (!is_root && (!storage_dev || storage_bytes < L.bytes)) return fail(ctx, RBS_E_NOMEM, "storage too small");
+    CK(cudaSetDevice(ctx->device));
+    const cudaStream_t st = (cudaStream_t)stream;
+    const int npad = (int)round_up(n, 8), Q = ctx->g.Q;
+    const size_t count = (size_t)(L.ANq - L.Wi) + (size_t)Q * npad * npad + npad;   // doubles
+    const ncclResult_t r = ncclBroadcast(L.Wi, L.Wi, count, ncclDouble, root, ctx->comm, st);
+    if (r != ncclSuccess) return fail(ctx, RBS_E_CUDA, std::string("ncclBroadcast(basis): ") + ncclGetErrorString(r));
+    CK(cudaStreamSynchronize(st));
+    if (!is_root) {
+        if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+        ctx->n = n;
+        ctx->npad = npad;
+        ctx->ldw = w_ld(npad);
+        ctx->Wi = L.Wi;
+        ctx->dANq = L.ANq;
+        ctx->scratch = L.Z;
+        std::vector<double> pad((size_t)Q * npad * npad + npad);
+        CK(cudaMemcpy(pad.data(), L.ANq, pad.size() * 8, cudaMemcpyDeviceToHost));
+        ctx->hANq.assign((size_t)Q * n * n, 0.0);
+        ctx->hfn.assign(n, 0.0);
+        for (int q = 0; q < Q; ++q)
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    ctx->hANq[((size_t)q * n + i) * n + j] = pad[((size_t)q * npad + i) * npad + j];
+        for (int j = 0; j < n; ++j) ctx->hfn[j] = pad[(size_t)Q * npad * npad + j];
+        if (rbs_status ts = terms_offline(ctx, L, st); ts != RBS_OK) return ts;
+        ctx->has_basis = true;
+    }
+    return RBS_OK;
+}
+
 extern "C" rbs_status rbs_local_range(const rbs_ctx* c, int64_t* z0, int64_t* z1, int64_t* g0, int64_t* g1,
                                       int64_t* n_stored, int64_t* n_owned) {
     if (!c) return RBS_E_ARG;
