@@ -321,42 +321,55 @@ def _interp_axis(v, axis, m_c, m_f):
     return np.moveaxis(out, 0, axis)
 
 
-def offline_blocks_blas(g, W):
+def offline_blocks_blas(g, W, threads=1):
     """A_{n,q} = W^T A_q W and f_n = W^T 1 (eq12c) with the oracle's
-    matrix-free operator for A_q w_j (or_apply_A, one column at a time) and a library
-    matmul for W^T Z (numpy/BLAS; a library primitive as one step); (i <= j) mirrored
-    as or_offline_blocks (O-3).  For full-size inputs, where or_offline_blocks' plain
-    loops take minutes; pinned against it (tests/test_oracle_pins.py)."""
+    matrix-free operator for A_q w_j (or_apply_A, one column at a time) and library
+    products for W^T (A_q w_j) (numpy/BLAS; a library primitive as one step); (i <= j)
+    mirrored as or_offline_blocks (O-3).  For full-size inputs, where or_offline_blocks'
+    plain loops take minutes; pinned against it (tests/test_oracle_pins.py).  One
+    column of A_q W at a time (memory: W plus `threads` columns); the C calls release
+    the GIL, so columns run in `threads` threads."""
+    from concurrent.futures import ThreadPoolExecutor
     W = np.asfortranarray(W, dtype=np.float64)
     n = W.shape[1]
     ANq = np.empty((g.Q, n, n))
-    for q in range(g.Q):
+
+    def col(qj):
+        q, j = qj
         e = np.zeros(g.Q)
         e[q] = 1.0
-        Z = np.empty_like(W)
-        for j in range(n):
-            Z[:, j] = g.apply_A(e, W[:, j])
-        M = W.T @ Z
+        return q, j, W.T @ g.apply_A(e, W[:, j])
+
+    jobs = [(q, j) for q in range(g.Q) for j in range(n)]
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        for q, j, c in ex.map(col, jobs):
+            ANq[q][:, j] = c
+    for q in range(g.Q):
+        M = ANq[q]
         ANq[q] = np.triu(M) + np.triu(M, 1).T
     return ANq, W.T @ np.ones(W.shape[0])
 
 
-def fullsize_basis(dim, m, blocks, mu_train, n, m_coarse):
+def fullsize_basis(dim, m, blocks, mu_train, n, m_coarse, threads=1):
     """Full-size test input at the bench's RB dimension (DESIGN.md input recipe): greedy
     (algorithm3, or_greedy) on the coarse grid m_coarse, separable linear interpolation
-    of its basis to the fine grid, orthonormalised by a library QR (input generation:
-    the span matters, not the MGS rounding), offline blocks by offline_blocks_blas.
+    of its basis to the fine grid, orthonormalised in place (modified Gram-Schmidt with
+    one re-orthogonalisation by library products: input generation, the span matters),
+    offline blocks by offline_blocks_blas.  Memory: W plus a few columns.
     Returns (W, ANq, fn)."""
     gc = Grid(dim, m_coarse, blocks)
     res = gc.greedy(mu_train, n)
     assert res["n"] == n, res["n"]
-    cols = []
+    N = m ** dim
+    W = np.empty((N, n), order="F")
     for j in range(n):
         v = res["W"][:, j].reshape((m_coarse,) * dim, order="F")   # axis 0 = x
         for ax in range(dim):
             v = _interp_axis(v, ax, m_coarse, m)
-        cols.append(v.reshape(-1, order="F"))
-    W = np.linalg.qr(np.stack(cols, axis=1))[0]
-    W = np.asfortranarray(W * np.sign(np.diag(W.T @ np.stack(cols, axis=1)))[None, :])
-    ANq, fn = offline_blocks_blas(Grid(dim, m, blocks), W)
+        w = v.reshape(-1, order="F")
+        for _ in range(2):
+            if j:
+                w = w - W[:, :j] @ (W[:, :j].T @ w)
+        W[:, j] = w / np.linalg.norm(w)
+    ANq, fn = offline_blocks_blas(Grid(dim, m, blocks), W, threads)
     return W, ANq, fn

@@ -367,7 +367,8 @@ def _fullsize(orc, cname, m_coarse):
     greedy, interpolated, orthonormalised, oracle offline blocks); built once per session"""
     if cname not in _FULL:
         c = CONFIGS[cname]
-        _FULL[cname] = orc.fullsize_basis(c.dim, c.m, c.blocks, train_set(c), c.n, m_coarse)
+        _FULL[cname] = orc.fullsize_basis(c.dim, c.m, c.blocks, train_set(c), c.n, m_coarse,
+                                          threads=os.cpu_count() or 1)
     return _FULL[cname]
 
 
