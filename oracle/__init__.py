@@ -22,7 +22,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 
-SYM_RBGS, FWD_RBGS, JACOBI = 0, 1, 2
+SYM_RBGS, FWD_RBGS, JACOBI, FWD_LEX, SYM_LEX = 0, 1, 2, 3, 4
+PRECOND_POST, PRECOND_SYM = 0, 1
+BETA_FR, BETA_PR = 0, 1
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "REDUCED_NOT_SPD", 3: "CURVATURE", 4: "PRECOND",
           5: "NONFINITE"}
 
@@ -39,7 +41,8 @@ def build(force: bool = False) -> str:
 class _Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("smoother", C.c_int),
                 ("sweeps", C.c_int), ("omega", C.c_double), ("delta", C.c_double),
-                ("n_active", C.c_int), ("gamma", C.c_double), ("active_n", C.POINTER(C.c_int))]
+                ("n_active", C.c_int), ("gamma", C.c_double), ("active_n", C.POINTER(C.c_int)),
+                ("precond", C.c_int), ("beta_rule", C.c_int)]
 
 
 _lib = None
@@ -140,7 +143,7 @@ class Grid:
 
     # -- solvers ------------------------------------------------------------
     def _solve(self, fname, W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps, omega, delta,
-               n_active=0, gamma=0.0):
+               n_active=0, gamma=0.0, precond=0, beta_rule=0):
         n = 0 if W is None else W.shape[1]
         Wf = np.asfortranarray(W, dtype=np.float64) if n else np.zeros((1, 1))
         ANq = np.ascontiguousarray(ANq, dtype=np.float64) if n else np.zeros(1)
@@ -148,7 +151,8 @@ class Grid:
         mu = np.ascontiguousarray(mu, dtype=np.float64)
         bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
         act = np.zeros(max_iter + 2, dtype=np.int32)
-        o = _Opts(tol, max_iter, smoother, sweeps, omega, delta, int(n_active), float(gamma), _i(act))
+        o = _Opts(tol, max_iter, smoother, sweeps, omega, delta, int(n_active), float(gamma), _i(act),
+                  int(precond), int(beta_rule))
         x = np.empty(self.N)
         its = C.c_int(0)
         hist = np.full(max_iter + 2, np.nan)
@@ -167,12 +171,29 @@ class Grid:
                            omega, delta, n_active)
 
     def rbcg(self, W, ANq, fn, mu, b=None, tol=1e-10, max_iter=20000, smoother=SYM_RBGS,
-             sweeps=1, omega=1.0, delta=1e-12, n_active=0, gamma=0.0):
+             sweeps=1, omega=1.0, delta=1e-12, n_active=0, gamma=0.0, precond=PRECOND_POST,
+             beta_rule=BETA_FR):
         """n_active: active RB dimension (0 = all columns); gamma > 0: the adaptive-n
         rule of PAPER.md:287 (the result's active_n[k] is the dimension of the k-th
-        preconditioner application)."""
+        preconditioner application); precond: the paper's post-smoothed RBI (0) or the
+        symmetric two-level RBI (1); beta_rule: as printed (0) or Polak-Ribiere (1)."""
         return self._solve("or_rbcg", W, ANq, fn, mu, b, tol, max_iter, smoother, sweeps,
-                           omega, delta, n_active, gamma)
+                           omega, delta, n_active, gamma, precond, beta_rule)
+
+    def precond_apply(self, W, ANq, mu, r, smoother=SYM_RBGS, sweeps=1, omega=1.0, precond=PRECOND_POST):
+        """y = M^{-1} r, one application of the RBCG preconditioner (or_precond_apply)."""
+        n = 0 if W is None else W.shape[1]
+        Wf = np.asfortranarray(W, dtype=np.float64) if n else np.zeros((1, 1))
+        A = np.ascontiguousarray(ANq, dtype=np.float64) if n else np.zeros(1)
+        act = np.zeros(2, dtype=np.int32)
+        o = _Opts(0.0, 1, smoother, sweeps, omega, 1e-12, 0, 0.0, _i(act), int(precond), 0)
+        y = np.empty(self.N)
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        st = self._lib().or_precond_apply(self.dim, C.c_int64(self.m), self._cb, n, _d(Wf), _d(A), _d(mu),
+                                          C.byref(o), _d(r), _d(y))
+        assert st == 0
+        return y
 
     def cg(self, mu, b=None, tol=1e-10, max_iter=100000):
         mu = np.ascontiguousarray(mu, dtype=np.float64)

@@ -186,11 +186,28 @@ static void jacobi_sweep(int dim, int64_t m, const int* blocks, const double* th
     free(z);
 }
 
+/* lexicographic Gauss-Seidel sweep (node order P ascending, or descending when
+ * backward): the ordering SPEC.md:288 uses for its program -- here a comparison smoother
+ * (NEXT(3)); same direct-form update as the red-black half-sweep */
+static void lex_sweep(int dim, int64_t m, const int* blocks, const double* theta,
+                      const double* b, double* y, int backward)
+{
+    int64_t N = dim == 3 ? m * m * m : m * m;
+    for (int64_t t = 0; t < N; ++t) {
+        int64_t P = backward ? N - 1 - t : t;
+        int64_t I = P % m + 1, J = (P / m) % m + 1, K = dim == 3 ? P / (m * m) + 1 : 1;
+        y[P] = gs_value(dim, m, blocks, theta, b, y, I, J, K, P);
+    }
+}
+
 void or_smooth(int dim, int64_t m, const int* blocks, const double* theta,
                const double* b, double* y, int kind, int sweeps, double omega)
 {
     for (int s = 0; s < sweeps; ++s) {
-        if (kind == OR_SMOOTH_JACOBI) {
+        if (kind == OR_SMOOTH_FWD_LEX || kind == OR_SMOOTH_SYM_LEX) {
+            lex_sweep(dim, m, blocks, theta, b, y, 0);
+            if (kind == OR_SMOOTH_SYM_LEX) lex_sweep(dim, m, blocks, theta, b, y, 1);
+        } else if (kind == OR_SMOOTH_JACOBI) {
             jacobi_sweep(dim, m, blocks, theta, b, y, omega);
         } else {
             /* forward sweep: red then black */
@@ -201,6 +218,26 @@ void or_smooth(int dim, int64_t m, const int* blocks, const double* theta,
                 or_gs_halfsweep(dim, m, blocks, theta, b, y, 1);
                 or_gs_halfsweep(dim, m, blocks, theta, b, y, 0);
             }
+        }
+    }
+}
+
+void or_smooth_adjoint(int dim, int64_t m, const int* blocks, const double* theta,
+                       const double* b, double* y, int kind, int sweeps, double omega)
+{
+    for (int s = 0; s < sweeps; ++s) {
+        if (kind == OR_SMOOTH_FWD_LEX || kind == OR_SMOOTH_SYM_LEX) {
+            if (kind == OR_SMOOTH_SYM_LEX) lex_sweep(dim, m, blocks, theta, b, y, 0);
+            lex_sweep(dim, m, blocks, theta, b, y, 1);
+        } else if (kind == OR_SMOOTH_JACOBI) {
+            jacobi_sweep(dim, m, blocks, theta, b, y, omega);
+        } else {
+            if (kind == OR_SMOOTH_SYM_RBGS) {     /* R,B,B,R reversed is itself */
+                or_gs_halfsweep(dim, m, blocks, theta, b, y, 0);
+                or_gs_halfsweep(dim, m, blocks, theta, b, y, 1);
+            }
+            or_gs_halfsweep(dim, m, blocks, theta, b, y, 1);   /* forward R,B reversed: B,R */
+            or_gs_halfsweep(dim, m, blocks, theta, b, y, 0);
         }
     }
 }
@@ -487,6 +524,24 @@ static void rbi_precond(const solver_ctx* s, const double* r, const double* rn_g
                         double* y, double* e_out)
 {
     memset(y, 0, sizeof(double) * (size_t)s->N);
+    if (s->o->precond == OR_PRECOND_SYM) {
+        /* symmetric two-level RBI (NEXT(3)): y1 = S*(A, r, 0); y2 = y1 + W A_n^{-1} W^T
+         * (r - A y1); y = S(A, r, y2) -- M^{-1} is symmetric (S* the adjoint of S) */
+        or_smooth_adjoint(s->dim, s->m, s->blocks, s->theta, r, y, s->o->smoother, s->o->sweeps,
+                          s->o->omega);
+        if (s->n > 0) {
+            double* q = (double*)malloc(sizeof(double) * (size_t)s->N);
+            or_apply_A(s->dim, s->m, s->blocks, s->theta, y, q);
+            for (int64_t i = 0; i < s->N; ++i) q[i] = r[i] - q[i];
+            project(s, q, s->rn);
+            free(q);
+            solve_active(s, s->rn, s->e);
+            if (e_out) memcpy(e_out, s->e, sizeof(double) * (size_t)s->n);
+            prolong_add(s, s->e, y);
+        }
+        or_smooth(s->dim, s->m, s->blocks, s->theta, r, y, s->o->smoother, s->o->sweeps, s->o->omega);
+        return;
+    }
     if (s->n > 0) {
         if (rn_given) memcpy(s->rn, rn_given, sizeof(double) * (size_t)s->n);
         else project(s, r, s->rn);
@@ -514,6 +569,7 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
     double* y = (double*)malloc(sizeof(double) * (size_t)N);
     double* p = (double*)malloc(sizeof(double) * (size_t)N);
     double* q = (double*)malloc(sizeof(double) * (size_t)N);
+    double* rold = o->beta_rule == OR_BETA_PR ? (double*)malloc(sizeof(double) * (size_t)N) : NULL;
     if (b_in) memcpy(f, b_in, sizeof(double) * (size_t)N);
     else for (int64_t i = 0; i < N; ++i) f[i] = 1.0;
     int status = OR_MAXIT;
@@ -532,7 +588,7 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
     if (!(fnorm > 0.0)) { status = OR_CONVERGED; goto final; }
     /* Step 2: y_0 = RBI(A, r_0, W, 1);  W^T r_0 = W^T f = f_n when b = f */
     if (o->active_n) o->active_n[0] = s.na;
-    rbi_precond(&s, r, b_in == NULL ? fn : NULL, y, a_n);
+    rbi_precond(&s, r, (b_in == NULL && o->precond != OR_PRECOND_SYM) ? fn : NULL, y, a_n);
     /* Step 3: p_0 = y_0 */
     memcpy(p, y, sizeof(double) * (size_t)N);
     double rho = or_dot(N, r, y);
@@ -549,6 +605,7 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
         double alpha = rho / sigma;
         /* Step 6-7 */
         for (int64_t i = 0; i < N; ++i) x[i] = x[i] + alpha * p[i];
+        if (rold) memcpy(rold, r, sizeof(double) * (size_t)N);   /* r_k, for the PR beta */
         const double rnorm_k = norm2(N, r);
         for (int64_t i = 0; i < N; ++i) r[i] = r[i] - alpha * q[i];
         const double rnorm_k1 = norm2(N, r);
@@ -569,7 +626,8 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
             status = isfinite(rho_new) ? OR_PRECOND : OR_NONFINITE;
             break;
         }
-        double beta = rho_new / rho;
+        /* FR as printed; PR (flexible): beta = y_{k+1}^T (r_{k+1} - r_k) / y_k^T r_k */
+        double beta = rold ? (rho_new - or_dot(N, y, rold)) / rho : rho_new / rho;
         /* Step 11: p_{k+1} = y_{k+1} + beta_k p_k */
         for (int64_t i = 0; i < N; ++i) p[i] = y[i] + beta * p[i];
         rho = rho_new;
@@ -581,8 +639,25 @@ final:
         *true_relres = fnorm > 0.0 ? norm2(N, q) / fnorm : 0.0;
     }
 done:
-    free(s.L); free(s.rn); free(s.e); free(f); free(r); free(y); free(p); free(q);
+    free(s.L); free(s.rn); free(s.e); free(f); free(r); free(y); free(p); free(q); free(rold);
     return status;
+}
+
+/* one application of the RBCG preconditioner y = M^{-1} r (either variant), for tests */
+int or_precond_apply(int dim, int64_t m, const int* blocks, int n, const double* W,
+                     const double* ANq, const double* mu, const or_opts* o, const double* r, double* y)
+{
+    solver_ctx s = {dim, m, blocks, grid_N(dim, m), grid_Q(dim, blocks), n, W, NULL, mu, o,
+                    NULL, NULL};
+    s.na = (o->n_active > 0 && o->n_active < n) ? o->n_active : n;
+    s.L = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+    s.rn = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    s.e = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    int st = 0;
+    if (setup_reduced(&s, ANq) >= 0) st = -1;
+    else rbi_precond(&s, r, NULL, y, NULL);
+    free(s.L); free(s.rn); free(s.e);
+    return st;
 }
 
 int or_cg(int dim, int64_t m, const int* blocks, const double* mu, const double* b_in,

@@ -25,7 +25,10 @@
 extern "C" {
 #endif
 
-enum { OR_SMOOTH_SYM_RBGS = 0, OR_SMOOTH_FWD_RBGS = 1, OR_SMOOTH_JACOBI = 2 };
+enum { OR_SMOOTH_SYM_RBGS = 0, OR_SMOOTH_FWD_RBGS = 1, OR_SMOOTH_JACOBI = 2,
+       OR_SMOOTH_FWD_LEX = 3, OR_SMOOTH_SYM_LEX = 4 };   /* lexicographic GS: comparison only */
+enum { OR_PRECOND_POST = 0, OR_PRECOND_SYM = 1 };   /* RBCG preconditioner (NEXT(3)) */
+enum { OR_BETA_FR = 0, OR_BETA_PR = 1 };            /* RBCG beta (NEXT(3)) */
 enum { OR_CONVERGED = 0, OR_MAXIT = 1, OR_REDUCED_NOT_SPD = 2, OR_CURVATURE = 3,
        OR_PRECOND = 4, OR_NONFINITE = 5 };
 
@@ -41,6 +44,11 @@ typedef struct {
                           dimension by one when ||r_k|| / ||r_{k+1}|| < gamma */
     int* active_n;     /* optional, max_iter+1 entries: active dimension of the k-th
                           preconditioner application (RBCG) / correction (RBI) */
+    int precond;       /* RBCG: OR_PRECOND_POST (the paper's RBI(A, r, W, 1)) or
+                          OR_PRECOND_SYM: pre-smoothing with the adjoint sweep, coarse
+                          correction, post-smoothing (NEXT(3)) */
+    int beta_rule;     /* RBCG: OR_BETA_FR (as printed) or OR_BETA_PR
+                          (Polak-Ribiere / flexible: (y_{k+1}^T (r_{k+1} - r_k)) / y_k^T r_k) */
 } or_opts;
 
 /* General affine operator (NEXT(4), AMB-23): blocks = {0,0,0} selects face
@@ -57,6 +65,12 @@ void or_gs_halfsweep(int dim, int64_t m, const int* blocks, const double* theta,
 /* smoother S(A, b, y) in place, PAPER.md:148-153 (eq8). */
 void or_smooth(int dim, int64_t m, const int* blocks, const double* theta,
                const double* b, double* y, int kind, int sweeps, double omega);
+/* its adjoint (in the A inner product) S*: the elementary sweeps in reverse order, each
+ * replaced by its adjoint (a red-black half-sweep and a Jacobi sweep are self-adjoint, a
+ * forward lexicographic sweep's adjoint is the backward sweep) -- the pre-smoother of
+ * the symmetric two-level preconditioner. */
+void or_smooth_adjoint(int dim, int64_t m, const int* blocks, const double* theta,
+                       const double* b, double* y, int kind, int sweeps, double omega);
 
 /* adaptive-n rule of PAPER.md:287 (DESIGN.md AMB-19): returns na + 1 when
  * ||r_k|| / ||r_{k+1}|| < gamma (gamma > 0) and na < n_max, else na. */
@@ -92,6 +106,11 @@ int or_rbcg(int dim, int64_t m, const int* blocks, int n, const double* W,
             const double* ANq, const double* fn, const double* mu, const double* b,
             const or_opts* o, double* x, int* its, double* hist, double* a_n,
             double* true_relres);
+
+/* one application y = M^{-1} r of the RBCG preconditioner selected by o->precond
+ * (tests of the preconditioner itself); returns 0, or -1 if A_n(mu) is not SPD. */
+int or_precond_apply(int dim, int64_t m, const int* blocks, int n, const double* W,
+                     const double* ANq, const double* mu, const or_opts* o, const double* r, double* y);
 
 /* plain CG (context only). */
 int or_cg(int dim, int64_t m, const int* blocks, const double* mu, const double* b,

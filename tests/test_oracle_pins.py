@@ -618,3 +618,117 @@ def test_fullsize_basis_interpolates_linearly(orc, dim, mc, mf):
     assert np.abs(W.T @ W - np.eye(3)).max() < 1e-12
     A2, f2 = g.offline_blocks(W)
     assert np.abs(A - A2).max() <= 1e-12 * np.abs(A2).max()
+
+
+# --------------------------------------------------------------------------- NEXT(3) variants
+@pytest.mark.parametrize("dim,m,blocks", [(2, 7, (2, 2)), (3, 4, (2, 2, 2))])
+def test_lexicographic_gs_is_textbook(orc, dim, m, blocks):
+    """Lexicographic Gauss-Seidel (the comparison ordering): one forward sweep
+    is (D + L) y_new = b - U y_old on the independently assembled matrix; the symmetric
+    sweep adds the backward sweep (D + U) y = b - L y_fwd."""
+    g = orc.Grid(dim, m, blocks)
+    mu = rand_mu(g.Q)
+    A = refs.cellwise_fd(dim, m, blocks, mu).tocsr()
+    rng = np.random.default_rng(41)
+    b, y0 = rng.standard_normal(g.N), rng.standard_normal(g.N)
+    Lw, Up = sp_tril(A), sp_triu(A)
+    yf = spla.spsolve_triangular(Lw, b - (A - Lw) @ y0, lower=True)
+    yb = spla.spsolve_triangular(Up, b - (A - Up) @ yf, lower=False)
+    assert np.abs(g.smooth(mu, b, y0, kind=orc.FWD_LEX) - yf).max() <= 1e-12 * np.abs(yf).max()
+    assert np.abs(g.smooth(mu, b, y0, kind=orc.SYM_LEX) - yb).max() <= 1e-12 * np.abs(yb).max()
+
+
+def sp_tril(A):
+    import scipy.sparse as sp
+    return sp.tril(A, format="csr")
+
+
+def sp_triu(A):
+    import scipy.sparse as sp
+    return sp.triu(A, format="csr")
+
+
+def _twolevel_independent(A, W, r, order):
+    """M^{-1} r of the symmetric two-level RBI from independent pieces: the symmetric
+    red-black GS from zero as explicit triangular solves (refs.sgs_rb_apply = B r), the
+    Galerkin coarse correction C = W (W^T A W)^{-1} W^T by numpy:
+    y1 = B r, y2 = y1 + C (r - A y1), y = y2 + B (r - A y2)."""
+    C = lambda v: W @ np.linalg.solve(W.T @ (A @ W), W.T @ v)
+    y1 = refs.sgs_rb_apply(A, order, r)
+    y2 = y1 + C(r - A @ y1)
+    return y2 + refs.sgs_rb_apply(A, order, r - A @ y2)
+
+
+def test_symmetric_twolevel_preconditioner(orc, small2d):
+    """NEXT(3): pre-smoothing with the adjoint sweep + coarse
+    correction + post-smoothing equals the independent composition, and its matrix is
+    symmetric positive definite -- unlike the paper's post-smoothed RBI, whose matrix is
+    not symmetric (AMB-6)."""
+    g, _, res = small2d
+    W, ANq = res["W"], res["ANq"]
+    mu = rand_mu(g.Q)
+    A = refs.cellwise_fd(2, g.m, g.blocks, mu).tocsr()
+    order = refs.red_black_order(2, g.m)
+    r = np.random.default_rng(43).standard_normal(g.N)
+    y = g.precond_apply(W, ANq, mu, r, precond=orc.PRECOND_SYM)
+    ref = _twolevel_independent(A, W, r, order)
+    assert np.linalg.norm(y - ref) <= 1e-11 * np.linalg.norm(ref)
+    E = np.eye(g.N)
+    Ms = np.stack([g.precond_apply(W, ANq, mu, E[:, j], precond=orc.PRECOND_SYM) for j in range(g.N)], 1)
+    Mp = np.stack([g.precond_apply(W, ANq, mu, E[:, j], precond=orc.PRECOND_POST) for j in range(g.N)], 1)
+    assert np.abs(Ms - Ms.T).max() <= 1e-11 * np.abs(Ms).max()
+    assert np.linalg.eigvalsh(0.5 * (Ms + Ms.T)).min() > 0
+    assert np.abs(Mp - Mp.T).max() > 1e-3 * np.abs(Mp).max()       # the paper's variant is not symmetric
+    # forward red-black sweeps: pre (B,R) is the adjoint of post (R,B) -> symmetric as well
+    Mf = np.stack([g.precond_apply(W, ANq, mu, E[:, j], smoother=orc.FWD_RBGS, precond=orc.PRECOND_SYM)
+                   for j in range(g.N)], 1)
+    assert np.abs(Mf - Mf.T).max() <= 1e-11 * np.abs(Mf).max()
+
+
+def test_rbcg_symmetric_precond_is_textbook_pcg(orc, small2d):
+    """RBCG with the symmetric two-level preconditioner is textbook PCG with M^{-1} built
+    from independent pieces (scipy cg): the same iteration count +-1, the same solution."""
+    g, _, res = small2d
+    mu = rand_mu(g.Q, rng=np.random.default_rng(44))
+    A = refs.cellwise_fd(2, g.m, g.blocks, mu).tocsr()
+    order = refs.red_black_order(2, g.m)
+    M = spla.LinearOperator(A.shape, matvec=lambda v: _twolevel_independent(A, res["W"], v, order))
+    count = [0]
+    b = np.ones(g.N)
+    xs, info = spla.cg(A, b, M=M, rtol=1e-10, atol=0.0, maxiter=2000,
+                       callback=lambda xk: count.__setitem__(0, count[0] + 1))
+    out = g.rbcg(res["W"], res["ANq"], res["fn"], mu, precond=orc.PRECOND_SYM)
+    assert out["status"] == "CONVERGED" and abs(out["its"] - count[0]) <= 1
+    assert np.linalg.norm(out["x"] - xs) <= 1e-8 * np.linalg.norm(xs)
+
+
+def test_rbcg_polak_ribiere(orc, small2d):
+    """Polak-Ribiere beta (flexible CG, NEXT(3)): (1) with the symmetric preconditioner PR
+    and the printed beta coincide in exact arithmetic (y_{k+1}^T r_k = 0), so the runs agree
+    to rounding; (2) with the paper's preconditioner the oracle's run equals a textbook
+    flexible PCG (PR beta) in numpy around the same preconditioner (a black box)."""
+    g, _, res = small2d
+    W, ANq, fn = res["W"], res["ANq"], res["fn"]
+    mu = rand_mu(g.Q, rng=np.random.default_rng(45))
+    a = g.rbcg(W, ANq, fn, mu, precond=orc.PRECOND_SYM, beta_rule=orc.BETA_FR, tol=1e-10)
+    b = g.rbcg(W, ANq, fn, mu, precond=orc.PRECOND_SYM, beta_rule=orc.BETA_PR, tol=1e-10)
+    assert abs(a["its"] - b["its"]) <= 1 and np.linalg.norm(a["x"] - b["x"]) <= 1e-9 * np.linalg.norm(a["x"])
+    A = refs.cellwise_fd(2, g.m, g.blocks, mu).tocsr()
+    Minv = lambda v: g.precond_apply(W, ANq, mu, v)
+    f = np.ones(g.N)
+    x, r = np.zeros(g.N), f.copy()
+    y = Minv(r)
+    p, rho, k = y.copy(), r @ y, 0
+    while True:
+        q = A @ p
+        al = rho / (p @ q)
+        x, r_old, r = x + al * p, r, r - al * q
+        k += 1
+        if np.linalg.norm(r) / np.linalg.norm(f) < 1e-10:
+            break
+        y = Minv(r)
+        rho_new = y @ r
+        p, rho = y + ((rho_new - y @ r_old) / rho) * p, rho_new
+    c = g.rbcg(W, ANq, fn, mu, beta_rule=orc.BETA_PR)
+    assert c["status"] == "CONVERGED" and abs(c["its"] - k) <= 1
+    assert np.linalg.norm(c["x"] - x) <= 1e-9 * np.linalg.norm(x)
