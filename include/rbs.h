@@ -214,7 +214,19 @@ typedef struct {
                             dimension grows by one (capped at n) for the next preconditioner
                             application; start value n_active.  Final values: rbs_last_n_active */
     double omega;        /* Jacobi damping, 0 < omega < 2 (default 1); ignored by Gauss-Seidel */
+    int precond;         /* RBCG preconditioner (NEXT(3)): RBS_PRECOND_POST
+                            (default: the paper's RBI(A, r, W, 1), post-smoothing only) or
+                            RBS_PRECOND_SYM: y1 = S*(A, r, 0) (the adjoint sweep: colour
+                            sequence reversed), y2 = y1 + W A_n^{-1} W^T (r - A y1),
+                            y = S(A, r, y2) -- a symmetric positive definite M^{-1}, so CG's
+                            theory holds (DESIGN.md AMB-25).  a_n then reports the first coarse
+                            correction.  Flat (non-march) kernels; not with mesh slabs. */
+    int beta_rule;       /* RBCG: RBS_BETA_FR (default, beta = y_{k+1}^T r_{k+1} / y_k^T r_k as
+                            printed) or RBS_BETA_PR (Polak-Ribiere / flexible:
+                            y_{k+1}^T (r_{k+1} - r_k) / y_k^T r_k); flat kernels, not with slabs */
 } rbs_solve_opts;
+enum { RBS_PRECOND_POST = 0, RBS_PRECOND_SYM = 1 };
+enum { RBS_BETA_FR = 0, RBS_BETA_PR = 1 };
 
 void rbs_default_opts(rbs_solve_opts* opts);
 

@@ -22,6 +22,8 @@ RBS_RBI, RBS_RBCG = 0, 1
 RBS_SMOOTH_SYM_RBGS, RBS_SMOOTH_FWD_RBGS, RBS_SMOOTH_JACOBI = 0, 1, 2
 RBS_MEM_DEVICE, RBS_MEM_HOST = 0, 1
 RBS_GREEDY_PLAIN, RBS_GREEDY_ADAPTIVE, RBS_GREEDY_SAMPLES = 0, 1, 2
+RBS_PRECOND_POST, RBS_PRECOND_SYM = 0, 1
+RBS_BETA_FR, RBS_BETA_PR = 0, 1
 QSTATUS = {0: "CONVERGED", 1: "MAXIT", 2: "REDUCED_NOT_SPD", 3: "CURVATURE", 4: "PRECOND",
            5: "NONFINITE"}
 
@@ -35,7 +37,7 @@ class rbs_solve_opts(C.Structure):
                 ("smoother", C.c_int), ("sweeps", C.c_int), ("delta", C.c_double),
                 ("record_history", C.c_int), ("x_location", C.c_int), ("graph_chunk", C.c_int),
                 ("profile", C.c_int), ("n_active", C.c_int), ("gamma", C.c_double),
-                ("omega", C.c_double)]
+                ("omega", C.c_double), ("precond", C.c_int), ("beta_rule", C.c_int)]
 
 
 _lib = None

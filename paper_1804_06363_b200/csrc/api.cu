@@ -295,9 +295,9 @@ BasisLayout basis_layout(const rbs_ctx* c, int n, void* base) {
 
 // solve workspace
 struct SolveLayout {
-    double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout, *T;
+    double *X, *X2, *R, *P0, *P1, *Y, *F, *Xout, *T, *Rold;
     double *theta, *fproj, *L, *Ainv, *E, *a_n, *partP, *partF, *phi;
-    double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist;
+    double *alpha, *beta, *rho, *rr, *fnorm, *relres, *hist, *rho_prev;
     int *active, *status, *its, *pivot, *ints, *na;
     size_t bytes;
 };
@@ -317,6 +317,7 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.P1 = cg ? cv.take<double>(vec) : nullptr;
     L.Y = cg ? cv.take<double>(vec) : nullptr;
     L.F = rhs ? cv.take<double>(vec) : nullptr;
+    L.Rold = (cg && o->beta_rule == RBS_BETA_PR) ? cv.take<double>(vec) : nullptr;   // r_k (PR beta)
     L.Xout = o->x_location == RBS_MEM_HOST ? cv.take<double>((size_t)B * c->g.N) : nullptr;
     L.theta = cv.take<double>((size_t)c->g.Q * Bp);
     L.phi = c->R > 0 ? cv.take<double>((size_t)Bp * c->R) : nullptr;
@@ -334,6 +335,7 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.rr = cv.take<double>(Bp);
     L.fnorm = cv.take<double>(Bp);
     L.relres = cv.take<double>(Bp);
+    L.rho_prev = cv.take<double>(Bp);
     L.hist = o->record_history ? cv.take<double>((size_t)Bp * (o->max_iter + 1)) : nullptr;
     L.active = cv.take<int>(Bp);
     L.status = cv.take<int>(Bp);
@@ -370,6 +372,12 @@ rbs_status check_opts(rbs_ctx* ctx, const rbs_solve_opts* o) {
     if (o->n_active < 0 || o->n_active > ctx->n) return fail(ctx, RBS_E_ARG, "n_active out of range 0..n");
     if (!(o->gamma >= 0.0)) return fail(ctx, RBS_E_ARG, "gamma must be >= 0");
     if (o->gamma > 0.0 && o->method != RBS_RBCG) return fail(ctx, RBS_E_ARG, "gamma rule is RBCG only");
+    if (o->precond != RBS_PRECOND_POST && o->precond != RBS_PRECOND_SYM) return fail(ctx, RBS_E_ARG, "bad precond");
+    if (o->beta_rule != RBS_BETA_FR && o->beta_rule != RBS_BETA_PR) return fail(ctx, RBS_E_ARG, "bad beta_rule");
+    if ((o->precond != RBS_PRECOND_POST || o->beta_rule != RBS_BETA_FR) && o->method != RBS_RBCG)
+        return fail(ctx, RBS_E_ARG, "precond / beta_rule are RBCG options");
+    if ((o->precond != RBS_PRECOND_POST || o->beta_rule != RBS_BETA_FR) && (ctx->dist || ctx->nslab > 1))
+        return fail(ctx, RBS_E_UNSUPPORTED, "mesh slabs: precond / beta_rule variants not supported");
     return RBS_OK;
 }
 
@@ -830,6 +838,8 @@ void rbs_default_opts(rbs_solve_opts* o) {
     o->n_active = 0;
     o->gamma = 0.0;
     o->omega = 1.0;
+    o->precond = RBS_PRECOND_POST;
+    o->beta_rule = RBS_BETA_FR;
 }
 
 rbs_status rbs_solve_workspace_size(const rbs_ctx* c, int B, const rbs_solve_opts* o, size_t* bytes) {
@@ -1062,13 +1072,16 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         }
         return cnt;
     };
-    auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last, int init) {
+    // sq: the colour sequence (default: the smoother's; the adjoint sweep of the symmetric
+    // preconditioner passes it reversed)
+    auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last, int init,
+                      const std::vector<int>* sq = nullptr) {
         if (jac) return smooth_jac(Yv, Yv, rhs, rconst, last, init);
         GSArgs a{};
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.Y = Yv; a.Rhs = rhs; a.rconst = rconst; a.init = init; a.s = S; a.done = done;
         int cnt = 0;
-        std::vector<int> cs = seq;
+        std::vector<int> cs = sq ? *sq : seq;
         if (cs.empty() && last) cs.push_back(-1);
         for (size_t t = 0; t < cs.size(); ++t) {
             a.color = cs[t];
@@ -1096,19 +1109,19 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         }
         return cnt;
     };
-    auto proj = [&](int mode, const double* P, bool use_active, double* Xv = nullptr) {
+    auto proj = [&](int mode, const double* P, bool use_active, double* Xv = nullptr, const double* Vv = nullptr) {
         if (use_rmarch && use_active) {
             ResidMarchArgs r{};
             r.g = g; r.Bp = Bp; r.npad = npad; r.ldw = ctx->ldw; r.mp = rpart; r.W = ctx->Wi;
             r.theta = L.theta; r.active = L.active; r.alpha = L.alpha; r.P = P;
-            r.X = Xv ? Xv : L.X; r.R = L.R; r.V = Fv; r.vconst = ctx->fconst;
+            r.X = Xv ? Xv : L.X; r.R = L.R; r.V = Vv ? Vv : Fv; r.vconst = ctx->fconst;
             r.part = L.partP; r.nct = nct; r.done = done;
             const int PF = resid2_smem_bytes(2, Bp, ctx->ldw, Q) <= (size_t)214 * 1024 ? 2 : 1;
             const size_t rsm = resid2_smem_bytes(PF, Bp, ctx->ldw, Q);
             pb(RBS_K_PROJ);
             const int md = mode == MODE_CG ? 0 : 1;
             if (v2off & 4) {
-                const ResidSmem rs1(Bp, ctx->ldw, Q, md, Fv != nullptr);
+                const ResidSmem rs1(Bp, ctx->ldw, Q, md, r.V != nullptr);
                 if (md == 0) k_resid_march<0><<<nct, kMarchThreads, rs1.total, st>>>(r);
                 else k_resid_march<1><<<nct, kMarchThreads, rs1.total, st>>>(r);
             } else if (Bp == 8) {
@@ -1124,7 +1137,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         ProjArgs a{};
         a.g = g; a.Bp = Bp; a.npad = npad; a.nct = nct; a.ngroups = (g.N + 3) / 4; a.ldw = ctx->ldw;
         a.W = ctx->Wi; a.theta = L.theta; a.active = use_active ? L.active : nullptr;
-        a.alpha = L.alpha; a.P = P; a.X = Xv ? Xv : L.X; a.R = L.R; a.V = Fv; a.vconst = ctx->fconst;
+        a.alpha = L.alpha; a.P = P; a.X = Xv ? Xv : L.X; a.R = L.R; a.V = Vv ? Vv : Fv; a.vconst = ctx->fconst;
         a.part = L.partP; a.done = use_active ? done : nullptr;
         a.nct = use_active ? nct : nct_plain;
         pb(RBS_K_PROJ);
@@ -1188,7 +1201,11 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
 
     // 2D: prolongation + all half-sweeps (+ y^T r) in one row-marching pass
-    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac && !g.faces;
+    // NEXT(3) variants run the flat kernels: the symmetric two-level preconditioner
+    // (RBS_PRECOND_SYM) and the Polak-Ribiere beta (RBS_BETA_PR)
+    const bool sym = cg && o->precond == RBS_PRECOND_SYM, pr = cg && o->beta_rule == RBS_BETA_PR;
+    const std::vector<int> rseq(seq.rbegin(), seq.rend());     // adjoint sweep: colours reversed
+    const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac && !g.faces && !sym && !pr;
     auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
                      int init) {
         SmoothMarchArgs a{};
@@ -1237,9 +1254,36 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         return 1;
     };
 
+    // symmetric two-level preconditioner y = M^{-1} r (RBS_PRECOND_SYM, NEXT(3)):
+    // y1 = S*(A, r, 0), y2 = y1 + W A_n^{-1} W^T (r - A y1), y = S(A, r, y2) (+ Step 10)
+    auto precond_sym = [&](int init) {
+        int c = 0;
+        k_fill_batch<<<fgrid, 256, 0, st>>>(L.Y, g.N, ctx->N8, Bp, 0, nullptr, 0.0);
+        ++c;
+        c += smooth(L.Y, L.R, 0.0, false, init, &rseq);           // pre: the adjoint sweep from 0
+        if (npad > 0) {
+            c += proj(MODE_RESID, nullptr, true, L.Y, L.R);        // W^T (r - A y1)
+            pb(RBS_K_REDUCE_SOLVE);
+            k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S, init ? 2 : 1);   // e (no stop test)
+            pe();
+            ++c;
+            c += prolong(L.Y, 1);                                  // y2 = y1 + W e
+        }
+        c += smooth(L.Y, L.R, 0.0, true, init);                    // post; Step 10 in the last CTA
+        return c;
+    };
+    // Polak-Ribiere beta (RBS_BETA_PR): r_k kept before Step 7, rho_k before Step 10;
+    // after it beta = (rho_{k+1} - y_{k+1}^T r_k) / rho_k
+    auto pr_fix = [&]() {
+        k_dot_pr<<<nctf, 256, 0, st>>>(L.Y, L.Rold, g.N, Bp, S);
+        k_beta_pr<<<1, 256, 0, st>>>(S, L.rho_prev, nctf);
+        return 2;
+    };
+
     // ---- RBCG Step 2-3: y_0 = RBI(A, r_0, W, 1), rho_0 = r_0^T y_0 ------------
     if (cg) {
-        if (use_march) launches += march(nullptr, L.Y, L.R, 0.0, true, 1);   // + rho_0, PRECOND
+        if (sym) launches += precond_sym(1);
+        else if (use_march) launches += march(nullptr, L.Y, L.R, 0.0, true, 1);   // + rho_0, PRECOND
         else if (jac) {
             double* y0b = (o->sweeps & 1) ? L.T : L.Y;
             launches += prolong(y0b, 0);
@@ -1263,9 +1307,13 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             double* Pold = (it & 1) ? L.P1 : L.P0;
             double* Pnew = (it & 1) ? L.P0 : L.P1;
             c += cgp(Pold, Pnew);             // Step 11 (prev) + A p, Step 5 (alpha) in last CTA
+            if (pr) cudaMemcpyAsync(L.Rold, L.R, (size_t)vecN * 8, cudaMemcpyDeviceToDevice, st);   // r_k
             c += proj(MODE_CG, Pnew, true);   // Steps 6-7, ||r||, W^T r
             pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Step 8
-            if (use_march) {
+            if (pr) cudaMemcpyAsync(L.rho_prev, L.rho, (size_t)Bp * 8, cudaMemcpyDeviceToDevice, st);  // rho_k
+            if (sym) {
+                c += precond_sym(0);                           // Step 9 (two-level) + Step 10
+            } else if (use_march) {
                 c += march(nullptr, L.Y, L.R, 0.0, true, 0);   // Step 9 + Step 10 (last CTA)
             } else if (jac) {
                 double* y0b = (o->sweeps & 1) ? L.T : L.Y;
@@ -1275,6 +1323,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 c += prolong(L.Y, 0);             // Step 9: y0 = W e
                 c += smooth(L.Y, L.R, 0.0, true, 0);  // y = S(A, r, y0); Step 10 in last CTA
             }
+            if (pr) c += pr_fix();
         } else if (use_march) {
             double* Xi = (it & 1) ? L.X2 : L.X;     // ping-pong: the march reads halos of x_old
             double* Xo = (it & 1) ? L.X : L.X2;
@@ -1299,7 +1348,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
              o->tol, o->delta, o->record_history, (void*)ctx->Wi, (void*)st, (void*)L.hist,
              rhs_dev ? 1 : 0, n, npad, ctx->fconst, o->n_active, o->gamma, o->omega,
              o->x_location, (void*)L.theta, (void*)L.partP, (void*)L.partF, (void*)L.ints, (void*)L.X);
-    const std::string key(keybuf);
+    const std::string key = std::string(keybuf) + "|" + std::to_string(o->precond) + "|" +
+                            std::to_string(o->beta_rule) + "|" + std::to_string((uintptr_t)L.Rold);
     if (prof) {
         // eager launches, one iteration at a time, events on the launching stream
         volatile int* hf = ctx->h_flag;

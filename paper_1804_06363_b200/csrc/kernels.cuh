@@ -1072,7 +1072,10 @@ constexpr int kRsThreads = 512;
 constexpr int kRsChunks = 32;     // chunks per row (one warp lane each in the second stage)
 constexpr int kRsPer = 12;        // columns of a chunk loaded together
 
-__global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
+// solve_only = 1: e = A_n^{-1} r_n only -- no stop test, no state change (the coarse
+// correction inside the symmetric two-level preconditioner, RBS_PRECOND_SYM); 2: the
+// same, and e is also reported as a_n (the first application)
+__global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s, int solve_only = 0) {
     if (ld_flag(s.done)) return;
     __shared__ double s_rn[kMaxN + 1];
     __shared__ double s_chunk[(kMaxN + 1) * kRsChunks];
@@ -1124,7 +1127,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             if ((tid & 31) == 0) s_rn[r < s.n ? r : s.npad] = v;
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0 && solve_only) s_go = 1;
+        if (tid == 0 && !solve_only) {
             const double rr2 = s_rn[s.npad];
             const double h = sqrt(rr2) / s.fnorm[b];
             const int it = ld_flag(s.kcount) + 1;
@@ -1147,7 +1151,8 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             if (tid == 0) {
                 int na = s.na[b];
                 const double prev = s_prev;
-                if (s_go && s.gamma > 0.0 && s.method == 1 && na < s.n && prev < s.gamma * s.gamma * s_rn[s.npad])
+                if (!solve_only && s_go && s.gamma > 0.0 && s.method == 1 && na < s.n &&
+                    prev < s.gamma * s.gamma * s_rn[s.npad])
                     ++na;
                 s.na[b] = na;
                 s_na = na;
@@ -1161,6 +1166,10 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
                 if (s_go) warp_chol_solve(Lb, s.npad, na, &z0, &z1, tid);
                 if (tid < s.n) s.E[tid * s.Bp + b] = tid < na ? z0 : 0.0;
                 if (tid + 32 < s.n) s.E[(tid + 32) * s.Bp + b] = tid + 32 < na ? z1 : 0.0;
+                if (solve_only == 2) {                     // first coarse correction
+                    if (tid < s.n) s.a_n[(int64_t)b * s.npad + tid] = tid < na ? z0 : 0.0;
+                    if (tid + 32 < s.n) s.a_n[(int64_t)b * s.npad + tid + 32] = tid + 32 < na ? z1 : 0.0;
+                }
             }
         } else {
         // e = A_n^{-1} r_n: row i by 8 threads (fixed order), frozen lanes get e = 0
@@ -1178,16 +1187,49 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s) {
             double v = 0.0;
             for (int l = 0; l < 8; ++l) v += s_e[tid * 8 + l];
             s.E[tid * s.Bp + b] = v;
+            if (solve_only == 2) s.a_n[(int64_t)b * s.npad + tid] = v;   // first coarse correction
         }
         }
     }
-    if (cta_is_last(s.ticket, &s_last)) {
+    if (!solve_only && cta_is_last(s.ticket, &s_last)) {
         const int any = cta_any_active(s);
         if (threadIdx.x == 0) {
             *(volatile int*)s.done = any ? 0 : 1;
             if (s.method == 0) *(volatile int*)s.kcount = ld_flag(s.kcount) + 1;
         }
         release_ticket(s.ticket);
+    }
+}
+
+// Polak-Ribiere beta (RBS_BETA_PR, NEXT(3)): per-CTA partials of y^T r_old over a
+// contiguous node range (fixed order), part[b][2][nctf] slot 0 ...
+__global__ void __launch_bounds__(256) k_dot_pr(const double* __restrict__ Y, const double* __restrict__ Ro,
+                                                int64_t N, int Bp, SolveState s) {
+    __shared__ double s_p[256];
+    if (ld_flag(s.done)) return;
+    const int tid = threadIdx.x, b = tid % Bp, gsz = 256 / Bp, k = tid / Bp;
+    const int64_t n0 = N * blockIdx.x / gridDim.x, n1 = N * (blockIdx.x + 1) / gridDim.x;
+    double acc = 0.0;
+    for (int64_t i = n0 + k; i < n1; i += gsz) acc = fma(Y[i * Bp + b], Ro[i * Bp + b], acc);
+    s_p[tid] = acc;
+    __syncthreads();
+    if (tid < Bp) {
+        double v = 0.0;
+        for (int u = 0; u < gsz; ++u) v += s_p[u * Bp + tid];
+        s.partF[((int64_t)tid * 2 + 0) * s.nctf + blockIdx.x] = v;
+    }
+}
+
+// ... then one CTA: d = y_{k+1}^T r_k (fixed-order sum of the partials) and
+// beta = (rho_{k+1} - d) / rho_k (the smoother's Step-10 epilogue already set
+// rho = rho_{k+1}; rho_k was saved in rho_prev before it)
+__global__ void __launch_bounds__(256) k_beta_pr(SolveState s, const double* __restrict__ rho_prev, int ncta) {
+    __shared__ double s_buf[256], s_d[kMaxBatch];
+    if (ld_flag(s.done)) return;
+    cta_sum_slot(s, 0, s_buf, s_d, ncta);
+    if (threadIdx.x < s.Bp && s.active[threadIdx.x]) {
+        const int b = threadIdx.x;
+        s.beta[b] = (s.rho[b] - s_d[b]) / rho_prev[b];
     }
 }
 
