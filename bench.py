@@ -355,7 +355,7 @@ def run_c5(a, world, rank, local):
     one-GPU reference solve; N > 1: z-slabs over the ranks (rbs_dist_init; NCCL halos and
     3 small allreduces per iteration).  Basis (offline, untimed): the
     multi-fidelity GPU builder of PAPER.md:310 -- GPU greedy on the 127^3 grid selects the
-    parameters, adaptive snapshots at them on the fine grid (RBS_GREEDY_SAMPLES).  A step =
+    parameters, the fine-grid snapshots at them solved 8 at a time (RBS_GREEDY_SAMPLES_BATCH).  A step =
     one batch of B queries to convergence on all ranks (the whole job: strong scaling)."""
     import torch
     import torch.distributed as dist
@@ -375,7 +375,7 @@ def run_c5(a, world, rank, local):
         del coarse, grc
         torch.cuda.empty_cache()
         fine = rbs.Solver(3, c.m, c.blocks, device=local)
-        gr = fine.build_greedy(sel, c.n, load=False, samples=True)
+        gr = fine.build_greedy(sel, c.n, load=False, samples=True, batched=True)
         W, ANq, fn, n = gr["W"], np.asarray(gr["ANq"]), np.asarray(gr["fn"]), gr["n"]
         snap = [int(x) for x in gr["snap_iters"]]
         del fine

@@ -77,7 +77,9 @@ enum { RBS_MEM_DEVICE = 0, RBS_MEM_HOST = 1 };
  * SAMPLES: adaptive snapshots at the given parameters in list order, no selection -- the
  * fine-grid half of the multi-fidelity approach: select on a coarse grid,
  * then build the fine basis from the selected parameters */
-enum { RBS_GREEDY_PLAIN = 0, RBS_GREEDY_ADAPTIVE = 1, RBS_GREEDY_SAMPLES = 2 };
+/* SAMPLES_BATCH: the same, the samples solved 8 at a time by RBCG with the symmetric two-level
+ * preconditioner on the basis built so far (constant rhs only; DESIGN.md AMB-27) */
+enum { RBS_GREEDY_PLAIN = 0, RBS_GREEDY_ADAPTIVE = 1, RBS_GREEDY_SAMPLES = 2, RBS_GREEDY_SAMPLES_BATCH = 3 };
 
 int rbs_version(void);
 const char* rbs_status_string(rbs_status s);

@@ -21,7 +21,7 @@ _SO = os.path.join(_HERE, "librbs.so")
 RBS_RBI, RBS_RBCG = 0, 1
 RBS_SMOOTH_SYM_RBGS, RBS_SMOOTH_FWD_RBGS, RBS_SMOOTH_JACOBI = 0, 1, 2
 RBS_MEM_DEVICE, RBS_MEM_HOST = 0, 1
-RBS_GREEDY_PLAIN, RBS_GREEDY_ADAPTIVE, RBS_GREEDY_SAMPLES = 0, 1, 2
+RBS_GREEDY_PLAIN, RBS_GREEDY_ADAPTIVE, RBS_GREEDY_SAMPLES, RBS_GREEDY_SAMPLES_BATCH = 0, 1, 2, 3
 RBS_PRECOND_POST, RBS_PRECOND_SYM = 0, 1
 RBS_BETA_FR, RBS_BETA_PR = 0, 1
 QSTATUS = {0: "CONVERGED", 1: "MAXIT", 2: "REDUCED_NOT_SPD", 3: "CURVATURE", 4: "PRECOND",
@@ -491,7 +491,7 @@ class Solver:
         return out
 
     def build_greedy(self, mu_train, n_max, adaptive=True, snapshot_tol=1e-12, drop_tol=1e-10,
-                     stream=None, load=True, phi_train=None, terms=None, samples=False):
+                     stream=None, load=True, phi_train=None, terms=None, samples=False, batched=False):
         """mu_train (nt, P).  Affine right-hand sides: phi_train (nt, R) and terms (R, N).
         samples=True: no selection, adaptive snapshots at mu_train in order (RBS_GREEDY_SAMPLES,
         the fine-grid half of the multi-fidelity approach)."""
@@ -504,7 +504,8 @@ class Solver:
             tdev = terms if torch.is_tensor(terms) else torch.as_tensor(np.ascontiguousarray(terms))
             tdev = tdev.to(device=self.device, dtype=torch.float64).contiguous()
         res = rbs_build_greedy(self.ctx, mu_train, n_max,
-                               RBS_GREEDY_SAMPLES if samples else (RBS_GREEDY_ADAPTIVE if adaptive else RBS_GREEDY_PLAIN),
+                               (RBS_GREEDY_SAMPLES_BATCH if batched else RBS_GREEDY_SAMPLES) if samples else
+                               (RBS_GREEDY_ADAPTIVE if adaptive else RBS_GREEDY_PLAIN),
                                snapshot_tol, drop_tol, Wcol, ws, stream, phi_train, tdev)
         n = res["n"]
         res["W"] = Wcol[:n].t()  # (N, n) view of the column-major result

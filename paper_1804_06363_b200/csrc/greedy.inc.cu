@@ -56,9 +56,10 @@ __global__ void k_store_col(const double* __restrict__ w, double wn, double* __r
 namespace {
 
 constexpr int kDotCtas = 296;
+constexpr int kSnapBatch = 8;   // fine snapshots solved together (RBS_GREEDY_SAMPLES_BATCH)
 
 struct GreedyLayout {
-    double *Wi, *ANq, *Z, *part, *rows, *x, *w, *dpart, *scal, *phi;
+    double *Wi, *ANq, *Z, *part, *rows, *x, *w, *dpart, *scal, *phi, *xb;
     double *tr_theta, *tr_fproj, *tr_L, *tr_E, *tr_a;
     double *tr_d[6];
     int* tr_i[5];
@@ -78,6 +79,7 @@ GreedyLayout greedy_layout(rbs_ctx* c, int nt, int n_max, void* base) {
     L.rows = cv.take<double>((size_t)8 * (npad + 1));
     L.x = cv.take<double>((size_t)c->N8);
     L.w = cv.take<double>((size_t)c->N8);
+    L.xb = cv.take<double>((size_t)kSnapBatch * c->g.N);   // batched fine snapshots (samples mode)
     L.dpart = cv.take<double>(kDotCtas);
     L.scal = cv.take<double>(8);
     L.phi = cv.take<double>(RBS_MAX_R);
@@ -94,7 +96,7 @@ GreedyLayout greedy_layout(rbs_ctx* c, int nt, int n_max, void* base) {
     tmp.ldw = w_ld(npad);
     rbs_solve_opts o;
     rbs_default_opts(&o);
-    L.solve_bytes = solve_layout(&tmp, 1, &o, true, nullptr).bytes;   // rhs buffer: affine snapshots
+    L.solve_bytes = solve_layout(&tmp, kSnapBatch, &o, true, nullptr).bytes;   // rhs buffer: affine snapshots
     L.solve_ws = cv.take<char>(L.solve_bytes);
     L.bytes = cv.off + 256;
     return L;
@@ -128,9 +130,16 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
     if (!ctx->has_op) return fail(ctx, RBS_E_STATE, "set the operator first");
     if (n_train < 1 || n_max < 1 || n_max > RBS_MAX_N) return fail(ctx, RBS_E_DIM, "bad n_train/n_max");
     if (!mu_train || !W_out || !n_out || !workspace) return fail(ctx, RBS_E_ARG, "NULL argument");
-    if (mode != RBS_GREEDY_PLAIN && mode != RBS_GREEDY_ADAPTIVE && mode != RBS_GREEDY_SAMPLES)
+    if (mode != RBS_GREEDY_PLAIN && mode != RBS_GREEDY_ADAPTIVE && mode != RBS_GREEDY_SAMPLES &&
+        mode != RBS_GREEDY_SAMPLES_BATCH)
         return fail(ctx, RBS_E_ARG, "bad mode");
-    const bool from_list = mode == RBS_GREEDY_SAMPLES;   // multi-fidelity fine half
+    // multi-fidelity fine half: the given samples in list order, no selection;
+    // SAMPLES_BATCH solves them kSnapBatch at a time ("solving the PDE N times on a fine
+    // grid"), each batch by RBCG preconditioned with the symmetric two-level RBI on the basis
+    // built so far (AMB-27)
+    const bool batched = mode == RBS_GREEDY_SAMPLES_BATCH;
+    const bool from_list = mode == RBS_GREEDY_SAMPLES || batched;
+    if (batched && R > 0) return fail(ctx, RBS_E_UNSUPPORTED, "batched samples: constant right-hand side only");
     // the greedy works in theta space with its own right-hand side: the context's affine
     // rhs terms and parameter map are dropped (set them again before loading a basis)
     ctx->R = 0;
@@ -178,7 +187,8 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
     rbs_default_opts(&so);
     so.tol = snapshot_tol;
     so.max_iter = 200000;
-    int n = 0, rej = 0, cand = 0, its_first = -1;
+    int n = 0, rej = 0, cand = 0, its_first = -1, chunk0 = -1;
+    int b_its[kSnapBatch] = {0}, b_qs[kSnapBatch] = {0};
     auto dot = [&](const double* a, int64_t sa, const double* b, int64_t sb, double* out) {
         k_dot<<<kDotCtas, 256, 0, st>>>(a, sa, b, sb, g.N, L.dpart);
         k_sum_to<<<1, 32, 0, st>>>(L.dpart, kDotCtas, out);
@@ -196,31 +206,61 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
         // N >= 2 (adaptive): RBCG with W_{N-1}, guarded (AMB-22): not converged
         // within 2*its_1 + 50 -> fall back to SGS-PCG; its < 0.
         int its = 0, qs = 0;
-        so.max_iter = (ctx->n == 0) ? 200000 : 2 * (its_first > 0 ? its_first : 1000) + 50;
-        const double* srhs = nullptr;
-        if (R > 0) {   // f(mu_cand) = sum_r phi_r f_r -> L.Z
-            CK(cudaMemcpyAsync(L.phi, phi_train + (size_t)cand * R, (size_t)R * 8, cudaMemcpyHostToDevice, st));
-            k_affine_rhs<<<grid_for(g.N, 256, ctx->num_sms * 8), 256, 0, st>>>(L.phi, R, terms, g.N, 1, L.Z);
-            CKL();
-            srhs = L.Z;
-        }
-        rbs_status s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, srhs, L.x, &its,
-                                       &qs, nullptr, nullptr, nullptr, nullptr, L.solve_ws,
-                                       L.solve_bytes, stream);
-        if (s != RBS_OK) return s;
-        if (ctx->n == 0 && its_first < 0) its_first = its;
-        if (qs != Q_CONVERGED && ctx->n > 0) {
-            ctx->n = 0;
-            ctx->hfn.clear();
-            ctx->hANq.clear();
-            so.max_iter = 200000;
-            s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, srhs, L.x, &its, &qs,
-                                nullptr, nullptr, nullptr, nullptr, L.solve_ws, L.solve_bytes, stream);
+        const double* xsrc = L.x;
+        if (batched) {
+            if (chunk0 < 0 || cand >= chunk0 + kSnapBatch) {   // the next batch of samples
+                chunk0 = cand;
+                const int cb = std::min(kSnapBatch, nt - cand);
+                rbs_solve_opts sb = so;
+                sb.max_iter = 200000;
+                sb.precond = RBS_PRECOND_SYM;
+                rbs_status s = rbs_solve_batch(ctx, cb, mu_train + (size_t)cand * P, &sb, nullptr, L.xb,
+                                               b_its, b_qs, nullptr, nullptr, nullptr, nullptr, L.solve_ws,
+                                               L.solve_bytes, stream);
+                if (s != RBS_OK) return s;
+            }
+            its = b_its[cand - chunk0];
+            qs = b_qs[cand - chunk0];
+            xsrc = L.xb + (size_t)(cand - chunk0) * g.N;
+            if (qs != Q_CONVERGED) {   // fallback: this snapshot alone by SGS-PCG (its reported < 0)
+                ctx->n = 0;
+                ctx->hfn.clear();
+                ctx->hANq.clear();
+                rbs_solve_opts s1 = so;
+                s1.max_iter = 200000;
+                rbs_status s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &s1, nullptr, L.x, &its, &qs,
+                                               nullptr, nullptr, nullptr, nullptr, L.solve_ws, L.solve_bytes, stream);
+                if (s != RBS_OK) return s;
+                its = -its;
+                xsrc = L.x;
+            }
+        } else {
+            so.max_iter = (ctx->n == 0) ? 200000 : 2 * (its_first > 0 ? its_first : 1000) + 50;
+            const double* srhs = nullptr;
+            if (R > 0) {   // f(mu_cand) = sum_r phi_r f_r -> L.Z
+                CK(cudaMemcpyAsync(L.phi, phi_train + (size_t)cand * R, (size_t)R * 8, cudaMemcpyHostToDevice, st));
+                k_affine_rhs<<<grid_for(g.N, 256, ctx->num_sms * 8), 256, 0, st>>>(L.phi, R, terms, g.N, 1, L.Z);
+                CKL();
+                srhs = L.Z;
+            }
+            rbs_status s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, srhs, L.x, &its,
+                                           &qs, nullptr, nullptr, nullptr, nullptr, L.solve_ws,
+                                           L.solve_bytes, stream);
             if (s != RBS_OK) return s;
-            its = -its;
+            if (ctx->n == 0 && its_first < 0) its_first = its;
+            if (qs != Q_CONVERGED && ctx->n > 0) {
+                ctx->n = 0;
+                ctx->hfn.clear();
+                ctx->hANq.clear();
+                so.max_iter = 200000;
+                s = rbs_solve_batch(ctx, 1, mu_train + (size_t)cand * P, &so, srhs, L.x, &its, &qs,
+                                    nullptr, nullptr, nullptr, nullptr, L.solve_ws, L.solve_bytes, stream);
+                if (s != RBS_OK) return s;
+                its = -its;
+            }
+            // ---- Step 4: W_N = MGS(W_{N-1}, x) ------------------------------------
         }
-        // ---- Step 4: W_N = MGS(W_{N-1}, x) ------------------------------------
-        CK(cudaMemcpyAsync(L.w, L.x, (size_t)g.N * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(L.w, xsrc, (size_t)g.N * 8, cudaMemcpyDeviceToDevice, st));
         dot(L.x, 1, L.x, 1, L.scal + 0);
         for (int pass = 0; pass < 2; ++pass)
             for (int j = 0; j < n; ++j) {

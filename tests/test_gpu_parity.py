@@ -579,6 +579,26 @@ def test_gpu_basis_from_samples_matches_oracle(orc, rbs):
     assert np.abs(res["fn"] - ref["fn"]).max() <= 1e-8 * np.abs(ref["fn"]).max()
 
 
+@pytest.mark.parametrize("dim,m,blocks,n", [(2, 63, (3, 3), 12), (3, 23, (2, 2, 2), 10)])
+def test_gpu_batched_samples_match_oracle(orc, rbs, dim, m, blocks, n):
+    """RBS_GREEDY_SAMPLES_BATCH (AMB-27): the same samples solved 8 at a time (RBCG with the
+    symmetric two-level preconditioner on the basis so far) -- every snapshot is the fine
+    solution to 1e-12, so the basis equals the oracle's or_basis_from_samples (same MGS
+    order) to the snapshot tolerance, and so do the offline blocks."""
+    gc = orc.Grid(dim, 15 if dim == 3 else 31, blocks)
+    tr = 0.1 * 100 ** np.random.default_rng(32).random((60, gc.Q))
+    mus = tr[gc.greedy(tr, n)["selected"]]
+    ref = orc.Grid(dim, m, blocks).basis_from_samples(mus)
+    res = rbs.Solver(dim, m, blocks).build_greedy(mus, n, samples=True, batched=True)
+    assert res["n"] == ref["n"] == n and res["n_rejected"] == 0
+    W = res["W"].cpu().numpy()
+    assert np.abs(W - ref["W"]).max() <= 1e-7
+    sv = np.linalg.svd(W.T @ ref["W"], compute_uv=False)
+    assert sv.min() >= 1 - 1e-10
+    assert np.abs(res["ANq"] - ref["ANq"]).max() <= 1e-7 * np.abs(ref["ANq"]).max()
+    assert np.all(res["snap_iters"] > 0)
+
+
 @pytest.mark.parametrize("dim,m,blocks,n,B", [
     (3, 13, (2, 2, 2), 20, 16),   # Bp 16: two rows per warp in the row-segment passes, k_wtr<16>
     (3, 12, (2, 3, 2), 24, 32),   # Bp 32: one row per warp, k_wtr<32>, ragged segments (12 = 3 x 4)
