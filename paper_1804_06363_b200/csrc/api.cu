@@ -192,6 +192,8 @@ void set_attrs_v2() {
     set_attrs_smooth2<BP, true, 24, 3>();
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_cgp2v<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cgp2v<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_resid2<BP, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -1184,7 +1186,11 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             c2.s = S; c2.done = done;
             const size_t csm = cgp2_smem_bytes(Bp, Q);
             const int gr = c2.part.nsx * c2.part.nsy;
-            if (Bp == 8) k_cgp2<8><<<gr, kMT, csm, st>>>(c2);
+            if (!(v2off & 4096)) {     // two queries per thread (k_cgp2v)
+                if (Bp == 8) k_cgp2v<8><<<gr, kMT, csm, st>>>(c2);
+                else if (Bp == 16) k_cgp2v<16><<<gr, kMT, csm, st>>>(c2);
+                else k_cgp2v<32><<<gr, kMT, csm, st>>>(c2);
+            } else if (Bp == 8) k_cgp2<8><<<gr, kMT, csm, st>>>(c2);
             else if (Bp == 16) k_cgp2<16><<<gr, kMT, csm, st>>>(c2);
             else k_cgp2<32><<<gr, kMT, csm, st>>>(c2);
         } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);

@@ -650,6 +650,193 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
 }
 
 // ===========================================================================
+// k_cgp2v<BP>: k_cgp2 with two queries per thread (16-byte shared / global
+// accesses): the same rows, lags and formulas, half the load / store / address
+// instructions per element (the pass is issue-bound).  The sigma partials of a
+// thread's two queries are kept apart and combined in a fixed order.
+// ===========================================================================
+template <int BP>
+__global__ void __launch_bounds__(kMT, 2) k_cgp2v(CGP2Args a) {
+    if (a.done && ld_flag(a.done)) return;
+    constexpr int HP = BP / 2, LGHP = LgB<BP>::v - 1;
+    constexpr int TW = kC2TX + 2;
+    constexpr int VROW = TW * BP;
+    constexpr int YR = 0, PR = kC2R * VROW, NR = 2 * kC2R * VROW, ST = NR + kC2P * VROW;
+    constexpr int JA = (TW * HP + kMT - 1) / kMT;      // p_new pair slots per thread
+    constexpr int JB = (kC2TX * HP + kMT - 1) / kMT;   // stencil pair slots per thread
+    extern __shared__ __align__(128) double smd[];
+    __shared__ int s_ci[TW], s_cu[TW];
+    __shared__ __align__(8) uint64_t bars[kC2R];
+    __shared__ double s_sig[kMaxBatch];
+    __shared__ int s_last;
+    const int m = a.g.m;
+    const int tid = threadIdx.x;
+    const int sx = blockIdx.x % a.part.nsx, sy = blockIdx.x / a.part.nsx;
+    const int x0 = 1 + sx * kC2TX;
+    const int y0 = 1 + sy * a.part.rows_per_seg;
+    const int y1 = min(m + 1, y0 + a.part.rows_per_seg);
+    const int xlo = x0 - 1;
+    const int Imin = max(1, xlo), Imax = min(m, x0 + kC2TX);
+    const int ncopy = Imax - Imin + 1, coff = Imin - xlo;
+    const int cmin = Imin - xlo, cmax = Imax - xlo;
+    const int nown = min(kC2TX, cmax);
+    const int Jfirst = y0 - 1;
+    const int nform = y1 - y0 + 2;
+    const int nsteps = y1 - y0 + 3;
+
+    for (int t = tid; t < ST; t += kMT) smd[t] = 0.0;
+    for (int t = tid; t < a.g.Q * BP; t += kMT) smd[ST + t] = a.g.scale * a.theta[t];
+    fill_colinfo(a.g, xlo, TW, s_ci, s_cu);
+    if (tid == 0) {
+        for (int k = 0; k < kC2R; ++k) mbar_init(&bars[k], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint32_t vb = (uint32_t)ncopy * BP * 8;
+    auto issue = [&](int u) {
+        const int J = Jfirst + u;
+        const bool in = J >= 1 && J <= m;
+        uint64_t* bar = &bars[u & (kC2R - 1)];
+        fence_async_smem();
+        mbar_expect_tx(bar, in ? 2 * vb : 0u);
+        if (!in) return;
+        const int64_t n0 = (int64_t)(J - 1) * m + (Imin - 1);
+        const int so = (u & (kC2R - 1)) * VROW + coff * BP;
+        bulk_g2s(smd + YR + so, a.Y + n0 * BP, vb, bar);
+        bulk_g2s(smd + PR + so, a.Pold + n0 * BP, vb, bar);
+    };
+    if (tid == 0)
+        for (int u = 0; u < kC2D && u < nform; ++u) issue(u);
+
+    const int h = tid & (HP - 1), b0 = 2 * h;       // this thread's queries b0, b0 + 1
+    const double bet0 = a.beta[b0], bet1 = a.beta[b0 + 1];
+    int oa[JA];
+    bool va[JA], wa[JA];
+#pragma unroll
+    for (int j = 0; j < JA; ++j) {
+        const int pe = tid + cmin * HP + j * kMT;  // pair element of the window row
+        const int col = pe >> LGHP;
+        va[j] = col <= cmax;
+        wa[j] = col >= 1 && col <= nown;
+        oa[j] = va[j] ? col * BP + b0 : 0;
+    }
+    int ob[JB], cub[JB], cib[JB];
+    bool vbq[JB];
+#pragma unroll
+    for (int j = 0; j < JB; ++j) {
+        const int item = (tid >> LGHP) + j * (kMT >> LGHP);
+        vbq[j] = item < nown;
+        const int col = vbq[j] ? item + 1 : 1;
+        ob[j] = col * BP + b0;
+        cub[j] = s_cu[col];
+        cib[j] = s_ci[col];
+    }
+    double sig0 = 0.0, sig1 = 0.0;
+    double* pg = a.Pnew + ((int64_t)(Jfirst - 1) * m + (xlo - 1)) * BP;
+    for (int t = 0; t < nsteps; ++t, pg += (int64_t)m * BP) {
+        const int Jb = Jfirst + t;
+        if (tid == 0 && t + kC2D < nform) issue(t + kC2D);
+        const bool arow = t < nform;
+        if (arow) mbar_wait(&bars[t & (kC2R - 1)], (uint32_t)((t / kC2R) & 1));
+        const bool ain = arow && Jb >= 1 && Jb <= m;
+        const double* ya = smd + YR + (t & (kC2R - 1)) * VROW;
+        const double* pa = smd + PR + (t & (kC2R - 1)) * VROW;
+        double* na = smd + NR + (t & (kC2P - 1)) * VROW;
+        // ---- loads: stage A (row Jb) and stage B (rows Jb-3 .. Jb-1) ---------
+        double2 yv[JA], pv[JA];
+#pragma unroll
+        for (int j = 0; j < JA; ++j) {
+            yv[j] = *reinterpret_cast<const double2*>(ya + oa[j]);
+            pv[j] = *reinterpret_cast<const double2*>(pa + oa[j]);
+        }
+        const int R = Jb - 2;
+        const bool brow = R >= y0 && R < y1;
+        const double* nc = smd + NR + ((t - 2) & (kC2P - 1)) * VROW;
+        const double* nd = smd + NR + ((t - 3) & (kC2P - 1)) * VROW;
+        const double* nu = smd + NR + ((t - 1) & (kC2P - 1)) * VROW;
+        double2 qc[JB], q0[JB], q1[JB], q2[JB], q3[JB];
+#pragma unroll
+        for (int j = 0; j < JB; ++j) {
+            qc[j] = *reinterpret_cast<const double2*>(nc + ob[j]);
+            q0[j] = *reinterpret_cast<const double2*>(nc + ob[j] - BP);
+            q1[j] = *reinterpret_cast<const double2*>(nc + ob[j] + BP);
+            q2[j] = *reinterpret_cast<const double2*>(nd + ob[j]);
+            q3[j] = *reinterpret_cast<const double2*>(nu + ob[j]);
+        }
+        // ---- stage A: p_new = y + beta p_old -----------------------------------
+        if (ain) {
+#pragma unroll
+            for (int j = 0; j < JA; ++j) {
+                const double2 v = make_double2(fma(bet0, pv[j].x, yv[j].x), fma(bet1, pv[j].y, yv[j].y));
+                if (va[j]) *reinterpret_cast<double2*>(na + oa[j]) = v;
+                if (wa[j]) *reinterpret_cast<double2*>(pg + oa[j]) = v;
+            }
+        } else if (arow) {
+            for (int e = tid; e < VROW; e += kMT) na[e] = 0.0;
+        }
+        // ---- stage B: sigma += p_new . (A p_new) on row R ----------------------
+        if (brow) {
+            const int by0 = axis_block(a.g, R - 1, a.g.py) * a.g.px, by1 = axis_block(a.g, R, a.g.py) * a.g.px;
+            const bool rowu = by0 == by1;
+#pragma unroll
+            for (int j = 0; j < JB; ++j) {
+                if (!vbq[j]) continue;
+                double qx, qy;
+                if (rowu && cub[j] >= 0) {
+                    const double2 sc = *reinterpret_cast<const double2*>(smd + ST + (cub[j] + by0) * BP + b0);
+                    qx = stencil_uniform(sc.x, qc[j].x, q0[j].x, q1[j].x, q2[j].x, q3[j].x);
+                    qy = stencil_uniform(sc.y, qc[j].y, q0[j].y, q1[j].y, q2[j].y, q3[j].y);
+                } else {
+                    double kap[4], nb[4] = {q0[j].x, q1[j].x, q2[j].x, q3[j].x};
+                    kappa2_blocks(a.theta, BP, b0, cib[j] & 0xff, cib[j] >> 8, by0, by1, kap);
+                    qx = stencil_apply<2>(a.g, kap, qc[j].x, nb);
+                    double kap1[4], nb1[4] = {q0[j].y, q1[j].y, q2[j].y, q3[j].y};
+                    kappa2_blocks(a.theta, BP, b0 + 1, cib[j] & 0xff, cib[j] >> 8, by0, by1, kap1);
+                    qy = stencil_apply<2>(a.g, kap1, qc[j].y, nb1);
+                }
+                sig0 = fma(qc[j].x, qx, sig0);
+                sig1 = fma(qc[j].y, qy, sig1);
+            }
+        }
+        __syncthreads();
+    }
+    // ---- partials; last CTA: alpha = rho / sigma, MAXIT / CURVATURE (Step 5)
+    // (the rings are dead: the partials go to dynamic shared memory -- two CTAs per SM)
+    SolveState& s = a.s;
+    double* s_a = smd;
+    s_a[2 * tid] = sig0;
+    s_a[2 * tid + 1] = sig1;
+    __syncthreads();
+    if (tid < BP) {
+        const int hh = tid >> 1, k = tid & 1;
+        double t0 = 0.0;
+        for (int u = hh; u < kMT; u += HP) t0 += s_a[2 * u + k];
+        s.partF[((int64_t)tid * 2 + 0) * s.nctf + blockIdx.x] = t0;
+    }
+    if (cta_is_last(s.ticket, &s_last)) {
+        cta_sum_slot(s, 0, s_a, s_sig);
+        const int k = ld_flag(s.kcount);
+        if (tid < s.Bp) {
+            const int bb = tid;
+            double al = 0.0;
+            if (s.active[bb]) {
+                const double sg = s_sig[bb];
+                if (k >= s.maxit) { s.status[bb] = Q_MAXIT; s.its[bb] = k; s.active[bb] = 0; }
+                else if (!(sg > 0.0)) {
+                    s.status[bb] = isfinite(sg) ? Q_CURVATURE : Q_NONFINITE;
+                    s.its[bb] = k;
+                    s.active[bb] = 0;
+                } else al = s.rho[bb] / sg;
+            }
+            s.alpha[bb] = al;
+        }
+        __threadfence();
+        update_done(s);
+        release_ticket(s.ticket);
+    }
+}
+
+// ===========================================================================
 // k_resid2<BP, MODE>: the projection pass as a row march.
 //   MODE 0 (RBCG Steps 6-8): q = A p, x += alpha p,
 //          r -= alpha q (x, r stored), v = r
