@@ -452,6 +452,9 @@ def run_c5(a, world, rank, local):
         ms = float(t.item())
     clk = clocks.stop()
     # e2e: host mu in, X (this rank's owned planes) out to pinned host memory, every step
+    # (one solve workspace at a time: each is ~48 GB at 511^3)
+    s._ws.clear()
+    torch.cuda.empty_cache()
     Xh = torch.empty((c.B, nx), dtype=torch.float64, pin_memory=True)
     s.solve_batch(mus_all[:c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False)
     if world > 1:
@@ -467,6 +470,8 @@ def run_c5(a, world, rank, local):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     prof = None
+    s._ws.clear()
+    torch.cuda.empty_cache()
     if world == 1:
         prof = step(0, profile=1, tol=0.0, max_iter=min(a.profile_iters, 10))["profile"]
     hbm, hbm_src = peaks()

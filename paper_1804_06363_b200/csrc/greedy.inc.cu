@@ -261,7 +261,7 @@ static rbs_status greedy_core(rbs_ctx* ctx, int n_train, const double* mu_train,
             // ---- Step 4: W_N = MGS(W_{N-1}, x) ------------------------------------
         }
         CK(cudaMemcpyAsync(L.w, xsrc, (size_t)g.N * 8, cudaMemcpyDeviceToDevice, st));
-        dot(L.x, 1, L.x, 1, L.scal + 0);
+        dot(L.w, 1, L.w, 1, L.scal + 0);            // ||x|| (w = x before the MGS passes)
         for (int pass = 0; pass < 2; ++pass)
             for (int j = 0; j < n; ++j) {
                 dot(L.Wi + j, ldw, L.w, 1, L.scal + 2);

@@ -5,7 +5,7 @@ timeout 900 python -m pytest tests -m gpu -x -q ${TESTK:+-k "$TESTK"} > gpurun_o
 tail -1 gpurun_out/q_tests.log
 python tools/prof_c2.py --build /tmp/c2basis.pt > gpurun_out/q_build.log 2>&1
 python tools/prof_c2.py --load /tmp/c2basis.pt --iters 30 | tee gpurun_out/q_v3.log
-RBS_DISABLE_V2=2048 python tools/prof_c2.py --load /tmp/c2basis.pt --iters 30 | tee gpurun_out/q_v2.log
+RBS_DISABLE_V2=${AB:-4096} python tools/prof_c2.py --load /tmp/c2basis.pt --iters 30 | tee gpurun_out/q_v2.log
 if [ -n "$NCU" ]; then
   ncu --set full --clock-control none --import-source on -k regex:${NCUK:-k_smooth2} -c 1 -o /tmp/q_s3 -f python tools/prof_c2.py --load /tmp/c2basis.pt --iters 2 > gpurun_out/q_ncu.log 2>&1
   python tools/ncu_brief.py /tmp/q_s3.ncu-rep > gpurun_out/q_ncu_brief.txt 2>&1
