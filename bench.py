@@ -378,7 +378,7 @@ def run_c5(a, world, rank, local):
         gr = fine.build_greedy(sel, c.n, load=False, samples=True, batched=True)
         W, ANq, fn, n = gr["W"], np.asarray(gr["ANq"]), np.asarray(gr["fn"]), gr["n"]
         snap = [int(x) for x in gr["snap_iters"]]
-        del fine
+        del fine, gr        # the builder's workspace and its references to W
         torch.cuda.empty_cache()
     if world > 1:
         meta = torch.tensor([n], device=dev)
