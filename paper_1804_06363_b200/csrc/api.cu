@@ -192,16 +192,10 @@ void set_attrs_v2() {
     set_attrs_smooth2<BP, true, 24, 3>();
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_cgp2<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(k_cgp2v<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_cgp2v<BP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_resid2<BP, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_resid2<BP, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_resid2v<BP, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_resid2v<BP, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_resid2v<BP, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_resid2v<BP, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 template <int BP, bool R, int TX, int WR>
 void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
@@ -235,11 +229,8 @@ void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, cons
     }
 }
 template <int BP, int PF>
-void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r, int v2off) {
-    if (!(v2off & 8192)) {     // two queries per thread in stage A (k_resid2v)
-        if (md == 0) k_resid2v<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
-        else k_resid2v<BP, 1, PF><<<grid, kMT, smem, st>>>(r);
-    } else if (md == 0) k_resid2<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
+void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r) {
+    if (md == 0) k_resid2<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
     else k_resid2<BP, 1, PF><<<grid, kMT, smem, st>>>(r);
 }
 
@@ -1134,14 +1125,14 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 if (md == 0) k_resid_march<0><<<nct, kMarchThreads, rs1.total, st>>>(r);
                 else k_resid_march<1><<<nct, kMarchThreads, rs1.total, st>>>(r);
             } else if (Bp == 8) {
-                if (PF == 2) launch_resid2<8, 2>(md, nct, rsm, st, r, v2off);
-                else launch_resid2<8, 1>(md, nct, rsm, st, r, v2off);
+                if (PF == 2) launch_resid2<8, 2>(md, nct, rsm, st, r);
+                else launch_resid2<8, 1>(md, nct, rsm, st, r);
             } else if (Bp == 16) {
-                if (PF == 2) launch_resid2<16, 2>(md, nct, rsm, st, r, v2off);
-                else launch_resid2<16, 1>(md, nct, rsm, st, r, v2off);
+                if (PF == 2) launch_resid2<16, 2>(md, nct, rsm, st, r);
+                else launch_resid2<16, 1>(md, nct, rsm, st, r);
             } else {
-                if (PF == 2) launch_resid2<32, 2>(md, nct, rsm, st, r, v2off);
-                else launch_resid2<32, 1>(md, nct, rsm, st, r, v2off);
+                if (PF == 2) launch_resid2<32, 2>(md, nct, rsm, st, r);
+                else launch_resid2<32, 1>(md, nct, rsm, st, r);
             }
             pe();
             return 1;
@@ -1196,11 +1187,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             c2.s = S; c2.done = done;
             const size_t csm = cgp2_smem_bytes(Bp, Q);
             const int gr = c2.part.nsx * c2.part.nsy;
-            if (!(v2off & 4096)) {     // two queries per thread (k_cgp2v)
-                if (Bp == 8) k_cgp2v<8><<<gr, kMT, csm, st>>>(c2);
-                else if (Bp == 16) k_cgp2v<16><<<gr, kMT, csm, st>>>(c2);
-                else k_cgp2v<32><<<gr, kMT, csm, st>>>(c2);
-            } else if (Bp == 8) k_cgp2<8><<<gr, kMT, csm, st>>>(c2);
+            if (Bp == 8) k_cgp2<8><<<gr, kMT, csm, st>>>(c2);
             else if (Bp == 16) k_cgp2<16><<<gr, kMT, csm, st>>>(c2);
             else k_cgp2<32><<<gr, kMT, csm, st>>>(c2);
         } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);

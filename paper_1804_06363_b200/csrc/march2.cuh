@@ -650,193 +650,6 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
 }
 
 // ===========================================================================
-// k_cgp2v<BP>: k_cgp2 with two queries per thread (16-byte shared / global
-// accesses): the same rows, lags and formulas, half the load / store / address
-// instructions per element (the pass is issue-bound).  The sigma partials of a
-// thread's two queries are kept apart and combined in a fixed order.
-// ===========================================================================
-template <int BP>
-__global__ void __launch_bounds__(kMT, 2) k_cgp2v(CGP2Args a) {
-    if (a.done && ld_flag(a.done)) return;
-    constexpr int HP = BP / 2, LGHP = LgB<BP>::v - 1;
-    constexpr int TW = kC2TX + 2;
-    constexpr int VROW = TW * BP;
-    constexpr int YR = 0, PR = kC2R * VROW, NR = 2 * kC2R * VROW, ST = NR + kC2P * VROW;
-    constexpr int JA = (TW * HP + kMT - 1) / kMT;      // p_new pair slots per thread
-    constexpr int JB = (kC2TX * HP + kMT - 1) / kMT;   // stencil pair slots per thread
-    extern __shared__ __align__(128) double smd[];
-    __shared__ int s_ci[TW], s_cu[TW];
-    __shared__ __align__(8) uint64_t bars[kC2R];
-    __shared__ double s_sig[kMaxBatch];
-    __shared__ int s_last;
-    const int m = a.g.m;
-    const int tid = threadIdx.x;
-    const int sx = blockIdx.x % a.part.nsx, sy = blockIdx.x / a.part.nsx;
-    const int x0 = 1 + sx * kC2TX;
-    const int y0 = 1 + sy * a.part.rows_per_seg;
-    const int y1 = min(m + 1, y0 + a.part.rows_per_seg);
-    const int xlo = x0 - 1;
-    const int Imin = max(1, xlo), Imax = min(m, x0 + kC2TX);
-    const int ncopy = Imax - Imin + 1, coff = Imin - xlo;
-    const int cmin = Imin - xlo, cmax = Imax - xlo;
-    const int nown = min(kC2TX, cmax);
-    const int Jfirst = y0 - 1;
-    const int nform = y1 - y0 + 2;
-    const int nsteps = y1 - y0 + 3;
-
-    for (int t = tid; t < ST; t += kMT) smd[t] = 0.0;
-    for (int t = tid; t < a.g.Q * BP; t += kMT) smd[ST + t] = a.g.scale * a.theta[t];
-    fill_colinfo(a.g, xlo, TW, s_ci, s_cu);
-    if (tid == 0) {
-        for (int k = 0; k < kC2R; ++k) mbar_init(&bars[k], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    const uint32_t vb = (uint32_t)ncopy * BP * 8;
-    auto issue = [&](int u) {
-        const int J = Jfirst + u;
-        const bool in = J >= 1 && J <= m;
-        uint64_t* bar = &bars[u & (kC2R - 1)];
-        fence_async_smem();
-        mbar_expect_tx(bar, in ? 2 * vb : 0u);
-        if (!in) return;
-        const int64_t n0 = (int64_t)(J - 1) * m + (Imin - 1);
-        const int so = (u & (kC2R - 1)) * VROW + coff * BP;
-        bulk_g2s(smd + YR + so, a.Y + n0 * BP, vb, bar);
-        bulk_g2s(smd + PR + so, a.Pold + n0 * BP, vb, bar);
-    };
-    if (tid == 0)
-        for (int u = 0; u < kC2D && u < nform; ++u) issue(u);
-
-    const int h = tid & (HP - 1), b0 = 2 * h;       // this thread's queries b0, b0 + 1
-    const double bet0 = a.beta[b0], bet1 = a.beta[b0 + 1];
-    int oa[JA];
-    bool va[JA], wa[JA];
-#pragma unroll
-    for (int j = 0; j < JA; ++j) {
-        const int pe = tid + cmin * HP + j * kMT;  // pair element of the window row
-        const int col = pe >> LGHP;
-        va[j] = col <= cmax;
-        wa[j] = col >= 1 && col <= nown;
-        oa[j] = va[j] ? col * BP + b0 : 0;
-    }
-    int ob[JB], cub[JB], cib[JB];
-    bool vbq[JB];
-#pragma unroll
-    for (int j = 0; j < JB; ++j) {
-        const int item = (tid >> LGHP) + j * (kMT >> LGHP);
-        vbq[j] = item < nown;
-        const int col = vbq[j] ? item + 1 : 1;
-        ob[j] = col * BP + b0;
-        cub[j] = s_cu[col];
-        cib[j] = s_ci[col];
-    }
-    double sig0 = 0.0, sig1 = 0.0;
-    double* pg = a.Pnew + ((int64_t)(Jfirst - 1) * m + (xlo - 1)) * BP;
-    for (int t = 0; t < nsteps; ++t, pg += (int64_t)m * BP) {
-        const int Jb = Jfirst + t;
-        if (tid == 0 && t + kC2D < nform) issue(t + kC2D);
-        const bool arow = t < nform;
-        if (arow) mbar_wait(&bars[t & (kC2R - 1)], (uint32_t)((t / kC2R) & 1));
-        const bool ain = arow && Jb >= 1 && Jb <= m;
-        const double* ya = smd + YR + (t & (kC2R - 1)) * VROW;
-        const double* pa = smd + PR + (t & (kC2R - 1)) * VROW;
-        double* na = smd + NR + (t & (kC2P - 1)) * VROW;
-        // ---- loads: stage A (row Jb) and stage B (rows Jb-3 .. Jb-1) ---------
-        double2 yv[JA], pv[JA];
-#pragma unroll
-        for (int j = 0; j < JA; ++j) {
-            yv[j] = *reinterpret_cast<const double2*>(ya + oa[j]);
-            pv[j] = *reinterpret_cast<const double2*>(pa + oa[j]);
-        }
-        const int R = Jb - 2;
-        const bool brow = R >= y0 && R < y1;
-        const double* nc = smd + NR + ((t - 2) & (kC2P - 1)) * VROW;
-        const double* nd = smd + NR + ((t - 3) & (kC2P - 1)) * VROW;
-        const double* nu = smd + NR + ((t - 1) & (kC2P - 1)) * VROW;
-        double2 qc[JB], q0[JB], q1[JB], q2[JB], q3[JB];
-#pragma unroll
-        for (int j = 0; j < JB; ++j) {
-            qc[j] = *reinterpret_cast<const double2*>(nc + ob[j]);
-            q0[j] = *reinterpret_cast<const double2*>(nc + ob[j] - BP);
-            q1[j] = *reinterpret_cast<const double2*>(nc + ob[j] + BP);
-            q2[j] = *reinterpret_cast<const double2*>(nd + ob[j]);
-            q3[j] = *reinterpret_cast<const double2*>(nu + ob[j]);
-        }
-        // ---- stage A: p_new = y + beta p_old -----------------------------------
-        if (ain) {
-#pragma unroll
-            for (int j = 0; j < JA; ++j) {
-                const double2 v = make_double2(fma(bet0, pv[j].x, yv[j].x), fma(bet1, pv[j].y, yv[j].y));
-                if (va[j]) *reinterpret_cast<double2*>(na + oa[j]) = v;
-                if (wa[j]) *reinterpret_cast<double2*>(pg + oa[j]) = v;
-            }
-        } else if (arow) {
-            for (int e = tid; e < VROW; e += kMT) na[e] = 0.0;
-        }
-        // ---- stage B: sigma += p_new . (A p_new) on row R ----------------------
-        if (brow) {
-            const int by0 = axis_block(a.g, R - 1, a.g.py) * a.g.px, by1 = axis_block(a.g, R, a.g.py) * a.g.px;
-            const bool rowu = by0 == by1;
-#pragma unroll
-            for (int j = 0; j < JB; ++j) {
-                if (!vbq[j]) continue;
-                double qx, qy;
-                if (rowu && cub[j] >= 0) {
-                    const double2 sc = *reinterpret_cast<const double2*>(smd + ST + (cub[j] + by0) * BP + b0);
-                    qx = stencil_uniform(sc.x, qc[j].x, q0[j].x, q1[j].x, q2[j].x, q3[j].x);
-                    qy = stencil_uniform(sc.y, qc[j].y, q0[j].y, q1[j].y, q2[j].y, q3[j].y);
-                } else {
-                    double kap[4], nb[4] = {q0[j].x, q1[j].x, q2[j].x, q3[j].x};
-                    kappa2_blocks(a.theta, BP, b0, cib[j] & 0xff, cib[j] >> 8, by0, by1, kap);
-                    qx = stencil_apply<2>(a.g, kap, qc[j].x, nb);
-                    double kap1[4], nb1[4] = {q0[j].y, q1[j].y, q2[j].y, q3[j].y};
-                    kappa2_blocks(a.theta, BP, b0 + 1, cib[j] & 0xff, cib[j] >> 8, by0, by1, kap1);
-                    qy = stencil_apply<2>(a.g, kap1, qc[j].y, nb1);
-                }
-                sig0 = fma(qc[j].x, qx, sig0);
-                sig1 = fma(qc[j].y, qy, sig1);
-            }
-        }
-        __syncthreads();
-    }
-    // ---- partials; last CTA: alpha = rho / sigma, MAXIT / CURVATURE (Step 5)
-    // (the rings are dead: the partials go to dynamic shared memory -- two CTAs per SM)
-    SolveState& s = a.s;
-    double* s_a = smd;
-    s_a[2 * tid] = sig0;
-    s_a[2 * tid + 1] = sig1;
-    __syncthreads();
-    if (tid < BP) {
-        const int hh = tid >> 1, k = tid & 1;
-        double t0 = 0.0;
-        for (int u = hh; u < kMT; u += HP) t0 += s_a[2 * u + k];
-        s.partF[((int64_t)tid * 2 + 0) * s.nctf + blockIdx.x] = t0;
-    }
-    if (cta_is_last(s.ticket, &s_last)) {
-        cta_sum_slot(s, 0, s_a, s_sig);
-        const int k = ld_flag(s.kcount);
-        if (tid < s.Bp) {
-            const int bb = tid;
-            double al = 0.0;
-            if (s.active[bb]) {
-                const double sg = s_sig[bb];
-                if (k >= s.maxit) { s.status[bb] = Q_MAXIT; s.its[bb] = k; s.active[bb] = 0; }
-                else if (!(sg > 0.0)) {
-                    s.status[bb] = isfinite(sg) ? Q_CURVATURE : Q_NONFINITE;
-                    s.its[bb] = k;
-                    s.active[bb] = 0;
-                } else al = s.rho[bb] / sg;
-            }
-            s.alpha[bb] = al;
-        }
-        __threadfence();
-        update_done(s);
-        release_ticket(s.ticket);
-    }
-}
-
-// ===========================================================================
 // k_resid2<BP, MODE>: the projection pass as a row march.
 //   MODE 0 (RBCG Steps 6-8): q = A p, x += alpha p,
 //          r -= alpha q (x, r stored), v = r
@@ -1085,254 +898,6 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
     if (tid < BP) {
         double v = 0.0;
         for (int u = tid; u < kMT; u += BP) v += s_rr[u];
-        a.part[((int64_t)tid * (npad + 1) + npad) * a.nct + blockIdx.x] = v;
-    }
-}
-
-// k_resid2v: k_resid2 with two queries per thread in stage A (16-byte shared /
-// global accesses, frozen lanes stored per lane); stage B (DMMA W^T v) unchanged
-template <int BP, int MODE, int kR2PF>
-__global__ void __launch_bounds__(kMT, 1) k_resid2v(ResidMarchArgs a) {
-    constexpr int kR2NS = 3 + kR2PF;     // stencil-input / W ring rows
-    constexpr int kR2NC = 2 + kR2PF;     // x / r / f ring rows
-    if (a.done && ld_flag(a.done)) return;
-    constexpr int LGB = LgB<BP>::v;
-    constexpr int BPV = BP + 4;
-    constexpr int NBT = BP / 8, LGNBT = LGB - 3;
-    constexpr int ROW1 = (kRmTX + 2) * BP, ROW0 = kRmTX * BP;
-    constexpr int SR = 0, XR = kR2NS * ROW1, RRg = XR + kR2NC * ROW0, VN = RRg + kR2NC * ROW0;
-    constexpr int WR = VN + 2 * kRmTX * BPV;
-    constexpr int HP = BP / 2, LGHP = LGB - 1;
-    constexpr int JA = (kRmTX * HP + kMT - 1) / kMT;   // stage-A pair slots per thread
-    extern __shared__ __align__(128) double smd[];
-    __shared__ int s_ci[kRmTX + 2], s_cu[kRmTX + 2];
-    __shared__ __align__(8) uint64_t bars[kR2PF + 1];
-    __shared__ int s_act[kMaxBatch];
-    __shared__ double s_alpha[kMaxBatch];
-    const int npad = a.npad, ldw = a.ldw, m = a.g.m;
-    const bool has_v = a.V != nullptr;
-    const int tid = threadIdx.x;
-    const int sx = blockIdx.x % a.mp.nsx, sy = blockIdx.x / a.mp.nsx;
-    const int x0 = 1 + sx * kRmTX;
-    const int y0 = 1 + sy * a.mp.rows_per_seg;
-    const int y1 = min(m + 1, y0 + a.mp.rows_per_seg);
-    const int xlo = x0 - 1;
-    const int Imin = max(1, xlo), Imax = min(m, x0 + kRmTX);
-    const int nc = min(kRmTX, m - x0 + 1);
-    const int ncs = Imax - Imin + 1, coffs = Imin - xlo;
-    const int Jbase = y0 - 1;
-    const int nsteps = (y1 - y0) + 2;
-    const int WROWD = kRmTX * ldw;
-    const int STo = WR + kR2NS * WROWD;
-
-    for (int t = tid; t < STo; t += kMT) smd[t] = 0.0;
-    for (int t = tid; t < a.g.Q * BP; t += kMT) smd[STo + t] = a.g.scale * a.theta[t];
-    for (int t = tid; t < BP; t += kMT) {
-        s_act[t] = a.active ? a.active[t] : 1;
-        s_alpha[t] = MODE == 0 ? a.alpha[t] : 0.0;
-    }
-    fill_colinfo(a.g, xlo, kRmTX + 2, s_ci, s_cu);
-    if (tid == 0) {
-        for (int k = 0; k <= kR2PF; ++k) mbar_init(&bars[k], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-
-    const double* Sin = MODE == 0 ? a.P : a.X;
-    auto issue = [&](int u) {
-        const int J = Jbase + u;
-        uint64_t* bar = &bars[u % (kR2PF + 1)];
-        const bool srow = J >= 1 && J <= m;
-        const bool crow = J >= y0 && J < y1;
-        const uint32_t sb = (uint32_t)ncs * BP * 8, cb = (uint32_t)nc * BP * 8, wb = (uint32_t)nc * ldw * 8;
-        uint32_t bytes = 0;
-        if (srow) bytes += sb;
-        if (crow) bytes += wb + (MODE == 0 ? 2 * cb : (has_v ? cb : 0u));
-        fence_async_smem();
-        mbar_expect_tx(bar, bytes);
-        if (srow) {
-            const int64_t n0 = (int64_t)(J - 1) * m + (Imin - 1);
-            bulk_g2s(smd + SR + (u % kR2NS) * ROW1 + coffs * BP, Sin + n0 * BP, sb, bar);
-        }
-        if (crow) {
-            const int64_t n0 = (int64_t)(J - 1) * m + (x0 - 1);
-            const int cs = u % kR2NC;
-            bulk_g2s(smd + WR + (u % kR2NS) * WROWD, a.W + n0 * ldw, wb, bar);
-            if (MODE == 0) {
-                bulk_g2s(smd + XR + cs * ROW0, a.X + n0 * BP, cb, bar);
-                bulk_g2s(smd + RRg + cs * ROW0, a.R + n0 * BP, cb, bar);
-            } else if (has_v) {
-                bulk_g2s(smd + RRg + cs * ROW0, a.V + n0 * BP, cb, bar);
-            }
-        }
-    };
-    if (tid == 0)
-        for (int u = 0; u <= kR2PF && u < nsteps; ++u) issue(u);
-
-    const int warp = tid >> 5, lane = tid & 31;
-    const int h = tid & (HP - 1), b = 2 * h;       // this thread's queries b, b + 1
-    const bool qact0 = s_act[b] != 0, qact1 = s_act[b + 1] != 0;
-    const double al0 = s_alpha[b], al1 = s_alpha[b + 1];
-    const double vconst = a.vconst;
-    // DMMA tasks (pair = (j-tile, b-tile), k-quarter of the 32-node row), contiguous per warp
-    const int npairs = (npad >> 3) * NBT;
-    const int ntask = npairs * 4;
-    const int ntpw = (ntask + kNW - 1) / kNW;
-    const int t0 = warp * ntpw;
-    const int myn = max(0, min(ntpw, ntask - t0));
-    int wofs[8], vofs[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int task = t0 + k;
-        const int pr = task >> 2, kq = task & 3;
-        const int btt = pr & (NBT - 1), jt = pr >> LGNBT;
-        wofs[k] = (kq * 8 + (lane & 3)) * ldw + jt * 8 + (lane >> 2);
-        vofs[k] = VN + (kq * 8 + (lane & 3)) * BPV + btt * 8 + (lane >> 2);
-    }
-    double acc[8][2];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k][0] = acc[k][1] = 0.0;
-    // stage-A slots (loop-invariant): owned column c, its block info
-    int oc[JA], ocu[JA], oci[JA];
-    bool ov_[JA];
-#pragma unroll
-    for (int j = 0; j < JA; ++j) {
-        const int c = (tid >> LGHP) + j * (kMT >> LGHP);
-        ov_[j] = c < nc;
-        oc[j] = ov_[j] ? c : 0;
-        ocu[j] = s_cu[oc[j] + 1];
-        oci[j] = s_ci[oc[j] + 1];
-    }
-    const uint32_t sbase = smem_u32(smd);
-    double rr0 = 0.0, rr1 = 0.0;
-    int sl_c = 0, sl_n = 1, sl_d = kR2NS - 1;    // ring slots of rows J, J+1, J-1 (mod NS)
-    int sl_x = 0;                                // ring slot of row J (mod NC)
-    double* xg = a.X + ((int64_t)(Jbase - 1) * m + (x0 - 1)) * BP + b;
-    double* rg = a.R + ((int64_t)(Jbase - 1) * m + (x0 - 1)) * BP + b;
-    const double* smc = smd;
-
-    for (int t = 0; t < nsteps; ++t, xg += (int64_t)m * BP, rg += (int64_t)m * BP) {
-        const int J = Jbase + t;
-        if (t == 0) mbar_wait(&bars[0], 0u);
-        if (tid == 0 && t + kR2PF + 1 < nsteps) issue(t + kR2PF + 1);
-        if (t + 1 < nsteps) mbar_wait(&bars[(t + 1) % (kR2PF + 1)], (uint32_t)(((t + 1) / (kR2PF + 1)) & 1));
-        if (t + 1 < nsteps && (J + 1 < 1 || J + 1 > m)) {
-            const int z = SR + sl_n * ROW1;
-            for (int e = tid; e < ROW1; e += kMT) smd[z + e] = 0.0;
-            __syncthreads();
-        }
-        // ---- stage A loads: row J -------------------------------------------------
-        const bool arow = J >= y0 && J < y1;
-        const int sc = SR + sl_c * ROW1 + BP + b, sd = SR + sl_d * ROW1 + BP + b;
-        const int su = SR + sl_n * ROW1 + BP + b;
-        const int xs = XR + sl_x * ROW0 + b, rs = RRg + sl_x * ROW0 + b;
-        double2 pc[JA], q0[JA], q1[JA], q2[JA], q3[JA], xa[JA], ra[JA];
-#pragma unroll
-        for (int j = 0; j < JA; ++j) {
-            const int o = oc[j] * BP;
-            pc[j] = *reinterpret_cast<const double2*>(smc + sc + o);
-            q0[j] = *reinterpret_cast<const double2*>(smc + sc + o - BP);
-            q1[j] = *reinterpret_cast<const double2*>(smc + sc + o + BP);
-            q2[j] = *reinterpret_cast<const double2*>(smc + sd + o);
-            q3[j] = *reinterpret_cast<const double2*>(smc + su + o);
-            if (MODE == 0) {
-                xa[j] = *reinterpret_cast<const double2*>(smc + xs + o);
-                ra[j] = *reinterpret_cast<const double2*>(smc + rs + o);
-            } else {
-                ra[j] = has_v ? *reinterpret_cast<const double2*>(smc + rs + o) : make_double2(vconst, vconst);
-            }
-        }
-        // ---- stage B: W^T v on row J-1 (DMMA) -----------------------------------
-        const int JB = J - 1;
-        if (JB >= y0 && JB < y1) {
-            const int vB = ((t + 1) & 1) * kRmTX * BPV;
-            const int Ws = WR + sl_d * WROWD;
-            const uint32_t WsA = sbase + 8u * Ws, vBA = sbase + 8u * vB;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (k >= myn) break;
-                const uint32_t wa = WsA + 8u * wofs[k], vb = vBA + 8u * vofs[k];
-                const double a0 = ldsd(wa), b0 = ldsd(vb), a1 = ldsd(wa + 32u * ldw), b1 = ldsd(vb + 32u * BPV);
-                dmma_8x8x4(acc[k][0], acc[k][1], a0, b0);
-                dmma_8x8x4(acc[k][0], acc[k][1], a1, b1);
-            }
-        }
-        // ---- stage A compute / stores (two queries per thread) --------------------
-        if (arow) {
-            const int vA = VN + (t & 1) * kRmTX * BPV + b;
-            const int by0 = axis_block(a.g, J - 1, a.g.py) * a.g.px, by1 = axis_block(a.g, J, a.g.py) * a.g.px;
-            const bool rowu = by0 == by1;
-#pragma unroll
-            for (int j = 0; j < JA; ++j) {
-                if (!ov_[j]) continue;
-                const int o = oc[j] * BP;
-                double qx, qy;
-                if (rowu && ocu[j] >= 0) {
-                    const double2 sct = *reinterpret_cast<const double2*>(smc + STo + (ocu[j] + by0) * BP + b);
-                    qx = stencil_uniform(sct.x, pc[j].x, q0[j].x, q1[j].x, q2[j].x, q3[j].x);
-                    qy = stencil_uniform(sct.y, pc[j].y, q0[j].y, q1[j].y, q2[j].y, q3[j].y);
-                } else {
-                    double kap[4], nb[4] = {q0[j].x, q1[j].x, q2[j].x, q3[j].x};
-                    kappa2_blocks(a.theta, BP, b, oci[j] & 0xff, oci[j] >> 8, by0, by1, kap);
-                    qx = stencil_apply<2>(a.g, kap, pc[j].x, nb);
-                    double kap1[4], nb1[4] = {q0[j].y, q1[j].y, q2[j].y, q3[j].y};
-                    kappa2_blocks(a.theta, BP, b + 1, oci[j] & 0xff, oci[j] >> 8, by0, by1, kap1);
-                    qy = stencil_apply<2>(a.g, kap1, pc[j].y, nb1);
-                }
-                double v0 = 0.0, v1 = 0.0;
-                if (MODE == 0) {
-                    const double x0v = fma(al0, pc[j].x, xa[j].x), x1v = fma(al1, pc[j].y, xa[j].y);
-                    const double r0v = fma(-al0, qx, ra[j].x), r1v = fma(-al1, qy, ra[j].y);
-                    if (qact0 && qact1) {     // frozen lanes keep their values bitwise
-                        *reinterpret_cast<double2*>(xg + o) = make_double2(x0v, x1v);
-                        *reinterpret_cast<double2*>(rg + o) = make_double2(r0v, r1v);
-                    } else {
-                        if (qact0) { xg[o] = x0v; rg[o] = r0v; }
-                        if (qact1) { xg[o + 1] = x1v; rg[o + 1] = r1v; }
-                    }
-                    v0 = qact0 ? r0v : 0.0;
-                    v1 = qact1 ? r1v : 0.0;
-                } else {
-                    v0 = qact0 ? ra[j].x - qx : 0.0;
-                    v1 = qact1 ? ra[j].y - qy : 0.0;
-                }
-                rr0 = fma(v0, v0, rr0);
-                rr1 = fma(v1, v1, rr1);
-                *reinterpret_cast<double2*>(smd + vA + oc[j] * BPV) = make_double2(v0, v1);
-            }
-        }
-        __syncthreads();
-        sl_d = sl_c;
-        sl_c = sl_n;
-        sl_n = sl_n + 1 == kR2NS ? 0 : sl_n + 1;
-        sl_x = sl_x + 1 == kR2NC ? 0 : sl_x + 1;
-    }
-    // ---- per-CTA partials: the 4 k-quarters of each (j-tile, b-tile) in order
-    double* s_q = smd;          // rings are dead: [ntask][64]
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (k >= myn) break;
-        const int task = t0 + k;
-        s_q[task * 64 + 2 * lane] = acc[k][0];
-        s_q[task * 64 + 2 * lane + 1] = acc[k][1];
-    }
-    double* s_rr = smd + ntask * 64;      // after the k-quarter tiles (rings are dead)
-    s_rr[2 * tid] = rr0;
-    s_rr[2 * tid + 1] = rr1;
-    __syncthreads();
-    for (int idx = tid; idx < npairs * 64; idx += kMT) {
-        const int pr = idx >> 6, w = idx & 63;            // w = 2*lane + h
-        const double v = ((s_q[(pr * 4 + 0) * 64 + w] + s_q[(pr * 4 + 1) * 64 + w]) +
-                          s_q[(pr * 4 + 2) * 64 + w]) + s_q[(pr * 4 + 3) * 64 + w];
-        const int ln = w >> 1, h = w & 1;
-        const int btt = pr & (NBT - 1), jt = pr >> LGNBT;
-        const int j = jt * 8 + (ln >> 2), bb = btt * 8 + 2 * (ln & 3) + h;
-        a.part[((int64_t)bb * (npad + 1) + j) * a.nct + blockIdx.x] = v;
-    }
-    if (tid < BP) {
-        const int hh = tid >> 1, k = tid & 1;
-        double v = 0.0;
-        for (int u = hh; u < kMT; u += HP) v += s_rr[2 * u + k];
         a.part[((int64_t)tid * (npad + 1) + npad) * a.nct + blockIdx.x] = v;
     }
 }
