@@ -25,7 +25,11 @@
  *  - Batched vectors at the boundary are query-major [B][N] fp64.  The
  *    internal layout is node-major [N][B_pad] (lane = query); the library
  *    transposes on entry/exit.
- *  - Not thread-safe: one context per device and per host thread.
+ *  - A context is not thread-safe: use one context per host thread.  Several
+ *    contexts may share a device (each owns its storage and workspace, e.g.
+ *    bench.py's concurrent batch streams); the library keeps no mutable
+ *    process-global state (kernel attributes are set once per device under a
+ *    lock at rbs_create).
  */
 #ifndef RBS_H
 #define RBS_H
