@@ -376,7 +376,32 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
             a.W = q.W; a.theta = L.theta; a.active = L.active; a.alpha = L.alpha;
             a.P = (it & 1) ? q.P0 : q.P1; a.X = q.X; a.R = q.R; a.V = nullptr; a.vconst = ctx->fconst;
             a.part = L.partP; a.done = done; a.col0 = q.colP;
-            launch_proj<MODE_CG>(q.g, q.nct, psm, st, a);
+            const int ch = wtr_smem_bytes(Bp, ctx->ldw, 64) <= (size_t)110 * 1024 ? 64 : 32;
+            const size_t wsm = wtr_smem_bytes(Bp, ctx->ldw, ch);
+            if (Bp <= 32 && !q.g.faces && wsm <= (size_t)110 * 1024 && npad > 0 && npad <= 64) {
+                // the unpartitioned path's pair (§7): x, r updated in row segments on the
+                // stored planes (ghost values are refreshed by the r halo), then W^T r and
+                // ||r||^2 streamed over the OWNED planes only
+                const int lgBs = ilog2(Bp);
+                k_xr3r<4, false><<<q.nctf, kFlat, fsm, st>>>(a, lgBs);
+                ProjArgs b2 = a;
+                const int64_t off = (int64_t)(q.z0 - q.g0) * plane;
+                b2.V = q.R + off * Bp;
+                b2.W = q.W + off * ctx->ldw;
+                b2.g.N = (int64_t)(q.z1 - q.z0) * plane;
+                if (ch == 64) {
+                    if (Bp == 8) k_wtr<8, 64><<<q.nct, kMT, wsm, st>>>(b2);
+                    else if (Bp == 16) k_wtr<16, 64><<<q.nct, kMT, wsm, st>>>(b2);
+                    else k_wtr<32, 64><<<q.nct, kMT, wsm, st>>>(b2);
+                } else {
+                    if (Bp == 8) k_wtr<8, 32><<<q.nct, kMT, wsm, st>>>(b2);
+                    else if (Bp == 16) k_wtr<16, 32><<<q.nct, kMT, wsm, st>>>(b2);
+                    else k_wtr<32, 32><<<q.nct, kMT, wsm, st>>>(b2);
+                }
+                ++c;
+            } else {
+                launch_proj<MODE_CG>(q.g, q.nct, psm, st, a);
+            }
             ++c;
         }
         if (dist) {   // rank sum, allreduce of [W^T r, ||r||^2], Steps 7-9
