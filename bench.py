@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--shard", default=None, choices=["weak", "strong"],
                    help="weak: every rank its own query set (c1/c2 default); strong: one fixed set split "
                         "over the ranks (c3/c4 default)")
+    p.add_argument("--precond", default="post", choices=["post", "sym"],
+                   help="RBCG preconditioner: the paper's post-smoothed RBI (default) or the symmetric "
+                        "two-level RBI (NEXT(3), RBS_PRECOND_SYM)")
     p.add_argument("--queries", type=int, default=0,
                    help="strong shards / c5: size of the fixed query set (0 = the config's)")
     return p.parse_args()
@@ -423,9 +426,11 @@ def run_c5(a, world, rank, local):
     X = torch.empty((c.B, nx), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
+    pkw = dict(precond=rbs.RBS_PRECOND_SYM) if a.precond == "sym" else {}
+
     def step(k, **kw):
         b = k % nb
-        return s.solve_batch(mus_all[b * c.B:(b + 1) * c.B], X=X, want_a_n=False, **kw)
+        return s.solve_batch(mus_all[b * c.B:(b + 1) * c.B], X=X, want_a_n=False, **{**pkw, **kw})
 
     for w in range(max(a.warmup, 1)):
         step(w)
@@ -456,13 +461,13 @@ def run_c5(a, world, rank, local):
     s._ws.clear()
     torch.cuda.empty_cache()
     Xh = torch.empty((c.B, nx), dtype=torch.float64, pin_memory=True)
-    s.solve_batch(mus_all[:c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False)
+    s.solve_batch(mus_all[:c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False, **pkw)
     if world > 1:
         dist.barrier()
     te = time.perf_counter()
     for k in range(a.steps):
         b = k % nb
-        s.solve_batch(mus_all[b * c.B:(b + 1) * c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False)
+        s.solve_batch(mus_all[b * c.B:(b + 1) * c.B], X=Xh, x_location=rbs.RBS_MEM_HOST, want_a_n=False, **pkw)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - te
     if world > 1:
@@ -475,13 +480,15 @@ def run_c5(a, world, rank, local):
     if world == 1:
         prof = step(0, profile=1, tol=0.0, max_iter=min(a.profile_iters, 10))["profile"]
     hbm, hbm_src = peaks()
-    line = {"metric": f"parameter queries solved/sec to rel. residual 1e-10 (c5, RBCG, {world} GPU)",
+    line = {"metric": f"parameter queries solved/sec to rel. residual 1e-10 (c5, RBCG{'-sym' if a.precond == 'sym' else ''}, {world} GPU)",
             "value": a.steps * c.B / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(c), "B": c.B, "n": n,
                        "parallelism": f"mesh z-slabs x{world} (NCCL)" if world > 1 else "1 GPU (reference solve)",
                        "queries": nq, "its_min_med_max": [min(its), int(np.median(its)), max(its)],
+                       "preconditioner": "symmetric two-level RBI (RBS_PRECOND_SYM)" if a.precond == "sym"
+                       else "post-smoothed RBI (the paper's)",
                        "true_relres_max": max(trr), "offline_s": round(offline_s, 1),
                        "basis": "multi-fidelity GPU builder (127^3 greedy selects, 511^3 snapshots)",
                        "snapshot_its": snap[:6] if rank == 0 else [],
@@ -583,6 +590,8 @@ def main():
     Xs = [torch.empty((Bq, c.N), dtype=torch.float64, device=s.device) for _ in range(S)]
 
     mkw = (dict(method=rbs.RBS_RBI, max_iter=500000) if a.method == "rbi" else dict(method=rbs.RBS_RBCG))
+    if a.precond == "sym" and a.method == "rbcg":
+        mkw["precond"] = rbs.RBS_PRECOND_SYM
 
     def step(t, k, **kw):
         mb = batches[k % nb]
@@ -736,7 +745,8 @@ def main():
     l2 = (f"inputs larger than L2 (W {wbytes / 1e6:.0f} MB + 4 x {sbytes / 4e6:.0f} MB state > 126 MB)"
           if wbytes + sbytes > 126e6 else
           f"inputs fit in L2 (W {wbytes / 1e6:.1f} MB + state {sbytes / 1e6:.1f} MB): warm-L2 figure")
-    metric = METRIC.replace("(c2,", f"({c.name},").replace("RBCG", a.method.upper())
+    metric = METRIC.replace("(c2,", f"({c.name},").replace(
+        "RBCG", a.method.upper() + ("-sym" if a.precond == "sym" and a.method == "rbcg" else ""))
     if world > 1:
         metric = metric.replace("1 GPU)", f"{world} GPUs)")
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
