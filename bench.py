@@ -501,7 +501,10 @@ def run_c5(a, world, rank, local):
         line["kernels"] = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
                                "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
         iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)
-        iter_bytes = (80 * c.B + 16 * n) * c.N
+        # minimum bytes per batch-iteration: the fused schedule's 80 B + 16n / B per node-query
+        # (DESIGN.md §7); the symmetric two-level preconditioner's passes (3D flat schedule: K1,
+        # K2, y = 0, 3 pre + 3 post half-sweeps, residual-projection, prolongation) 200 B + 24n / B
+        iter_bytes = ((200 * c.B + 24 * n) if a.precond == "sym" else (80 * c.B + 16 * n)) * c.N
         line["roofline"] = {"bound": "hbm", "kernel": "iteration", "achieved": iter_bytes / (iter_us * 1e-6) / 1e9,
                             "peak": hbm, "unit": "GB/s", "frac": iter_bytes / (iter_us * 1e-6) / 1e9 / hbm,
                             "traffic": None, "peak_source": hbm_src, "alg_bytes_per_launch": iter_bytes,
@@ -721,7 +724,8 @@ def main():
     top = max((k for k in alg if k in kernels), key=lambda k: kernels[k]["share"])
     kt = kernels[top]
     iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bp_ queries
-    iter_bytes = ((24 * Bp_ + 16 * n) if a.method == "rbi" else (80 * Bp_ + 16 * n)) * N   # minimum per batch-iteration
+    iter_bytes = ((24 * Bp_ + 16 * n) if a.method == "rbi" else
+                  (200 * Bp_ + 24 * n) if a.precond == "sym" else (80 * Bp_ + 16 * n)) * N   # per batch-iteration
     traffic, traffic_src = ncu_traffic(a.config, top)
     roof = {"bound": "hbm", "kernel": top, "timed_instantiation": TIMED_KERNEL.get((a.config, top)),
             "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",
