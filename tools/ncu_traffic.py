@@ -17,8 +17,12 @@ hdr = rows[0]
 iname, ird, iwr, it = (hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"),
                        hdr.index("dram__bytes_write.sum"), hdr.index("gpu__time_duration.sum"))
 units = rows[1]
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
+
+
+def num(v):
+    return float(str(v).replace(",", ""))
 cls = {"k_smooth2": "k_gs", "k_resid2": "k_proj", "k_cgp2": "k_cgp", "k_reduce_solve": "k_reduce_solve"}
 acc = {}
 for r in rows[2:]:
@@ -26,8 +30,8 @@ for r in rows[2:]:
     c = next((v for k, v in cls.items() if name.startswith(k) or ("void " + k) in name), None)
     if c is None:
         continue
-    b = float(r[ird]) * scale[units[ird]] + float(r[iwr]) * scale[units[iwr]]
-    t = float(r[it]) * tscale[units[it]]
+    b = num(r[ird]) * scale.get(units[ird], 1e6) + num(r[iwr]) * scale.get(units[iwr], 1e6)
+    t = num(r[it]) * tscale.get(units[it], 1.0)
     e = acc.setdefault(c, {"kernel": name, "n": 0, "bytes": 0.0, "us": 0.0})
     e["n"] += 1
     e["bytes"] += b
