@@ -167,6 +167,27 @@ void launch_proj(const Geo& g, int grid, size_t smem, cudaStream_t st, const Pro
     else k_proj<MODE, 3><<<grid, kThreads, smem, st>>>(a);
 }
 
+// launch with programmatic dependent launch (the 2D iteration passes, rbs_internal.cuh
+// pdl_wait / pdl_trigger): the pass may start its prologue while the previous drains
+template <typename... P, typename... A>
+void launch_k(bool pdl, void (*k)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, A... args) {
+    if (!pdl) {
+        k<<<grid, block, smem, st>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // k_smooth2 dynamic shared memory cap: 227 KB per CTA minus its static part
 constexpr int kSmooth2MaxDyn = 225 * 1024;
 template <int BP, bool R, int TX, int WR>
@@ -198,40 +219,41 @@ void set_attrs_v2() {
     cudaFuncSetAttribute(k_resid2<BP, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 template <int BP, bool R, int TX, int WR>
-void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a) {
+void launch_smooth2t(int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a, bool pdl) {
     switch (S) {
-        case 0: k_smooth2<BP, 0, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
-        case 1: k_smooth2<BP, 1, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
-        case 2: k_smooth2<BP, 2, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
-        default: k_smooth2<BP, 3, R, TX, WR><<<grid, kMT, smem, st>>>(a); break;
+        case 0: launch_k(pdl, k_smooth2<BP, 0, R, TX, WR>, grid, kMT, smem, st, a); break;
+        case 1: launch_k(pdl, k_smooth2<BP, 1, R, TX, WR>, grid, kMT, smem, st, a); break;
+        case 2: launch_k(pdl, k_smooth2<BP, 2, R, TX, WR>, grid, kMT, smem, st, a); break;
+        default: launch_k(pdl, k_smooth2<BP, 3, R, TX, WR>, grid, kMT, smem, st, a); break;
     }
 }
 // variant: 0 = strip 32 / W ring 3, 1 = strip 32 / W ring 2, 2 = strip 24 / W ring 3
 template <int BP>
 void launch_smooth2(int var, int S, int grid, size_t smem, cudaStream_t st, const SmoothMarchArgs& a, int v2off) {
+    const bool pdl = !(v2off & 16384);
     if (BP == 32 && S == 3 && a.Rhs && a.npad == 40 && var == 0 && !(v2off & 1024)) {
-        k_smooth2<32, 3, true, 32, 3, 10><<<grid, kMT, smem, st>>>(a);     // n = 33..40 (c2)
+        launch_k(pdl, k_smooth2<32, 3, true, 32, 3, 10>, grid, kMT, smem, st, a);     // n = 33..40 (c2)
         return;
     }
     if (BP == 32 && S == 3 && a.Rhs && a.npad == 64 && var == 1 && !(v2off & 1024)) {
-        k_smooth2<32, 3, true, 32, 2, 16><<<grid, kMT, smem, st>>>(a);     // n = 57..64 (c3)
+        launch_k(pdl, k_smooth2<32, 3, true, 32, 2, 16>, grid, kMT, smem, st, a);     // n = 57..64 (c3)
         return;
     }
     if (var == 0) {
-        if (a.Rhs) launch_smooth2t<BP, true, 32, 3>(S, grid, smem, st, a);
-        else launch_smooth2t<BP, false, 32, 3>(S, grid, smem, st, a);
+        if (a.Rhs) launch_smooth2t<BP, true, 32, 3>(S, grid, smem, st, a, pdl);
+        else launch_smooth2t<BP, false, 32, 3>(S, grid, smem, st, a, pdl);
     } else if (var == 1) {
-        if (a.Rhs) launch_smooth2t<BP, true, 32, 2>(S, grid, smem, st, a);
-        else launch_smooth2t<BP, false, 32, 2>(S, grid, smem, st, a);
+        if (a.Rhs) launch_smooth2t<BP, true, 32, 2>(S, grid, smem, st, a, pdl);
+        else launch_smooth2t<BP, false, 32, 2>(S, grid, smem, st, a, pdl);
     } else {
-        if (a.Rhs) launch_smooth2t<BP, true, 24, 3>(S, grid, smem, st, a);
-        else launch_smooth2t<BP, false, 24, 3>(S, grid, smem, st, a);
+        if (a.Rhs) launch_smooth2t<BP, true, 24, 3>(S, grid, smem, st, a, pdl);
+        else launch_smooth2t<BP, false, 24, 3>(S, grid, smem, st, a, pdl);
     }
 }
 template <int BP, int PF>
-void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r) {
-    if (md == 0) k_resid2<BP, 0, PF><<<grid, kMT, smem, st>>>(r);
-    else k_resid2<BP, 1, PF><<<grid, kMT, smem, st>>>(r);
+void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMarchArgs& r, bool pdl) {
+    if (md == 0) launch_k(pdl, k_resid2<BP, 0, PF>, grid, kMT, smem, st, r);
+    else launch_k(pdl, k_resid2<BP, 1, PF>, grid, kMT, smem, st, r);
 }
 
 // cudaFuncSetAttribute applies to the current device only: once per device
@@ -886,8 +908,10 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     cudaStream_t st = (cudaStream_t)stream;
     const Geo& g = ctx->g;
     const int Bp = pow2_batch(B), lgB = ilog2(Bp), n = ctx->n, npad = ctx->npad, Q = g.Q;
-    // RBS_DISABLE_V2 (debug / A-B, read at rbs_create): bit 0 smoother, bit 1 p-update, bit 2 projection
+    // RBS_DISABLE_V2 (debug / A-B, read at rbs_create): bit 0 smoother, bit 1 p-update, bit 2 projection,
+    // bit 14 programmatic dependent launch of the 2D iteration passes
     const int v2off = ctx->v2off;
+    const bool pdl = !(v2off & 16384);
     const bool cg = o->method == RBS_RBCG;
     // 2D, B_pad <= 32: the projection pass is the row march (k_resid_march)
     const bool use_rmarch = g.dim == 2 && Bp <= 32 && !g.faces;   // row marches: block tables
@@ -1125,14 +1149,14 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 if (md == 0) k_resid_march<0><<<nct, kMarchThreads, rs1.total, st>>>(r);
                 else k_resid_march<1><<<nct, kMarchThreads, rs1.total, st>>>(r);
             } else if (Bp == 8) {
-                if (PF == 2) launch_resid2<8, 2>(md, nct, rsm, st, r);
-                else launch_resid2<8, 1>(md, nct, rsm, st, r);
+                if (PF == 2) launch_resid2<8, 2>(md, nct, rsm, st, r, pdl);
+                else launch_resid2<8, 1>(md, nct, rsm, st, r, pdl);
             } else if (Bp == 16) {
-                if (PF == 2) launch_resid2<16, 2>(md, nct, rsm, st, r);
-                else launch_resid2<16, 1>(md, nct, rsm, st, r);
+                if (PF == 2) launch_resid2<16, 2>(md, nct, rsm, st, r, pdl);
+                else launch_resid2<16, 1>(md, nct, rsm, st, r, pdl);
             } else {
-                if (PF == 2) launch_resid2<32, 2>(md, nct, rsm, st, r);
-                else launch_resid2<32, 1>(md, nct, rsm, st, r);
+                if (PF == 2) launch_resid2<32, 2>(md, nct, rsm, st, r, pdl);
+                else launch_resid2<32, 1>(md, nct, rsm, st, r, pdl);
             }
             pe();
             return 1;
@@ -1187,9 +1211,9 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             c2.s = S; c2.done = done;
             const size_t csm = cgp2_smem_bytes(Bp, Q);
             const int gr = c2.part.nsx * c2.part.nsy;
-            if (Bp == 8) k_cgp2<8><<<gr, kMT, csm, st>>>(c2);
-            else if (Bp == 16) k_cgp2<16><<<gr, kMT, csm, st>>>(c2);
-            else k_cgp2<32><<<gr, kMT, csm, st>>>(c2);
+            if (Bp == 8) launch_k(pdl, k_cgp2<8>, gr, kMT, csm, st, c2);
+            else if (Bp == 16) launch_k(pdl, k_cgp2<16>, gr, kMT, csm, st, c2);
+            else launch_k(pdl, k_cgp2<32>, gr, kMT, csm, st, c2);
         } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
         else if (Bp <= 32 && !(v2off & 8)) {      // two passes: stream p_new, then sigma in row segments
             const int64_t nb2 = (int64_t)g.N * Bp / 2;
@@ -1312,7 +1336,10 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             c += cgp(Pold, Pnew);             // Step 11 (prev) + A p, Step 5 (alpha) in last CTA
             if (pr) cudaMemcpyAsync(L.Rold, L.R, (size_t)vecN * 8, cudaMemcpyDeviceToDevice, st);   // r_k
             c += proj(MODE_CG, Pnew, true);   // Steps 6-7, ||r||, W^T r
-            pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Step 8
+            pb(RBS_K_REDUCE_SOLVE);
+            launch_k(pdl && use_march, k_reduce_solve, Bp, kRsThreads, 0, st, S, 0);   // Step 8
+            pe();
+            ++c;
             if (pr) cudaMemcpyAsync(L.rho_prev, L.rho, (size_t)Bp * 8, cudaMemcpyDeviceToDevice, st);  // rho_k
             if (sym) {
                 c += precond_sym(0);                           // Step 9 (two-level) + Step 10

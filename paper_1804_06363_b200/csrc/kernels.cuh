@@ -1076,7 +1076,6 @@ constexpr int kRsPer = 12;        // columns of a chunk loaded together
 // correction inside the symmetric two-level preconditioner, RBS_PRECOND_SYM); 2: the
 // same, and e is also reported as a_n (the first application)
 __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s, int solve_only = 0) {
-    if (ld_flag(s.done)) return;
     __shared__ double s_rn[kMaxN + 1];
     __shared__ double s_chunk[(kMaxN + 1) * kRsChunks];
     __shared__ double s_e[kMaxN * 8];
@@ -1084,17 +1083,20 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s, int s
     __shared__ int s_go, s_last, s_na;
     const int b = blockIdx.x, tid = threadIdx.x;
     const int rows = s.npad + 1, nr = s.n + 1;     // rows 0..n-1 and the rr row (npad)
-    const bool act = s.active[b] != 0;
-    // A_n^{-1} row slice of this thread for the fixed-order matvec below, loaded
-    // before the partial sums so the two global-load latencies overlap
+    // A_n^{-1} row slice of this thread for the fixed-order matvec below (constant during
+    // the solve: loaded before the dependency wait, so it overlaps the previous pass)
     const int mi = tid >> 3, ml = tid & 7;
     double ai[kMaxN / 8];
     {
-        const bool mv = act && !s.tri && mi < s.n;
+        const bool mv = !s.tri && mi < s.n && b < s.B;
         const double* Ai = s.Ainv + (int64_t)b * s.npad * s.npad + mi * s.npad;
 #pragma unroll
         for (int k = 0; k < kMaxN / 8; ++k) ai[k] = (mv && ml + 8 * k < s.n) ? __ldcg(Ai + ml + 8 * k) : 0.0;
     }
+    pdl_wait();                       // the partials and the flags come from the previous pass
+    if (ld_flag(s.done)) return;
+    pdl_trigger();                    // the next pass may start its prologue on the idle SMs
+    const bool act = s.active[b] != 0;
     if (act) {
         // two-stage fixed-order sums: 32 chunks of <= 10 columns per row (all loads of a
         // chunk in flight at once), then one warp per row combines its 32 chunks

@@ -143,7 +143,6 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
     // prolongation unrolls completely (no loop-carried branch; loads scheduled ahead)
     constexpr int kS2WR = WR, kS2D = WR - 1;
     S2CLK_ENTRY
-    if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
     constexpr int TW = TX + 2 * S;
     constexpr int VROW = TW * BP;
@@ -186,10 +185,6 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
 
     // ---- init: zero the rings (Dirichlet columns/rows stay zero), tables ------
     for (int t = tid; t < EO; t += kMT) smd[t] = 0.0;
-    for (int t = tid; t < WO - EO; t += kMT) {
-        const int j = t / (BP + 4), bb = t - j * (BP + 4);
-        smd[EO + t] = (a.has_e && j < npad && bb < BP) ? a.E[j * BP + bb] : 0.0;
-    }
     for (int t = tid; t < kS2WR * WROW; t += kMT) smd[WO + t] = 0.0;
     for (int t = tid; t < a.g.Q * BP; t += kMT) {
         const double v = a.theta[t];
@@ -197,12 +192,18 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
         smd[CHO + t] = a.g.h2 / (4.0 * v);
     }
     fill_colinfo(a.g, xlo, TW, s_ci, s_cu);
-    for (int t = tid; t < BP; t += kMT) s_act[t] = a.active[t];
     if (tid == 0) {
         for (int k = 0; k < kS2WR; ++k) mbar_init(&wbar[k], 1);
         for (int k = 0; k < kS2RR; ++k) mbar_init(&rbar[k], 1);
         mbar_fence_init();
     }
+    pdl_wait();                       // E, the active flags, r and x_old come from earlier passes
+    if (a.done && ld_flag(a.done)) return;
+    for (int t = tid; t < WO - EO; t += kMT) {
+        const int j = t / (BP + 4), bb = t - j * (BP + 4);
+        smd[EO + t] = (a.has_e && j < npad && bb < BP) ? a.E[j * BP + bb] : 0.0;
+    }
+    for (int t = tid; t < BP; t += kMT) s_act[t] = a.active[t];
     __syncthreads();
 
     const uint32_t wb = a.has_e ? (uint32_t)ncopy * ldw * 8 : 0u;
@@ -398,6 +399,7 @@ __global__ void __launch_bounds__(kMT, 1) k_smooth2(SmoothMarchArgs a) {
         S2CLK(4);
     }
     S2CLK_FLUSH;
+    pdl_trigger();
     if (!a.last) return;
     // ---- partials and RBCG Step 10 in the last CTA (rings are dead) ----------
     double* s_a = smd;
@@ -476,7 +478,6 @@ __host__ __device__ inline size_t cgp2_smem_bytes(int Bp, int Q) {
 
 template <int BP>
 __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
-    if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
     constexpr int TW = kC2TX + 2;
     constexpr int VROW = TW * BP;
@@ -511,6 +512,8 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
         for (int k = 0; k < kC2R; ++k) mbar_init(&bars[k], 1);
         mbar_fence_init();
     }
+    pdl_wait();                       // y, p_old, beta and the flags come from earlier passes
+    if (a.done && ld_flag(a.done)) return;
     __syncthreads();
     const uint32_t vb = (uint32_t)ncopy * BP * 8;
     auto issue = [&](int u) {
@@ -617,6 +620,7 @@ __global__ void __launch_bounds__(kMT, 2) k_cgp2(CGP2Args a) {
         }
         __syncthreads();
     }
+    pdl_trigger();
     // ---- partials; last CTA: alpha = rho / sigma, MAXIT / CURVATURE (Step 5)
     SolveState& s = a.s;
     s_a[tid] = sig;
@@ -673,7 +677,6 @@ template <int BP, int MODE, int kR2PF>
 __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
     constexpr int kR2NS = 3 + kR2PF;     // stencil-input / W ring rows
     constexpr int kR2NC = 2 + kR2PF;     // x / r / f ring rows
-    if (a.done && ld_flag(a.done)) return;
     constexpr int LGB = LgB<BP>::v;
     constexpr int BPV = BP + 4;
     constexpr int NBT = BP / 8, LGNBT = LGB - 3;
@@ -705,14 +708,16 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
 
     for (int t = tid; t < STo; t += kMT) smd[t] = 0.0;
     for (int t = tid; t < a.g.Q * BP; t += kMT) smd[STo + t] = a.g.scale * a.theta[t];
-    for (int t = tid; t < BP; t += kMT) {
-        s_act[t] = a.active ? a.active[t] : 1;
-        s_alpha[t] = MODE == 0 ? a.alpha[t] : 0.0;
-    }
     fill_colinfo(a.g, xlo, kRmTX + 2, s_ci, s_cu);
     if (tid == 0) {
         for (int k = 0; k <= kR2PF; ++k) mbar_init(&bars[k], 1);
         mbar_fence_init();
+    }
+    pdl_wait();                       // p, x, r, alpha and the flags come from earlier passes
+    if (a.done && ld_flag(a.done)) return;
+    for (int t = tid; t < BP; t += kMT) {
+        s_act[t] = a.active ? a.active[t] : 1;
+        s_alpha[t] = MODE == 0 ? a.alpha[t] : 0.0;
     }
     __syncthreads();
 
@@ -875,6 +880,7 @@ __global__ void __launch_bounds__(kMT, 1) k_resid2(ResidMarchArgs a) {
         sl_n = sl_n + 1 == kR2NS ? 0 : sl_n + 1;
         sl_x = sl_x + 1 == kR2NC ? 0 : sl_x + 1;
     }
+    pdl_trigger();
     // ---- per-CTA partials: the 4 k-quarters of each (j-tile, b-tile) in order
     double* s_q = smd;          // rings are dead: [ntask][64]
 #pragma unroll

@@ -229,6 +229,17 @@ __device__ __forceinline__ double gs_value(const Geo& g, const double* k, double
     return num / den;
 }
 
+// ---- programmatic dependent launch (the 2D iteration passes) -----------------
+// A pass launched with cudaLaunchAttributeProgrammaticStreamSerialization may start
+// its prologue (shared-memory zeroing, constant tables, barrier init) while the
+// previous pass drains; pdl_wait() blocks until that pass has completed and its
+// writes are visible (a no-op for an ordinary launch).  Every pass calls
+// pdl_trigger() only after its own pdl_wait(), so when pass k+1 starts its prologue
+// pass k-1 has completed: a prologue may read only inputs that do not change during
+// the solve (W, theta, A_n^{-1}).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- FP64 tensor core: D(8x8) += A(8x4, row) * B(4x8, col) ------------------
 // lane l: a = A[l>>2][l&3], b = B[l&3][l>>2], d0,d1 = D[l>>2][2(l&3)+{0,1}]
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
