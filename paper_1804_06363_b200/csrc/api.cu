@@ -1041,10 +1041,12 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
 
     // ---- pass builders -------------------------------------------------------
-    auto prolong = [&](double* Yv, int acc) {
+    // skip: the colour of the half-sweep that follows (its nodes are overwritten unread)
+    auto prolong = [&](double* Yv, int acc, int skip = -1) {
         ProlongArgs a{};
         a.N = g.N; a.Bp = Bp; a.npad = npad; a.ldw = ctx->ldw; a.W = ctx->Wi; a.E = L.E; a.active = L.active;
         a.Y = Yv; a.accumulate = acc; a.done = done;
+        a.skip_color = skip; a.dim = g.dim; a.m = g.m; a.kofs = g.kofs; a.fm = g.fm;
         pb(RBS_K_PROLONG);
         if (npad > 0) {
             k_prolong<<<pgrid, kThreads, 0, st>>>(a);
@@ -1232,6 +1234,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     // (RBS_PRECOND_SYM) and the Polak-Ribiere beta (RBS_BETA_PR)
     const bool sym = cg && o->precond == RBS_PRECOND_SYM, pr = cg && o->beta_rule == RBS_BETA_PR;
     const std::vector<int> rseq(seq.rbegin(), seq.rend());     // adjoint sweep: colours reversed
+    // the red-black half-sweep that follows every prolongation (none: Jacobi / no sweeps)
+    const int first_col = (!jac && !seq.empty()) ? seq[0] : -1;
     const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac && !g.faces && !sym && !pr;
     auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
                      int init) {
@@ -1294,7 +1298,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S, init ? 2 : 1);   // e (no stop test)
             pe();
             ++c;
-            c += prolong(L.Y, 1);                                  // y2 = y1 + W e
+            c += prolong(L.Y, 1, first_col);                       // y2 = y1 + W e
         }
         c += smooth(L.Y, L.R, 0.0, true, init);                    // post; Step 10 in the last CTA
         return c;
@@ -1316,7 +1320,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             launches += prolong(y0b, 0);
             launches += smooth_jac(y0b, L.Y, L.R, 0.0, true, 1);
         } else {
-            launches += prolong(L.Y, 0);
+            launches += prolong(L.Y, 0, first_col);
             launches += smooth(L.Y, L.R, 0.0, true, 1);
         }
         CKL();
@@ -1350,7 +1354,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 c += prolong(y0b, 0);                          // Step 9: y0 = W e
                 c += smooth_jac(y0b, L.Y, L.R, 0.0, true, 0);  // Jacobi sweeps; Step 10
             } else {
-                c += prolong(L.Y, 0);             // Step 9: y0 = W e
+                c += prolong(L.Y, 0, first_col);  // Step 9: y0 = W e
                 c += smooth(L.Y, L.R, 0.0, true, 0);  // y = S(A, r, y0); Step 10 in last CTA
             }
             if (pr) c += pr_fix();
@@ -1361,7 +1365,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             c += proj(MODE_RESID, nullptr, true, Xo);           // Steps 2, 4
             pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Steps 3, 5
         } else {
-            c += prolong(L.X, 1);                               // Step 6
+            c += prolong(L.X, 1, first_col);                    // Step 6
             c += smooth(L.X, Fv, ctx->fconst, false, 0);        // Step 7
             c += proj(MODE_RESID, nullptr, true);               // Steps 2, 4
             pb(RBS_K_REDUCE_SOLVE); k_reduce_solve<<<Bp, kRsThreads, 0, st>>>(S); pe(); ++c;  // Steps 3, 5

@@ -402,6 +402,11 @@ struct ProlongArgs {
     double* Y;            // [N8][Bp]
     int accumulate;
     const int* done;
+    // skip_color >= 0: nodes of that red-black colour are not prolongated -- the
+    // smoother's first half-sweep (that colour) overwrites them without reading them
+    // (direct form, AMB-6), so their W rows are not loaded and y is not written there
+    int skip_color, dim, m, kofs;
+    FastDiv fm;
 };
 
 __device__ __forceinline__ void prolong_store(const ProlongArgs& a, int64_t i, int b, double d0,
@@ -440,14 +445,32 @@ __global__ void __launch_bounds__(kThreads) k_prolong(ProlongArgs a) {
     for (int64_t nt = gw / nbt; nt < ntile; nt += 2 * ts) {
         const int64_t nt2 = nt + ts;
         const bool two = nt2 < ntile;
-        const double* wA = a.W + (nt * 8 + (lane >> 2)) * a.ldw + (lane & 3);
-        const double* wB = a.W + ((two ? nt2 : nt) * 8 + (lane >> 2)) * a.ldw + (lane & 3);
+        const int64_t iA = nt * 8 + (lane >> 2), iB = (two ? nt2 : nt) * 8 + (lane >> 2);
+        const double* wA = a.W + iA * a.ldw + (lane & 3);
+        const double* wB = a.W + iB * a.ldw + (lane & 3);
+        bool ldA = true, ldB = true;
+        if (a.skip_color >= 0) {            // red-black colour of the fragment's node rows
+            auto col = [&](int64_t i) {
+                const uint32_t t = fdiv((uint32_t)i, a.fm);
+                const int I = (int)((uint32_t)i - t * (uint32_t)a.m) + 1;
+                int par;
+                if (a.dim == 2) {
+                    par = (I + (int)t + 1) & 1;
+                } else {
+                    const uint32_t u = fdiv(t, a.fm);
+                    par = (I + (int)(t - u * (uint32_t)a.m) + 1 + (int)u + 1 + a.kofs) & 1;
+                }
+                return par;
+            };
+            ldA = iA >= a.N || col(iA) != a.skip_color;
+            ldB = iB >= a.N || col(iB) != a.skip_color;
+        }
         double xa[16], xb[16];
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
             if (kk < nk) {
-                xa[kk] = __ldg(wA + kk * 4);
-                xb[kk] = __ldg(wB + kk * 4);
+                xa[kk] = ldA ? __ldg(wA + kk * 4) : 0.0;
+                xb[kk] = ldB ? __ldg(wB + kk * 4) : 0.0;
             }
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
@@ -456,8 +479,8 @@ __global__ void __launch_bounds__(kThreads) k_prolong(ProlongArgs a) {
                 dmma_8x8x4(a0, a1, xa[kk], ef[kk]);
                 dmma_8x8x4(b0, b1, xb[kk], ef[kk]);
             }
-        prolong_store(a, nt * 8 + (lane >> 2), b, a0, a1, act0, act1);
-        if (two) prolong_store(a, nt2 * 8 + (lane >> 2), b, b0, b1, act0, act1);
+        if (ldA) prolong_store(a, iA, b, a0, a1, act0, act1);
+        if (two && ldB) prolong_store(a, iB, b, b0, b1, act0, act1);
     }
 }
 

@@ -476,6 +476,8 @@ rbs_status solve_slabs(rbs_ctx* ctx, int B, const double* mu_host, const rbs_sol
                 ProlongArgs a{};
                 a.N = q.g.N; a.Bp = Bp; a.npad = npad; a.ldw = ctx->ldw; a.W = q.W; a.E = L.E;
                 a.active = L.active; a.Y = q.Y; a.accumulate = 0; a.done = done;
+                a.skip_color = seq.empty() ? -1 : seq[0];   // overwritten unread by the first half-sweep
+                a.dim = 3; a.m = q.g.m; a.kofs = q.g.kofs; a.fm = q.g.fm;
                 const int pgrid = grid_for(((q.g.N + 7) / 8) * (Bp / 8), 8, ctx->num_sms * 16);
                 k_prolong<<<pgrid, kThreads, 0, st>>>(a);
             } else {
