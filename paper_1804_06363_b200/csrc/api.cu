@@ -1235,7 +1235,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     const bool sym = cg && o->precond == RBS_PRECOND_SYM, pr = cg && o->beta_rule == RBS_BETA_PR;
     const std::vector<int> rseq(seq.rbegin(), seq.rend());     // adjoint sweep: colours reversed
     // the red-black half-sweep that follows every prolongation (none: Jacobi / no sweeps)
-    const int first_col = (!jac && !seq.empty()) ? seq[0] : -1;
+    const int first_col = (!jac && !seq.empty() && !(v2off & 32768)) ? seq[0] : -1;
     const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac && !g.faces && !sym && !pr;
     auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
                      int init) {
