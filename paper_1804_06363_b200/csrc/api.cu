@@ -16,10 +16,11 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include "../../include/rbs.h"
-#include "march2.cuh"
+#include "zmarch.cuh"
 
 using namespace rbs;
 
@@ -256,6 +257,72 @@ void launch_resid2(int md, int grid, size_t smem, cudaStream_t st, const ResidMa
     else launch_k(pdl, k_resid2<BP, 1, PF>, grid, kMT, smem, st, r);
 }
 
+// ---- TMA tensor maps of the 3D z-plane marches (zmarch.cuh) -------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link);
+// resolved once, immutable afterwards
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+// 4-D map of a node-major batch vector v[m][m][m][Bp] (dims innermost first: lane, I, J, K)
+// with box [Bp][bx][by][1]; out-of-range elements of a box are zero-filled
+bool zmap(CUtensorMap* map, const double* v, const Geo& g, int Bp, int bx, int by) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    const cuuint64_t m = (cuuint64_t)g.m;
+    cuuint64_t dims[4] = {(cuuint64_t)Bp, m, m, (cuuint64_t)g.mz};
+    cuuint64_t strides[3] = {(cuuint64_t)Bp * 8, m * Bp * 8, m * m * Bp * 8};
+    cuuint32_t box[4] = {(cuuint32_t)Bp, (cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(v), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// z-march work partition: tiles x z-segments; the segment count minimises
+// rounds x (planes per unit + 2 halo planes) over a persistent grid of `grid` CTAs
+ZPart z_part(const Geo& g, int TX, int TY, int grid) {
+    ZPart p{};
+    p.ntx = (g.m + TX - 1) / TX;
+    p.nty = (g.m + TY - 1) / TY;
+    const int tiles = p.ntx * p.nty;
+    int64_t best = -1;
+    for (int nz = 1; nz <= std::min(g.m, 64); ++nz) {
+        const int zlen = (g.m + nz - 1) / nz, nze = (g.m + zlen - 1) / zlen;
+        const int64_t units = (int64_t)tiles * nze, rounds = (units + grid - 1) / grid;
+        const int64_t cost = rounds * (zlen + 2);
+        if (best < 0 || cost < best) {
+            best = cost;
+            p.nz = nze;
+            p.zlen = zlen;
+            p.units = (int)units;
+        }
+    }
+    return p;
+}
+// dynamic shared memory of the z-march kernels: rings + theta table, capped so the
+// kernels' static shared memory (barriers, LAST epilogue buffers, ~9 KB) still fits 227 KB
+constexpr size_t kZMaxDyn = 217 * 1024;
+template <int BP>
+void set_attrs_z() {
+    auto cap = [](size_t b) { return (int)std::min(b, kZMaxDyn); };
+    cudaFuncSetAttribute(k_cgz<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap(zsmem_bytes<BP>(0, RBS_MAX_Q)));
+    cudaFuncSetAttribute(k_gsz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         cap(zsmem_bytes<BP>(1, RBS_MAX_Q)));
+    cudaFuncSetAttribute(k_gsz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         cap(zsmem_bytes<BP>(1, RBS_MAX_Q)));
+    cudaFuncSetAttribute(k_xrz<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap(zsmem_bytes<BP>(2, RBS_MAX_Q)));
+}
+
 // cudaFuncSetAttribute applies to the current device only: once per device
 std::mutex g_attr_mu;
 bool g_attr_done[64] = {false};
@@ -289,6 +356,9 @@ void set_attrs(int dev) {
     set_attrs_v2<8>();
     set_attrs_v2<16>();
     set_attrs_v2<32>();
+    set_attrs_z<8>();
+    set_attrs_z<16>();
+    set_attrs_z<32>();
     g_attr_done[dev] = true;
 }
 
@@ -1024,6 +1094,26 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     const std::vector<int> seq = color_seq(o->smoother, o->sweeps);
     const int pgrid = grid_for(((g.N + 7) / 8) * (Bp / 8), 8, ctx->num_sms * 16);
 
+    // 3D z-plane marches fed by TMA tensor maps (zmarch.cuh): thermal-block operator on a
+    // full grid, B_pad 8 / 16 / 32 (RBS_DISABLE_V2 bit 16 keeps the row-segment kernels)
+    const bool zm3 = g.dim == 3 && !g.faces && g.kofs == 0 && g.mz == g.m && (Bp == 8 || Bp == 16 || Bp == 32) &&
+                     !(v2off & 65536) && tmap_encoder() != nullptr;
+    const int ztx = Bp == 8 ? ZShape<8>::TX : Bp == 16 ? ZShape<16>::TX : ZShape<32>::TX;
+    const int zty = Bp == 8 ? ZShape<8>::TY : Bp == 16 ? ZShape<16>::TY : ZShape<32>::TY;
+    ZPart zpt{};
+    int zgrid = 0;
+    if (zm3) {
+        zpt = z_part(g, ztx, zty, std::min(ctx->num_sms, nctf));
+        zgrid = std::min(std::min(ctx->num_sms, nctf), zpt.units);
+    }
+    auto zsm = [&](int kind) {
+        const size_t b = Bp == 8 ? zsmem_bytes<8>(kind, Q) : Bp == 16 ? zsmem_bytes<16>(kind, Q) : zsmem_bytes<32>(kind, Q);
+        return b <= kZMaxDyn ? b : (size_t)0;
+    };
+    // haloed (stencil operand) / interior (pointwise operand) plane-tile maps of a batch vector
+    auto zmap_h = [&](CUtensorMap* mp, const double* v) { return zmap(mp, v, g, Bp, ztx + 2, zty + 2); };
+    auto zmap_i = [&](CUtensorMap* mp, const double* v) { return zmap(mp, v, g, Bp, ztx, zty); };
+
     // ---- profiling hooks (no-ops unless opts.profile) -------------------------
     const bool prof = o->profile != 0;
     int pne = 0;
@@ -1112,10 +1202,23 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         for (size_t t = 0; t < cs.size(); ++t) {
             a.color = cs[t];
             const bool l = last && t + 1 == cs.size();
+            CUtensorMap my, mr;
             pb(RBS_K_GS);
             if (g.dim == 2) {
                 if (l) k_gs<2, true><<<nctf, kFlat, fsm, st>>>(a);
                 else k_gs<2, false><<<nctf, kFlat, fsm, st>>>(a);
+            } else if (zm3 && a.color >= 0 && zsm(1) && zmap_h(&my, Yv) && zmap_i(&mr, rhs ? rhs : Yv)) {
+                // z-plane march: y tile with halo + r tile per plane by tensor-map copies
+                if (Bp == 8) {
+                    if (l) k_gsz<8, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
+                    else k_gsz<8, false><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
+                } else if (Bp == 16) {
+                    if (l) k_gsz<16, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
+                    else k_gsz<16, false><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
+                } else {
+                    if (l) k_gsz<32, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
+                    else k_gsz<32, false><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
+                }
             } else if (Bp <= 32 && !(v2off & 8) && a.color >= 0) {   // row pencils (x in registers)
                 // 4-node row segments, all loads of a segment in flight (128 registers,
                 // one CTA per SM: measured 2.2x the element-per-thread k_gs at 127^3, B = 16)
@@ -1173,7 +1276,12 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         int nl = 1;
         if (mode == MODE_CG && g.dim == 3 && use_active && Bp <= 32 && !(v2off & 8)) {
             // two passes: x, r update in row segments, then W^T r, ||r||^2 on the new r
-            if (g.faces) k_xr3r<4, true><<<nctf, kFlat, fsm, st>>>(a, lgB);
+            CUtensorMap mpz;
+            if (zm3 && zsm(2) && zmap_h(&mpz, P)) {   // z-plane march, p tile with halo by tensor map
+                if (Bp == 8) k_xrz<8><<<zgrid, kZT, zsm(2), st>>>(mpz, a, zpt);
+                else if (Bp == 16) k_xrz<16><<<zgrid, kZT, zsm(2), st>>>(mpz, a, zpt);
+                else k_xrz<32><<<zgrid, kZT, zsm(2), st>>>(mpz, a, zpt);
+            } else if (g.faces) k_xr3r<4, true><<<nctf, kFlat, fsm, st>>>(a, lgB);
             else k_xr3r<4, false><<<nctf, kFlat, fsm, st>>>(a, lgB);
             ProjArgs b2 = a;
             b2.V = L.R;
@@ -1204,6 +1312,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.beta = L.beta; a.Y = L.Y; a.Pold = Pold; a.Pnew = Pnew; a.s = S; a.done = done;
         int nl = 1;
+        CUtensorMap zmy, zmp;
         pb(RBS_K_CGP);
         if (!(v2off & 2) && g.dim == 2 && Bp <= 32 && !g.faces) {
             CGP2Args c2{};
@@ -1217,7 +1326,12 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             else if (Bp == 16) launch_k(pdl, k_cgp2<16>, gr, kMT, csm, st, c2);
             else launch_k(pdl, k_cgp2<32>, gr, kMT, csm, st, c2);
         } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
-        else if (Bp <= 32 && !(v2off & 8)) {      // two passes: stream p_new, then sigma in row segments
+        else if (zm3 && zsm(0) && zmap_h(&zmy, L.Y) && zmap_h(&zmp, Pold)) {
+            // one z-plane march: p = y + beta p_old on the haloed tiles, sigma = p^T A p
+            if (Bp == 8) k_cgz<8><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+            else if (Bp == 16) k_cgz<16><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+            else k_cgz<32><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+        } else if (Bp <= 32 && !(v2off & 8)) {      // two passes: stream p_new, then sigma in row segments
             const int64_t nb2 = (int64_t)g.N * Bp / 2;
             k_pnew3<<<(unsigned)std::min<int64_t>((nb2 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(
                 a.Y, a.Pold, a.Pnew, a.beta, a.active, nb2, Bp, a.done);

@@ -1216,11 +1216,15 @@ __global__ void __launch_bounds__(kRsThreads) k_reduce_solve(SolveState s, int s
         }
         }
     }
-    if (!solve_only && cta_is_last(s.ticket, &s_last)) {
+    // RBI: the iteration counter and the done flag in the last CTA.  RBCG skips the ticket
+    // (an L2 round trip chain per iteration): the smoother pass that follows recomputes the
+    // done flag in its last CTA, so a batch whose last query converged here costs one more
+    // (all-lanes-frozen) smoother pass per solve instead
+    if (!solve_only && s.method == 0 && cta_is_last(s.ticket, &s_last)) {
         const int any = cta_any_active(s);
         if (threadIdx.x == 0) {
             *(volatile int*)s.done = any ? 0 : 1;
-            if (s.method == 0) *(volatile int*)s.kcount = ld_flag(s.kcount) + 1;
+            *(volatile int*)s.kcount = ld_flag(s.kcount) + 1;
         }
         release_ticket(s.ticket);
     }

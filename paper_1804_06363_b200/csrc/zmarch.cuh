@@ -1,0 +1,482 @@
+// zmarch.cuh -- z-plane marching passes for 3D grids (sm_100a), fed by TMA tensor maps.
+//
+// The 3D streaming passes of an RBCG iteration as 2.5D marches: a CTA owns an (x, y)
+// tile of TX x TY nodes and a segment of z-planes and walks up the planes.  Each
+// plane's tile arrives by ONE 4-D tensor-map copy (cp.async.bulk.tensor.4d, SASS
+// UTMALDG) of the node-major batch vector v[K][J][I][Bp] -- box [Bp][TX+2][TY+2][1]
+// for the operand the 7-point stencil reads (its x/y halo included; halo nodes outside
+// the grid are zero-filled by the TMA unit, i.e. the homogeneous Dirichlet values), box
+// [Bp][TX][TY][1] for the pointwise operands -- into shared-memory rings completing on
+// mbarriers, several planes ahead of the compute.  Every z-neighbour is served from the
+// ring (each plane is read from HBM once per pass; the x/y halo, ~1.4x the tile, from
+// L2) and every pass has one CTA barrier per plane.
+//
+//   k_cgz   RBCG Step 11 + sigma of Step 5: p = y + beta p_old, sigma = p^T A p
+//            -- one pass instead of k_pnew3 + k_sigma3r
+//   k_gsz   one red-black Gauss-Seidel half-sweep (eq8, AMB-5/6),
+//           LAST: y^T r, y^T y and RBCG Step 10
+//   k_xrz   RBCG Steps 6-7: x += alpha p, r -= alpha A p
+//
+// Per node the arithmetic is exactly that of the row-segment kernels (node_kappa,
+// stencil_apply, gs_value, neighbour order -x,+x,-y,+y,-z,+z), so node values are
+// bitwise the same; only the order of the per-CTA partial sums differs.  Thermal-block
+// operator on a full grid only (no mesh slabs, no face coefficients): those keep the
+// row-segment kernels.
+#pragma once
+#include <cuda.h>
+
+#include "march2.cuh"
+
+namespace rbs {
+
+constexpr int kZT = 512;                // threads per CTA (== kFlat: the LAST epilogues are shared)
+static_assert(kZT == kFlat, "z-march epilogues reuse the flat passes' reductions");
+
+// tile shapes: 2048 interior node-queries per plane (4 per thread) for every batch width
+template <int BP> struct ZShape;
+template <> struct ZShape<8>  { static constexpr int TX = 32, TY = 8; };
+template <> struct ZShape<16> { static constexpr int TX = 16, TY = 8; };
+template <> struct ZShape<32> { static constexpr int TX = 16, TY = 4; };
+
+template <int BP>
+struct ZGeom {
+    static constexpr int TX = ZShape<BP>::TX, TY = ZShape<BP>::TY;
+    static constexpr int HX = TX + 2, HY = TY + 2;
+    static constexpr int HP = HX * HY * BP;      // doubles of a haloed plane tile
+    static constexpr int IP = TX * TY * BP;      // doubles of an interior plane tile
+    static constexpr int NE = IP / kZT;          // interior elements per thread
+    static constexpr int LGB = LgB<BP>::v;
+    // TMA issue distance DI (planes ahead of the compute): the stencil operand's ring holds
+    // the 3-plane window + DI slots (a slot is refilled only after the step that last reads
+    // it has passed its barrier); 2 for the widest batch so every ring fits 227 KB
+    static constexpr int DI = BP == 32 ? 2 : 3;
+    static constexpr int NA = DI + 3;
+    static_assert(IP % kZT == 0, "tile must hold a whole number of elements per thread");
+};
+
+// work partition: ntx x nty tiles x nz z-segments of zlen planes, units handed out
+// round-robin to a persistent grid (unit u: tile u % tiles, segment u / tiles)
+struct ZPart {
+    int ntx, nty, nz, zlen, units;
+};
+
+template <int BP>
+__host__ __device__ constexpr size_t zsmem_bytes(int kind, int Q) {
+    // kind 0: k_cgz (y ring NA + p_old ring DI, haloed), 1: k_gsz (y ring NA haloed + r ring
+    // DI+1 interior), 2: k_xrz (p ring NA haloed)
+    using Z = ZGeom<BP>;
+    return (size_t)8 * (kind == 0 ? (Z::NA + Z::DI) * Z::HP
+                        : kind == 1 ? Z::NA * Z::HP + (Z::DI + 1) * Z::IP
+                                    : Z::NA * Z::HP) +
+           (size_t)Q * BP * 8;
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// per-thread view of its NE interior elements of the current tile (loop invariant over z)
+template <int BP>
+struct ZElems {
+    using Z = ZGeom<BP>;
+    uint32_t h[Z::NE];       // byte offset of the element in a haloed plane
+    int64_t gxy[Z::NE];      // element offset within a global plane: ((J-1) m + I-1) Bp + b
+    int ij[Z::NE];           // I + J (colour), -1: outside the grid
+    int cxy[Z::NE];          // bx + by*px of the node's cells if they agree in x and y, else -1
+    __device__ __forceinline__ void init(const Geo& g, int x0, int y0, int tid) {
+        const int b = tid & (BP - 1);
+#pragma unroll
+        for (int j = 0; j < Z::NE; ++j) {
+            const int n = (tid + j * kZT) >> Z::LGB;
+            const int ix = n % Z::TX, iy = n / Z::TX;
+            const int I = x0 + ix, J = y0 + iy;
+            h[j] = 8u * (uint32_t)(((iy + 1) * Z::HX + ix + 1) * BP + b);
+            gxy[j] = ((int64_t)(J - 1) * g.m + (I - 1)) * BP + b;
+            const bool in = I <= g.m && J <= g.m;
+            ij[j] = in ? I + J : -1;
+            const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
+            const int by0 = axis_block(g, J - 1, g.py), by1 = axis_block(g, J, g.py);
+            cxy[j] = (bx0 == bx1 && by0 == by1) ? bx0 + by0 * g.px : -1;
+        }
+    }
+};
+
+__device__ __forceinline__ void zunit(const ZPart& p, int m, int u, int TX, int TY, int& x0, int& y0, int& za,
+                                      int& zb) {
+    const int tiles = p.ntx * p.nty;
+    const int zs = u / tiles, t = u - zs * tiles;
+    const int ty = t / p.ntx, tx = t - ty * p.ntx;
+    x0 = 1 + tx * TX;
+    y0 = 1 + ty * TY;
+    za = 1 + zs * p.zlen;
+    zb = min(m + 1, za + p.zlen);
+}
+
+// the 7-point stencil / Gauss-Seidel value with all six edge coefficients equal to c:
+// the same operations in the same order as stencil_apply<3> / gs_value<3> with k[e] = c
+// (bitwise equal), without an addressable coefficient array (no local-memory traffic)
+__device__ __forceinline__ double stencil_c(const Geo& g, double c, double vp, const double* nb) {
+    double s = c * (vp - nb[0]);
+#pragma unroll
+    for (int e = 1; e < 6; ++e) s = fma(c, vp - nb[e], s);
+    return g.scale * s;
+}
+__device__ __forceinline__ double gs_c(const Geo& g, double c, double rhs, const double* nb) {
+    double num = g.h2 * rhs, den = c;
+    num = fma(c, nb[0], num);
+#pragma unroll
+    for (int e = 1; e < 6; ++e) {
+        num = fma(c, nb[e], num);
+        den += c;
+    }
+    return num / den;
+}
+// general node (block interface): cell-averaged coefficients out of line
+__device__ __noinline__ double stencil_general(const Geo& g, const double* s_th, int ldb, int b, int I, int J,
+                                               int K, double vp, const double* nb) {
+    double k[6];
+    node_kappa<3>(g, s_th, ldb, b, I, J, K, k);
+    return stencil_apply<3>(g, k, vp, nb);
+}
+__device__ __noinline__ double gs_general(const Geo& g, const double* s_th, int ldb, int b, int I, int J, int K,
+                                          double rhs, const double* nb) {
+    double k[6];
+    node_kappa<3>(g, s_th, ldb, b, I, J, K, k);
+    return gs_value<3>(g, k, rhs, nb);
+}
+
+// ===========================================================================
+// k_cgz: RBCG Step 11 + Step 5 for 3D grids.
+//   step t (plane K = za-1+t arrives: y and p_old tiles with halo):
+//     p = y + beta p_old over the whole haloed tile, in place in the y slot;
+//     the owned interior nodes are stored to Pnew
+//   then sigma += p^T A p on plane K-1 (slots of K-2, K-1, K)
+// ===========================================================================
+template <int BP>
+__global__ void __launch_bounds__(kZT, 1)
+    k_cgz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP, CGPArgs a, ZPart zp) {
+    using Z = ZGeom<BP>;
+    constexpr int NA = Z::NA, NP = Z::DI, DI = Z::DI;
+    extern __shared__ __align__(128) double smd[];
+    __shared__ __align__(8) uint64_t barA[NA], barP[NP];
+    if (a.done && ld_flag(a.done)) return;
+    const Geo& g = a.g;
+    const int m = g.m, tid = threadIdx.x, b = tid & (BP - 1);
+    double* s_th = smd + (NA + NP) * Z::HP;
+    for (int t = tid; t < g.Q * BP; t += kZT) s_th[t] = a.theta[t];
+    if (tid == 0) {
+        for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
+        for (int k = 0; k < NP; ++k) mbar_init(&barP[k], 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&mY);
+        tma_prefetch_desc(&mP);
+    }
+    const bool act = a.active[b] != 0;
+    const double bet = a.beta[b];
+    const uint32_t sA = smem_u32(smd), sP = sA + 8u * NA * Z::HP;
+    const int64_t sz = (int64_t)m * m * BP;
+    const int pxy = g.px * g.py;
+    constexpr uint32_t HPB = 8u * Z::HP;
+    uint32_t G = 0;      // planes loaded by this CTA before the current unit
+    double sig = 0.0;
+    for (int u = blockIdx.x; u < zp.units; u += gridDim.x) {
+        int x0, y0, za, zb;
+        zunit(zp, m, u, Z::TX, Z::TY, x0, y0, za, zb);
+        const int T = zb - za + 2;                 // planes za-1 .. zb
+        ZElems<BP> el;
+        el.init(g, x0, y0, tid);
+        __syncthreads();                           // previous unit's slots are no longer read
+        auto issue = [&](int t) {
+            const int K = za - 1 + t;
+            const uint32_t q = G + (uint32_t)t;
+            const bool in = K >= 1 && K <= m;
+            fence_async_smem();
+            mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
+            mbar_expect_tx(&barP[q % NP], in ? HPB : 0u);
+            if (in) {
+                tma_load_4d(smd + (q % NA) * Z::HP, &mY, 0, x0 - 2, y0 - 2, K - 1, &barA[q % NA]);
+                tma_load_4d(smd + NA * Z::HP + (q % NP) * Z::HP, &mP, 0, x0 - 2, y0 - 2, K - 1, &barP[q % NP]);
+            }
+        };
+        if (tid == 0)
+            for (int t = 0; t < DI && t < T; ++t) issue(t);
+        for (int t = 0; t < T; ++t) {
+            const int K = za - 1 + t;
+            const uint32_t q = G + (uint32_t)t;
+            mbar_wait(&barA[q % NA], (q / NA) & 1);
+            mbar_wait(&barP[q % NP], (q / NP) & 1);
+            const bool in = K >= 1 && K <= m;
+            const uint32_t ya = sA + (q % NA) * HPB, pa = sP + (q % NP) * HPB;
+            if (in) {
+                // interior elements (stored when owned) ...
+                const bool own = K >= za && K < zb && act;
+                double* pout = a.Pnew + (int64_t)(K - 1) * sz;
+#pragma unroll
+                for (int j = 0; j < Z::NE; ++j) {
+                    const double v = fma(bet, ldsd(pa + el.h[j]), ldsd(ya + el.h[j]));
+                    stsd(ya + el.h[j], v);
+                    if (own && el.ij[j] >= 0) pout[el.gxy[j]] = v;
+                }
+                // ... and the halo ring (x = 0 or TX+1, or y = 0 or TY+1)
+                constexpr int NHALO = (2 * Z::HX + 2 * Z::TY) * BP;
+                for (int e = tid; e < NHALO; e += kZT) {
+                    const int n = e >> Z::LGB;
+                    int hx, hy;
+                    if (n < Z::HX) { hx = n; hy = 0; }
+                    else if (n < 2 * Z::HX) { hx = n - Z::HX; hy = Z::HY - 1; }
+                    else { const int r = n - 2 * Z::HX; hx = (r & 1) ? Z::HX - 1 : 0; hy = 1 + (r >> 1); }
+                    const uint32_t o = 8u * (uint32_t)((hy * Z::HX + hx) * BP + b);
+                    stsd(ya + o, fma(bet, ldsd(pa + o), ldsd(ya + o)));
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && t + DI < T) issue(t + DI);
+            // sigma on plane Kc = K - 1 (owned planes za .. zb-1)
+            if (t >= 2 && act) {
+                const int Kc = K - 1;
+                const uint32_t ym = sA + ((q - 2) % NA) * HPB, yc = sA + ((q - 1) % NA) * HPB;
+                const bool zm = Kc > 1, zpl = Kc < m;
+                const int bz0 = axis_block(g, Kc - 1, g.pz), bz1 = axis_block(g, Kc, g.pz);
+                const int bzu = bz0 == bz1 ? bz0 * pxy : -1;
+#pragma unroll
+                for (int j = 0; j < Z::NE; ++j) {
+                    if (el.ij[j] < 0) continue;
+                    const uint32_t o = el.h[j];
+                    const double pp = ldsd(yc + o);
+                    const double nb[6] = {ldsd(yc + o - 8 * BP), ldsd(yc + o + 8 * BP),
+                                          ldsd(yc + o - 8 * Z::HX * BP), ldsd(yc + o + 8 * Z::HX * BP),
+                                          zm ? ldsd(ym + o) : 0.0, zpl ? ldsd(ya + o) : 0.0};
+                    double qv;
+                    if (el.cxy[j] >= 0 && bzu >= 0) {
+                        qv = stencil_c(g, s_th[(el.cxy[j] + bzu) * BP + b], pp, nb);
+                    } else {
+                        const int n = (tid + j * kZT) >> Z::LGB;
+                        qv = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp, nb);
+                    }
+                    sig = fma(pp, qv, sig);
+                }
+            }
+        }
+        G += (uint32_t)T;
+    }
+    cgp_step5(a, sig);
+}
+
+// ===========================================================================
+// k_gsz: one red-black half-sweep of colour a.color (eq8, AMB-5/6).
+//   step t (plane K = za-1+t arrives): the sweep's nodes of plane K-1 are updated from
+//   their neighbours (all of the other colour, unchanged by this half-sweep) and stored
+// LAST: y^T r, y^T y over every owned node + RBCG Step 10 in the last CTA.
+// ===========================================================================
+template <int BP, bool LAST>
+__global__ void __launch_bounds__(kZT, 1)
+    k_gsz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mR, GSArgs a, ZPart zp) {
+    using Z = ZGeom<BP>;
+    constexpr int NA = Z::NA, NB = Z::DI + 1, DI = Z::DI;
+    extern __shared__ __align__(128) double smd[];
+    __shared__ __align__(8) uint64_t barA[NA], barB[NB];
+    if (a.done && ld_flag(a.done)) return;
+    const Geo& g = a.g;
+    const int m = g.m, tid = threadIdx.x, b = tid & (BP - 1);
+    double* s_th = smd + NA * Z::HP + NB * Z::IP;
+    for (int t = tid; t < g.Q * BP; t += kZT) s_th[t] = a.theta[t];
+    const bool hasr = a.Rhs != nullptr;
+    if (tid == 0) {
+        for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
+        for (int k = 0; k < NB; ++k) mbar_init(&barB[k], 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&mY);
+        if (hasr) tma_prefetch_desc(&mR);
+    }
+    const bool act = a.active[b] != 0;
+    const uint32_t sA = smem_u32(smd), sB = sA + 8u * NA * Z::HP;
+    const int64_t sz = (int64_t)m * m * BP;
+    const int pxy = g.px * g.py;
+    constexpr uint32_t HPB = 8u * Z::HP, IPB = 8u * Z::IP;
+    const double rconst = a.rconst;
+    uint32_t G = 0;
+    double yr = 0.0, yy = 0.0;
+    for (int u = blockIdx.x; u < zp.units; u += gridDim.x) {
+        int x0, y0, za, zb;
+        zunit(zp, m, u, Z::TX, Z::TY, x0, y0, za, zb);
+        const int T = zb - za + 2;
+        ZElems<BP> el;
+        el.init(g, x0, y0, tid);
+        __syncthreads();
+        // plane t: y haloed into A[q % NA]; r interior (owned planes) into B[q % NB]
+        auto issue = [&](int t) {
+            const int K = za - 1 + t;
+            const uint32_t q = G + (uint32_t)t;
+            const bool in = K >= 1 && K <= m, own = hasr && K >= za && K < zb;
+            fence_async_smem();
+            mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
+            mbar_expect_tx(&barB[q % NB], own ? IPB : 0u);
+            if (in) tma_load_4d(smd + (q % NA) * Z::HP, &mY, 0, x0 - 2, y0 - 2, K - 1, &barA[q % NA]);
+            if (own)
+                tma_load_4d(smd + NA * Z::HP + (q % NB) * Z::IP, &mR, 0, x0 - 1, y0 - 1, K - 1, &barB[q % NB]);
+        };
+        if (tid == 0)
+            for (int t = 0; t < DI && t < T; ++t) issue(t);
+        for (int t = 0; t < T; ++t) {
+            const int K = za - 1 + t;
+            const uint32_t q = G + (uint32_t)t;
+            mbar_wait(&barA[q % NA], (q / NA) & 1);
+            if (t >= 1) mbar_wait(&barB[(q - 1) % NB], ((q - 1) / NB) & 1);   // r of plane K-1
+            if (t >= 2 && act) {
+                const int Kc = K - 1;
+                const uint32_t ym = sA + ((q - 2) % NA) * HPB, yc = sA + ((q - 1) % NA) * HPB,
+                               yp = sA + (q % NA) * HPB;
+                const uint32_t rb = sB + ((q - 1) % NB) * IPB + 8u * tid;
+                const bool zm = Kc > 1, zpl = Kc < m;
+                const int bz0 = axis_block(g, Kc - 1, g.pz), bz1 = axis_block(g, Kc, g.pz);
+                const int bzu = bz0 == bz1 ? bz0 * pxy : -1;
+                double* yo = a.Y + (int64_t)(Kc - 1) * sz;
+#pragma unroll
+                for (int j = 0; j < Z::NE; ++j) {
+                    if (el.ij[j] < 0) continue;
+                    const uint32_t o = el.h[j];
+                    const double rh = hasr ? ldsd(rb + 8u * j * kZT) : rconst;
+                    if (((el.ij[j] + Kc) & 1) == a.color) {
+                        const double nb[6] = {ldsd(yc + o - 8 * BP), ldsd(yc + o + 8 * BP),
+                                              ldsd(yc + o - 8 * Z::HX * BP), ldsd(yc + o + 8 * Z::HX * BP),
+                                              zm ? ldsd(ym + o) : 0.0, zpl ? ldsd(yp + o) : 0.0};
+                        double v;
+                        if (el.cxy[j] >= 0 && bzu >= 0) {
+                            v = gs_c(g, s_th[(el.cxy[j] + bzu) * BP + b], rh, nb);
+                        } else {
+                            const int n = (tid + j * kZT) >> Z::LGB;
+                            v = gs_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, rh, nb);
+                        }
+                        yo[el.gxy[j]] = v;
+                        if (LAST) {
+                            yr = fma(v, rh, yr);
+                            yy = fma(v, v, yy);
+                        }
+                    } else if (LAST) {
+                        const double v = ldsd(yc + o);
+                        yr = fma(v, rh, yr);
+                        yy = fma(v, v, yy);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && t + DI < T) issue(t + DI);
+        }
+        G += (uint32_t)T;
+    }
+    if (LAST) gs_step10(a, yr, yy);
+}
+
+// ===========================================================================
+// k_xrz: RBCG Steps 6-7 for 3D grids: x += alpha p, r -= alpha A p.
+//   step t (plane K = za-1+t of p arrives): x, r of plane K are loaded into registers
+//   (consumed at step t+1), plane K-1 is updated and stored.
+// ===========================================================================
+template <int BP>
+__global__ void __launch_bounds__(kZT, 1)
+    k_xrz(const __grid_constant__ CUtensorMap mP, ProjArgs a, ZPart zp) {
+    using Z = ZGeom<BP>;
+    constexpr int NA = Z::NA, DI = Z::DI;
+    extern __shared__ __align__(128) double smd[];
+    __shared__ __align__(8) uint64_t barA[NA];
+    if (a.done && ld_flag(a.done)) return;
+    const Geo& g = a.g;
+    const int m = g.m, tid = threadIdx.x, b = tid & (BP - 1);
+    double* s_th = smd + NA * Z::HP;
+    for (int t = tid; t < g.Q * BP; t += kZT) s_th[t] = a.theta[t];
+    if (tid == 0) {
+        for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&mP);
+    }
+    const bool act = a.active[b] != 0;
+    const double al = a.alpha[b];
+    const uint32_t sA = smem_u32(smd);
+    const int64_t sz = (int64_t)m * m * BP;
+    const int pxy = g.px * g.py;
+    constexpr uint32_t HPB = 8u * Z::HP;
+    uint32_t G = 0;
+    for (int u = blockIdx.x; u < zp.units; u += gridDim.x) {
+        int x0, y0, za, zb;
+        zunit(zp, m, u, Z::TX, Z::TY, x0, y0, za, zb);
+        const int T = zb - za + 2;
+        ZElems<BP> el;
+        el.init(g, x0, y0, tid);
+        __syncthreads();
+        auto issue = [&](int t) {
+            const int K = za - 1 + t;
+            const uint32_t q = G + (uint32_t)t;
+            const bool in = K >= 1 && K <= m;
+            fence_async_smem();
+            mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
+            if (in) tma_load_4d(smd + (q % NA) * Z::HP, &mP, 0, x0 - 2, y0 - 2, K - 1, &barA[q % NA]);
+        };
+        if (tid == 0)
+            for (int t = 0; t < DI && t < T; ++t) issue(t);
+        double cx[Z::NE], cr[Z::NE];
+#pragma unroll
+        for (int j = 0; j < Z::NE; ++j) cx[j] = cr[j] = 0.0;
+        for (int t = 0; t < T; ++t) {
+            const int K = za - 1 + t;
+            const uint32_t q = G + (uint32_t)t;
+            // x, r of plane K (owned) into registers: used at step t+1
+            double nx[Z::NE], nr[Z::NE];
+            const bool ownK = act && K >= za && K < zb;
+            const int64_t pk = (int64_t)(K - 1) * sz;
+#pragma unroll
+            for (int j = 0; j < Z::NE; ++j) {
+                nx[j] = nr[j] = 0.0;
+                if (ownK && el.ij[j] >= 0) {
+                    nx[j] = a.X[pk + el.gxy[j]];
+                    nr[j] = a.R[pk + el.gxy[j]];
+                }
+            }
+            mbar_wait(&barA[q % NA], (q / NA) & 1);
+            if (t >= 2 && act) {
+                const int Kc = K - 1;
+                const uint32_t ym = sA + ((q - 2) % NA) * HPB, yc = sA + ((q - 1) % NA) * HPB,
+                               yp = sA + (q % NA) * HPB;
+                const bool zm = Kc > 1, zpl = Kc < m;
+                const int bz0 = axis_block(g, Kc - 1, g.pz), bz1 = axis_block(g, Kc, g.pz);
+                const int bzu = bz0 == bz1 ? bz0 * pxy : -1;
+                const int64_t pc = (int64_t)(Kc - 1) * sz;
+#pragma unroll
+                for (int j = 0; j < Z::NE; ++j) {
+                    if (el.ij[j] < 0) continue;
+                    const uint32_t o = el.h[j];
+                    const double pp = ldsd(yc + o);
+                    const double nb[6] = {ldsd(yc + o - 8 * BP), ldsd(yc + o + 8 * BP),
+                                          ldsd(yc + o - 8 * Z::HX * BP), ldsd(yc + o + 8 * Z::HX * BP),
+                                          zm ? ldsd(ym + o) : 0.0, zpl ? ldsd(yp + o) : 0.0};
+                    double qv;
+                    if (el.cxy[j] >= 0 && bzu >= 0) {
+                        qv = stencil_c(g, s_th[(el.cxy[j] + bzu) * BP + b], pp, nb);
+                    } else {
+                        const int n = (tid + j * kZT) >> Z::LGB;
+                        qv = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp, nb);
+                    }
+                    a.X[pc + el.gxy[j]] = fma(al, pp, cx[j]);
+                    a.R[pc + el.gxy[j]] = fma(-al, qv, cr[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < Z::NE; ++j) {
+                cx[j] = nx[j];
+                cr[j] = nr[j];
+            }
+            __syncthreads();
+            if (tid == 0 && t + DI < T) issue(t + DI);
+        }
+        G += (uint32_t)T;
+    }
+}
+
+}  // namespace rbs

@@ -1,0 +1,89 @@
+"""GPU parity of the 3D z-plane marches (paper_1804_06363_b200/csrc/zmarch.cuh: k_cgz,
+k_gsz, k_xrz fed by 4-D TMA tensor-map copies) -- RBCG Steps 5-7, 11 and the red-black
+half-sweeps (eq8, 269-275 algorithm2) on grids that span several (x, y)
+tiles, several z-segments and ragged tile edges in x, y and z, for every batch width
+(B_pad 8 / 16 / 32).  Against the oracle (criteria of tests/test_gpu_parity.py) and against
+the row-segment kernels they replace (RBS_DISABLE_V2 bit 16): per node the arithmetic is
+the same, only the order of the per-CTA partial sums differs, so the two GPU paths agree
+to rounding and take the same number of iterations."""
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import compare, oracle_basis, oracle_refs, rbs  # noqa: F401  (fixture)
+
+pytestmark = pytest.mark.gpu
+
+
+def _solver_pair(rbs, dim, m, blocks, res):
+    z = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    old = os.environ.get("RBS_DISABLE_V2")
+    os.environ["RBS_DISABLE_V2"] = "65536"          # read once at rbs_create
+    try:
+        r = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    finally:
+        if old is None:
+            del os.environ["RBS_DISABLE_V2"]
+        else:
+            os.environ["RBS_DISABLE_V2"] = old
+    return z, r
+
+
+# m = 37: B_pad 8 -> 2 x 5 tiles of 32 x 8 (ragged in x and y), 13 z-segments of 3 planes;
+# B_pad 16 -> 3 x 5 tiles of 16 x 8; B_pad 32 -> 3 x 10 tiles of 16 x 4 (ragged y)
+@pytest.mark.parametrize("m,blocks,n,B", [(37, (2, 2, 2), 12, 3), (37, (2, 3, 2), 16, 16),
+                                          (29, (2, 2, 3), 10, 27), (8, (2, 2, 2), 6, 5)])
+def test_zmarch_rbcg_matches_oracle_and_row_segments(orc, rbs, m, blocks, n, B):
+    g, res = oracle_basis(orc, 3, m, blocks, n, 24, 5)
+    z, r = _solver_pair(rbs, 3, m, blocks, res)
+    mus = 0.1 * 100 ** np.random.default_rng(31 + B).random((B, g.Q))
+    kw = dict(record_history=1, max_iter=20000)
+    oz = z.solve_batch(mus, **kw)
+    orow = r.solve_batch(mus, **kw)
+    assert list(oz["status"]) == list(orow["status"])
+    assert np.array_equal(oz["its"], orow["its"])
+    Xz, Xr = oz["X"].cpu().numpy(), orow["X"].cpu().numpy()
+    assert np.max(np.linalg.norm(Xz - Xr, axis=1) / np.linalg.norm(Xr, axis=1)) <= 1e-11
+    sample = list(range(min(B, 4)))
+    refs = oracle_refs(g, res["W"], res["ANq"], res["fn"], mus[sample], "rbcg", max_iter=20000)
+    compare(dict(oz, X=oz["X"][sample], status=[oz["status"][i] for i in sample], its=oz["its"][sample],
+                 a_n=oz["a_n"][sample], history=[oz["history"][i] for i in sample]),
+            g, res["W"], res["ANq"], res["fn"], mus[sample], "rbcg", refs=refs)
+
+
+@pytest.mark.parametrize("B", [8, 16, 32])
+def test_zmarch_fixed_iterations_bitwise_node_values(orc, rbs, B):
+    """Fixed-iteration RBCG (tol 0, 7 iterations) on a 41^3 grid: the z-march and the
+    row-segment path agree to rounding at every lane (the only difference is the order
+    of the CTA partial sums of sigma and y^T r)."""
+    g, res = oracle_basis(orc, 3, 41, (2, 2, 2), 8, 20, 9)
+    z, r = _solver_pair(rbs, 3, 41, (2, 2, 2), res)
+    mus = 0.1 * 100 ** np.random.default_rng(B).random((B, g.Q))
+    oz = z.solve_batch(mus, tol=0.0, max_iter=7)
+    orow = r.solve_batch(mus, tol=0.0, max_iter=7)
+    Xz, Xr = oz["X"].cpu().numpy(), orow["X"].cpu().numpy()
+    assert np.max(np.abs(Xz - Xr)) <= 1e-12 * np.max(np.abs(Xr))
+    ref = g.rbcg(res["W"], res["ANq"], res["fn"], mus[0], tol=0.0, max_iter=7)
+    assert np.linalg.norm(Xz[0] - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+
+
+@pytest.mark.parametrize("smoother,sweeps", [(0, 2), (1, 3)])
+def test_zmarch_smoother_variants(orc, rbs, smoother, sweeps):
+    """forward RB-GS with two sweeps and symmetric with three: the half-sweep sequence
+    of k_gsz launches (colours, LAST epilogue) against the oracle."""
+    g, res = oracle_basis(orc, 3, 19, (2, 2, 2), 8, 20, 3)
+    s = rbs.Solver(3, 19, (2, 2, 2)).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = 0.1 * 100 ** np.random.default_rng(4).random((6, g.Q))
+    out = s.solve_batch(mus, smoother=smoother, sweeps=sweeps, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbcg", smoother=smoother, sweeps=sweeps)
+
+
+def test_zmarch_rbi(orc, rbs):
+    """stand-alone RBI in 3D (the half-sweeps run as k_gsz; Step 2's residual keeps the
+    projection pass) against the oracle."""
+    g, res = oracle_basis(orc, 3, 15, (2, 2, 2), 10, 20, 2)
+    s = rbs.Solver(3, 15, (2, 2, 2)).load_basis(res["W"], res["ANq"], res["fn"])
+    mus = 0.1 * 100 ** np.random.default_rng(8).random((5, g.Q))
+    out = s.solve_batch(mus, method=rbs.RBS_RBI, max_iter=500000, record_history=1)
+    compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbi", max_iter=500000)

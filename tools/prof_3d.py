@@ -19,6 +19,9 @@ ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--faces", action="store_true")
 ap.add_argument("--n", type=int, default=20)
 ap.add_argument("--ntrain", type=int, default=64)
+ap.add_argument("--random-basis", action="store_true",
+                help="random orthonormal W (timing only: fixed-iteration solves, no greedy build)")
+ap.add_argument("--B", type=int, default=16)
 a = ap.parse_args()
 blocks = (2, 2, 2)
 rng = np.random.default_rng(5)
@@ -27,14 +30,20 @@ if a.faces:
     s = rbs.Solver(3, a.m, faces=cases.faces_from_blocks(3, a.m, blocks))
 else:
     s = rbs.Solver(3, a.m, blocks)
-if os.environ.get("PROF3D_BASIS") and os.path.exists(os.environ["PROF3D_BASIS"]):
+if a.random_basis:
+    g = torch.Generator(device="cuda").manual_seed(1)
+    W = torch.randn(a.m ** 3, a.n, device="cuda", dtype=torch.float64, generator=g)
+    W, _ = torch.linalg.qr(W)
+    s.load_basis(W)
+    del W
+elif os.environ.get("PROF3D_BASIS") and os.path.exists(os.environ["PROF3D_BASIS"]):
     d = torch.load(os.environ["PROF3D_BASIS"], weights_only=False)
     s.load_basis(d["W"], d["ANq"], d["fn"])
 else:
     gr = s.build_greedy(tr, a.n)
     if os.environ.get("PROF3D_BASIS"):
         torch.save({"W": gr["W"].cpu(), "ANq": gr["ANq"], "fn": gr["fn"]}, os.environ["PROF3D_BASIS"])
-mus = 0.1 * 100 ** rng.random((16, 8))
+mus = 0.1 * 100 ** rng.random((a.B, 8))
 torch.cuda.nvtx.range_push("solve")      # ncu --nvtx --nvtx-include "solve/" captures only this
 out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False)
 torch.cuda.nvtx.range_pop()
