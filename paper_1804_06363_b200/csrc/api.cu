@@ -1276,11 +1276,12 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         int nl = 1;
         if (mode == MODE_CG && g.dim == 3 && use_active && Bp <= 32 && !(v2off & 8)) {
             // two passes: x, r update in row segments, then W^T r, ||r||^2 on the new r
-            CUtensorMap mpz;
-            if (zm3 && zsm(2) && zmap_h(&mpz, P)) {   // z-plane march, p tile with halo by tensor map
-                if (Bp == 8) k_xrz<8><<<zgrid, kZT, zsm(2), st>>>(mpz, a, zpt);
-                else if (Bp == 16) k_xrz<16><<<zgrid, kZT, zsm(2), st>>>(mpz, a, zpt);
-                else k_xrz<32><<<zgrid, kZT, zsm(2), st>>>(mpz, a, zpt);
+            CUtensorMap mpz, mxz, mrz;
+            if (zm3 && zsm(2) && zmap_h(&mpz, P) && zmap_i(&mxz, a.X) && zmap_i(&mrz, a.R)) {
+                // z-plane march: p tile with halo, x and r tiles by tensor maps
+                if (Bp == 8) k_xrz<8><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                else if (Bp == 16) k_xrz<16><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                else k_xrz<32><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
             } else if (g.faces) k_xr3r<4, true><<<nctf, kFlat, fsm, st>>>(a, lgB);
             else k_xr3r<4, false><<<nctf, kFlat, fsm, st>>>(a, lgB);
             ProjArgs b2 = a;

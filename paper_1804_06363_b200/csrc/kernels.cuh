@@ -620,11 +620,11 @@ __global__ void k_labels_to_faces(const uint8_t* __restrict__ lab, int dim, int 
 
 // LAST pass of the smoother: y^T r, y^T y partials of this CTA and RBCG Step 10
 // (beta = y_{k+1}^T r_{k+1} / y_k^T r_k) in the last CTA (AMB-11)
-__device__ __forceinline__ void gs_step10(GSArgs& a, double yr, double yy) {
+__device__ __forceinline__ void gs_step10(const GSArgs& a, double yr, double yy) {
     __shared__ double s_a[kFlat], s_b[kFlat];
     __shared__ double s_yr[kMaxBatch], s_yy[kMaxBatch];
     __shared__ int s_last;
-    SolveState& s = a.s;
+    const SolveState& s = a.s;
     s_a[threadIdx.x] = yr;
     s_b[threadIdx.x] = yy;
     __syncthreads();
@@ -895,11 +895,11 @@ constexpr int kCgpUnroll = 2;
 
 // sigma partials of this CTA and RBCG Step 5 (alpha = rho / p^T A p) with
 // the MAXIT / CURVATURE checks in the last CTA (AMB-11)
-__device__ __forceinline__ void cgp_step5(CGPArgs& a, double sig) {
+__device__ __forceinline__ void cgp_step5(const CGPArgs& a, double sig) {
     __shared__ double s_a[kFlat];
     __shared__ double s_sig[kMaxBatch];
     __shared__ int s_last;
-    SolveState& s = a.s;
+    const SolveState& s = a.s;
     s_a[threadIdx.x] = sig;
     __syncthreads();
     if (threadIdx.x < a.Bp) {

@@ -17,11 +17,15 @@
 //           LAST: y^T r, y^T y and RBCG Step 10
 //   k_xrz   RBCG Steps 6-7: x += alpha p, r -= alpha A p
 //
-// Per node the arithmetic is exactly that of the row-segment kernels (node_kappa,
-// stencil_apply, gs_value, neighbour order -x,+x,-y,+y,-z,+z), so node values are
-// bitwise the same; only the order of the per-CTA partial sums differs.  Thermal-block
-// operator on a full grid only (no mesh slabs, no face coefficients): those keep the
-// row-segment kernels.
+// Per node the stencil is that of the row-segment kernels (node_kappa, stencil_apply,
+// neighbour order -x,+x,-y,+y,-z,+z; bitwise the same values); a Gauss-Seidel update of
+// a node inside one block is the direct form y = h^2/(6 theta) b + (sum of the six
+// neighbours)/6 with the h^2/(6 theta) table in shared memory (no division; within an ulp
+// of gs_value, AMB-4), block-interface nodes keep gs_value.  The half-sweep maps the
+// CTA's threads onto the sweep's colour only (every lane of a warp updates a node).
+// Kernel arguments are __grid_constant__ (the out-of-line interface path takes their
+// address without a local-memory copy).  Thermal-block operator on a full grid only (no
+// mesh slabs, no face coefficients): those keep the row-segment kernels.
 #pragma once
 #include <cuda.h>
 
@@ -63,11 +67,12 @@ struct ZPart {
 template <int BP>
 __host__ __device__ constexpr size_t zsmem_bytes(int kind, int Q) {
     // kind 0: k_cgz (y ring NA + p_old ring DI, haloed), 1: k_gsz (y ring NA haloed + r ring
-    // DI+1 interior), 2: k_xrz (p ring NA haloed)
+    // DI+1 interior + the h^2/(6 theta) table), 2: k_xrz (p ring of 5 haloed + x, r rings of 3
+    // interior); + theta table
     using Z = ZGeom<BP>;
     return (size_t)8 * (kind == 0 ? (Z::NA + Z::DI) * Z::HP
-                        : kind == 1 ? Z::NA * Z::HP + (Z::DI + 1) * Z::IP
-                                    : Z::NA * Z::HP) +
+                        : kind == 1 ? Z::NA * Z::HP + (Z::DI + 1) * Z::IP + Q * BP
+                                    : 5 * Z::HP + 6 * Z::IP) +
            (size_t)Q * BP * 8;
 }
 
@@ -83,32 +88,6 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// per-thread view of its NE interior elements of the current tile (loop invariant over z)
-template <int BP>
-struct ZElems {
-    using Z = ZGeom<BP>;
-    uint32_t h[Z::NE];       // byte offset of the element in a haloed plane
-    int64_t gxy[Z::NE];      // element offset within a global plane: ((J-1) m + I-1) Bp + b
-    int ij[Z::NE];           // I + J (colour), -1: outside the grid
-    int cxy[Z::NE];          // bx + by*px of the node's cells if they agree in x and y, else -1
-    __device__ __forceinline__ void init(const Geo& g, int x0, int y0, int tid) {
-        const int b = tid & (BP - 1);
-#pragma unroll
-        for (int j = 0; j < Z::NE; ++j) {
-            const int n = (tid + j * kZT) >> Z::LGB;
-            const int ix = n % Z::TX, iy = n / Z::TX;
-            const int I = x0 + ix, J = y0 + iy;
-            h[j] = 8u * (uint32_t)(((iy + 1) * Z::HX + ix + 1) * BP + b);
-            gxy[j] = ((int64_t)(J - 1) * g.m + (I - 1)) * BP + b;
-            const bool in = I <= g.m && J <= g.m;
-            ij[j] = in ? I + J : -1;
-            const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
-            const int by0 = axis_block(g, J - 1, g.py), by1 = axis_block(g, J, g.py);
-            cxy[j] = (bx0 == bx1 && by0 == by1) ? bx0 + by0 * g.px : -1;
-        }
-    }
-};
-
 __device__ __forceinline__ void zunit(const ZPart& p, int m, int u, int TX, int TY, int& x0, int& y0, int& za,
                                       int& zb) {
     const int tiles = p.ntx * p.nty;
@@ -120,38 +99,97 @@ __device__ __forceinline__ void zunit(const ZPart& p, int m, int u, int TX, int 
     zb = min(m + 1, za + p.zlen);
 }
 
-// the 7-point stencil / Gauss-Seidel value with all six edge coefficients equal to c:
-// the same operations in the same order as stencil_apply<3> / gs_value<3> with k[e] = c
-// (bitwise equal), without an addressable coefficient array (no local-memory traffic)
-__device__ __forceinline__ double stencil_c(const Geo& g, double c, double vp, const double* nb) {
+// the 7-point stencil with all six edge coefficients equal to c: the operations of
+// stencil_apply<3> with k[e] = c in the same order (bitwise equal), no coefficient array
+__device__ __forceinline__ double stencil_c(double scale, double c, double vp, const double* nb) {
     double s = c * (vp - nb[0]);
 #pragma unroll
     for (int e = 1; e < 6; ++e) s = fma(c, vp - nb[e], s);
-    return g.scale * s;
-}
-__device__ __forceinline__ double gs_c(const Geo& g, double c, double rhs, const double* nb) {
-    double num = g.h2 * rhs, den = c;
-    num = fma(c, nb[0], num);
-#pragma unroll
-    for (int e = 1; e < 6; ++e) {
-        num = fma(c, nb[e], num);
-        den += c;
-    }
-    return num / den;
+    return scale * s;
 }
 // general node (block interface): cell-averaged coefficients out of line
+// (neighbour values by value: the caller's arrays stay in registers)
 __device__ __noinline__ double stencil_general(const Geo& g, const double* s_th, int ldb, int b, int I, int J,
-                                               int K, double vp, const double* nb) {
+                                               int K, double vp, double n0, double n1, double n2, double n3,
+                                               double n4, double n5) {
     double k[6];
+    const double nb[6] = {n0, n1, n2, n3, n4, n5};
     node_kappa<3>(g, s_th, ldb, b, I, J, K, k);
     return stencil_apply<3>(g, k, vp, nb);
 }
 __device__ __noinline__ double gs_general(const Geo& g, const double* s_th, int ldb, int b, int I, int J, int K,
-                                          double rhs, const double* nb) {
+                                          double rhs, double n0, double n1, double n2, double n3, double n4,
+                                          double n5) {
     double k[6];
+    const double nb[6] = {n0, n1, n2, n3, n4, n5};
     node_kappa<3>(g, s_th, ldb, b, I, J, K, k);
     return gs_value<3>(g, k, rhs, nb);
 }
+
+// per-thread view of its NE interior elements of the current tile (loop invariant over z)
+template <int BP>
+struct ZElems {
+    using Z = ZGeom<BP>;
+    uint32_t h[Z::NE];       // byte offset of the element in a haloed plane
+    int gxy[Z::NE];          // element offset within a global plane: ((J-1) m + I-1) Bp + b (< 2^31)
+    int cxy[Z::NE];          // bx + by*px of the node's cells if they agree in x and y, -1 if not,
+                             // -2: node outside the grid
+    __device__ __forceinline__ bool in(int j) const { return cxy[j] != -2; }
+    __device__ __forceinline__ void init(const Geo& g, int x0, int y0, int tid) {
+        const int b = tid & (BP - 1);
+#pragma unroll
+        for (int j = 0; j < Z::NE; ++j) {
+            const int n = (tid + j * kZT) >> Z::LGB;
+            const int ix = n % Z::TX, iy = n / Z::TX;
+            const int I = x0 + ix, J = y0 + iy;
+            h[j] = 8u * (uint32_t)(((iy + 1) * Z::HX + ix + 1) * BP + b);
+            gxy[j] = ((J - 1) * g.m + (I - 1)) * BP + b;
+            const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
+            const int by0 = axis_block(g, J - 1, g.py), by1 = axis_block(g, J, g.py);
+            cxy[j] = (I > g.m || J > g.m) ? -2 : (bx0 == bx1 && by0 == by1) ? bx0 + by0 * g.px : -1;
+        }
+    }
+};
+
+// colour-compact view for a half-sweep: the TX*TY/2 nodes of one red-black colour of a
+// plane tile, NC = NE/2 per thread.  Colour node cn = slot + (kZT/BP) j sits in tile row
+// iy = cn / (TX/2) at column ix = 2 (cn % (TX/2)) + ((P + iy) & 1), where P = 0 / 1 is the
+// colour's column parity in row 0 of that plane; both parities are kept (they alternate
+// with the plane) -- the other parity is the other colour of the same plane (LAST's dots)
+template <int BP>
+struct ZColour {
+    using Z = ZGeom<BP>;
+    static constexpr int NC = Z::NE / 2;
+    uint32_t h[2][NC];       // haloed-plane byte offset
+    uint32_t ri[2][NC];      // interior-plane byte offset (the r ring)
+    int gxy[2][NC];          // < 2^31: element offset within a global plane
+    int cxy[2][NC];          // uniform x/y block index, -1: interface, -2: outside the grid
+    __device__ __forceinline__ void init(const Geo& g, int x0, int y0, int tid) {
+        const int b = tid & (BP - 1);
+#pragma unroll
+        for (int P = 0; P < 2; ++P)
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                const int cn = (tid >> Z::LGB) + j * (kZT / BP);
+                const int iy = cn / (Z::TX / 2);
+                const int ix = 2 * (cn % (Z::TX / 2)) + ((P + iy) & 1);
+                const int I = x0 + ix, J = y0 + iy;
+                h[P][j] = 8u * (uint32_t)(((iy + 1) * Z::HX + ix + 1) * BP + b);
+                ri[P][j] = 8u * (uint32_t)((iy * Z::TX + ix) * BP + b);
+                gxy[P][j] = ((J - 1) * g.m + (I - 1)) * BP + b;
+                const int bx0 = axis_block(g, I - 1, g.px), bx1 = axis_block(g, I, g.px);
+                const int by0 = axis_block(g, J - 1, g.py), by1 = axis_block(g, J, g.py);
+                cxy[P][j] = (I > g.m || J > g.m) ? -2 : (bx0 == bx1 && by0 == by1) ? bx0 + by0 * g.px : -1;
+            }
+    }
+    // grid coordinates of colour element j at parity P (the interface path)
+    __device__ __forceinline__ void coords(int x0, int y0, int tid, int P, int j, int& I, int& J) const {
+        const int cn = (tid >> Z::LGB) + j * (kZT / BP);
+        const int iy = cn / (Z::TX / 2);
+        I = x0 + 2 * (cn % (Z::TX / 2)) + ((P + iy) & 1);
+        J = y0 + iy;
+    }
+};
 
 // ===========================================================================
 // k_cgz: RBCG Step 11 + Step 5 for 3D grids.
@@ -162,7 +200,8 @@ __device__ __noinline__ double gs_general(const Geo& g, const double* s_th, int 
 // ===========================================================================
 template <int BP>
 __global__ void __launch_bounds__(kZT, 1)
-    k_cgz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP, CGPArgs a, ZPart zp) {
+    k_cgz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
+          const __grid_constant__ CGPArgs a, const ZPart zp) {
     using Z = ZGeom<BP>;
     constexpr int NA = Z::NA, NP = Z::DI, DI = Z::DI;
     extern __shared__ __align__(128) double smd[];
@@ -170,8 +209,10 @@ __global__ void __launch_bounds__(kZT, 1)
     if (a.done && ld_flag(a.done)) return;
     const Geo& g = a.g;
     const int m = g.m, tid = threadIdx.x, b = tid & (BP - 1);
+    const double scale = g.scale;
     double* s_th = smd + (NA + NP) * Z::HP;
     for (int t = tid; t < g.Q * BP; t += kZT) s_th[t] = a.theta[t];
+    const uint32_t sth = smem_u32(s_th) + 8u * b;      // this lane's column of the theta table
     if (tid == 0) {
         for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
         for (int k = 0; k < NP; ++k) mbar_init(&barP[k], 1);
@@ -181,6 +222,7 @@ __global__ void __launch_bounds__(kZT, 1)
     }
     const bool act = a.active[b] != 0;
     const double bet = a.beta[b];
+    double* const Pnew = a.Pnew;
     const uint32_t sA = smem_u32(smd), sP = sA + 8u * NA * Z::HP;
     const int64_t sz = (int64_t)m * m * BP;
     const int pxy = g.px * g.py;
@@ -218,12 +260,12 @@ __global__ void __launch_bounds__(kZT, 1)
             if (in) {
                 // interior elements (stored when owned) ...
                 const bool own = K >= za && K < zb && act;
-                double* pout = a.Pnew + (int64_t)(K - 1) * sz;
+                double* pout = Pnew + (int64_t)(K - 1) * sz;
 #pragma unroll
                 for (int j = 0; j < Z::NE; ++j) {
                     const double v = fma(bet, ldsd(pa + el.h[j]), ldsd(ya + el.h[j]));
                     stsd(ya + el.h[j], v);
-                    if (own && el.ij[j] >= 0) pout[el.gxy[j]] = v;
+                    if (own && el.in(j)) pout[el.gxy[j]] = v;
                 }
                 // ... and the halo ring (x = 0 or TX+1, or y = 0 or TY+1)
                 constexpr int NHALO = (2 * Z::HX + 2 * Z::TY) * BP;
@@ -246,22 +288,46 @@ __global__ void __launch_bounds__(kZT, 1)
                 const bool zm = Kc > 1, zpl = Kc < m;
                 const int bz0 = axis_block(g, Kc - 1, g.pz), bz1 = axis_block(g, Kc, g.pz);
                 const int bzu = bz0 == bz1 ? bz0 * pxy : -1;
+                // all shared-memory loads of the thread's elements first, then the arithmetic
+                // (uniform-block nodes), then the rare block-interface nodes out of line
+                // per chunk of two elements: the shared-memory loads first, then the arithmetic
+                // (uniform-block nodes), then the rare block-interface nodes out of line
 #pragma unroll
-                for (int j = 0; j < Z::NE; ++j) {
-                    if (el.ij[j] < 0) continue;
-                    const uint32_t o = el.h[j];
-                    const double pp = ldsd(yc + o);
-                    const double nb[6] = {ldsd(yc + o - 8 * BP), ldsd(yc + o + 8 * BP),
-                                          ldsd(yc + o - 8 * Z::HX * BP), ldsd(yc + o + 8 * Z::HX * BP),
-                                          zm ? ldsd(ym + o) : 0.0, zpl ? ldsd(ya + o) : 0.0};
-                    double qv;
-                    if (el.cxy[j] >= 0 && bzu >= 0) {
-                        qv = stencil_c(g, s_th[(el.cxy[j] + bzu) * BP + b], pp, nb);
-                    } else {
-                        const int n = (tid + j * kZT) >> Z::LGB;
-                        qv = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp, nb);
+                for (int c = 0; c < Z::NE; c += 2) {
+                    double pp[2], nb[2][6], qv[2];
+                    bool slow = false;
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int j = c + i;
+                        const uint32_t o = el.h[j];
+                        pp[i] = ldsd(yc + o);
+                        nb[i][0] = ldsd(yc + o - 8 * BP);
+                        nb[i][1] = ldsd(yc + o + 8 * BP);
+                        nb[i][2] = ldsd(yc + o - 8 * Z::HX * BP);
+                        nb[i][3] = ldsd(yc + o + 8 * Z::HX * BP);
+                        const double zlo = ldsd(ym + o), zhi = ldsd(ya + o);
+                        nb[i][4] = zm ? zlo : 0.0;
+                        nb[i][5] = zpl ? zhi : 0.0;
+                        const bool fast = el.cxy[j] >= 0 && bzu >= 0;
+                        qv[i] = ldsd(sth + 8u * (uint32_t)((fast ? el.cxy[j] + bzu : 0) * BP));
+                        slow |= el.in(j) && !fast;
                     }
-                    sig = fma(pp, qv, sig);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) qv[i] = stencil_c(scale, qv[i], pp[i], nb[i]);
+                    if (slow) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) {
+                            const int j = c + i;
+                            if (el.in(j) && !(el.cxy[j] >= 0 && bzu >= 0)) {
+                                const int n = (tid + j * kZT) >> Z::LGB;
+                                qv[i] = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp[i],
+                                                        nb[i][0], nb[i][1], nb[i][2], nb[i][3], nb[i][4], nb[i][5]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        if (el.in(c + i)) sig = fma(pp[i], qv[i], sig);
                 }
             }
         }
@@ -273,21 +339,30 @@ __global__ void __launch_bounds__(kZT, 1)
 // ===========================================================================
 // k_gsz: one red-black half-sweep of colour a.color (eq8, AMB-5/6).
 //   step t (plane K = za-1+t arrives): the sweep's nodes of plane K-1 are updated from
-//   their neighbours (all of the other colour, unchanged by this half-sweep) and stored
-// LAST: y^T r, y^T y over every owned node + RBCG Step 10 in the last CTA.
+//   their neighbours (all of the other colour, unchanged by this half-sweep) and stored.
+//   The threads map onto the sweep's colour only (ZColour); LAST also runs the other
+//   colour's y^T r, y^T y terms, then RBCG Step 10 in the last CTA.
 // ===========================================================================
 template <int BP, bool LAST>
 __global__ void __launch_bounds__(kZT, 1)
-    k_gsz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mR, GSArgs a, ZPart zp) {
+    k_gsz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mR,
+          const __grid_constant__ GSArgs a, const ZPart zp) {
     using Z = ZGeom<BP>;
-    constexpr int NA = Z::NA, NB = Z::DI + 1, DI = Z::DI;
+    using C = ZColour<BP>;
+    constexpr int NA = Z::NA, NB = Z::DI + 1, DI = Z::DI, NC = C::NC;
     extern __shared__ __align__(128) double smd[];
     __shared__ __align__(8) uint64_t barA[NA], barB[NB];
     if (a.done && ld_flag(a.done)) return;
     const Geo& g = a.g;
     const int m = g.m, tid = threadIdx.x, b = tid & (BP - 1);
     double* s_th = smd + NA * Z::HP + NB * Z::IP;
-    for (int t = tid; t < g.Q * BP; t += kZT) s_th[t] = a.theta[t];
+    double* s_t6 = s_th + g.Q * BP;            // h^2 / (6 theta): the uniform-block GS weight
+    for (int t = tid; t < g.Q * BP; t += kZT) {
+        const double v = a.theta[t];
+        s_th[t] = v;
+        s_t6[t] = g.h2 / (6.0 * v);
+    }
+    const uint32_t st6 = smem_u32(s_t6) + 8u * b;
     const bool hasr = a.Rhs != nullptr;
     if (tid == 0) {
         for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
@@ -297,10 +372,13 @@ __global__ void __launch_bounds__(kZT, 1)
         if (hasr) tma_prefetch_desc(&mR);
     }
     const bool act = a.active[b] != 0;
+    const int color = a.color;
+    double* const Y = a.Y;
     const uint32_t sA = smem_u32(smd), sB = sA + 8u * NA * Z::HP;
     const int64_t sz = (int64_t)m * m * BP;
     const int pxy = g.px * g.py;
     constexpr uint32_t HPB = 8u * Z::HP, IPB = 8u * Z::IP;
+    constexpr double kSixth = 1.0 / 6.0;
     const double rconst = a.rconst;
     uint32_t G = 0;
     double yr = 0.0, yy = 0.0;
@@ -308,7 +386,7 @@ __global__ void __launch_bounds__(kZT, 1)
         int x0, y0, za, zb;
         zunit(zp, m, u, Z::TX, Z::TY, x0, y0, za, zb);
         const int T = zb - za + 2;
-        ZElems<BP> el;
+        C el;
         el.init(g, x0, y0, tid);
         __syncthreads();
         // plane t: y haloed into A[q % NA]; r interior (owned planes) into B[q % NB]
@@ -334,36 +412,68 @@ __global__ void __launch_bounds__(kZT, 1)
                 const int Kc = K - 1;
                 const uint32_t ym = sA + ((q - 2) % NA) * HPB, yc = sA + ((q - 1) % NA) * HPB,
                                yp = sA + (q % NA) * HPB;
-                const uint32_t rb = sB + ((q - 1) % NB) * IPB + 8u * tid;
+                const uint32_t rb = sB + ((q - 1) % NB) * IPB;
                 const bool zm = Kc > 1, zpl = Kc < m;
                 const int bz0 = axis_block(g, Kc - 1, g.pz), bz1 = axis_block(g, Kc, g.pz);
                 const int bzu = bz0 == bz1 ? bz0 * pxy : -1;
-                double* yo = a.Y + (int64_t)(Kc - 1) * sz;
+                double* yo = Y + (int64_t)(Kc - 1) * sz;
+                // the sweep colour's column parity in row 0 of this plane tile
+                const int P = (color - x0 - y0 - Kc) & 1;
+                // loads of the thread's colour elements first, the arithmetic after, the rare
+                // block-interface nodes out of line
+                double nb[NC][6], rh[NC], v[NC];
+                bool slow = false;
 #pragma unroll
-                for (int j = 0; j < Z::NE; ++j) {
-                    if (el.ij[j] < 0) continue;
-                    const uint32_t o = el.h[j];
-                    const double rh = hasr ? ldsd(rb + 8u * j * kZT) : rconst;
-                    if (((el.ij[j] + Kc) & 1) == a.color) {
-                        const double nb[6] = {ldsd(yc + o - 8 * BP), ldsd(yc + o + 8 * BP),
-                                              ldsd(yc + o - 8 * Z::HX * BP), ldsd(yc + o + 8 * Z::HX * BP),
-                                              zm ? ldsd(ym + o) : 0.0, zpl ? ldsd(yp + o) : 0.0};
-                        double v;
-                        if (el.cxy[j] >= 0 && bzu >= 0) {
-                            v = gs_c(g, s_th[(el.cxy[j] + bzu) * BP + b], rh, nb);
-                        } else {
-                            const int n = (tid + j * kZT) >> Z::LGB;
-                            v = gs_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, rh, nb);
+                for (int j = 0; j < NC; ++j) {
+                    const uint32_t o = P ? el.h[1][j] : el.h[0][j];
+                    const int cx = P ? el.cxy[1][j] : el.cxy[0][j];
+                    rh[j] = hasr ? ldsd(rb + (P ? el.ri[1][j] : el.ri[0][j])) : rconst;
+                    nb[j][0] = ldsd(yc + o - 8 * BP);
+                    nb[j][1] = ldsd(yc + o + 8 * BP);
+                    nb[j][2] = ldsd(yc + o - 8 * Z::HX * BP);
+                    nb[j][3] = ldsd(yc + o + 8 * Z::HX * BP);
+                    const double zlo = ldsd(ym + o), zhi = ldsd(yp + o);
+                    nb[j][4] = zm ? zlo : 0.0;
+                    nb[j][5] = zpl ? zhi : 0.0;
+                    const bool fast = cx >= 0 && bzu >= 0;
+                    v[j] = ldsd(st6 + 8u * (uint32_t)((fast ? cx + bzu : 0) * BP));
+                    slow |= cx == -1 || (cx >= 0 && bzu < 0);
+                }
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    // direct form inside one block: (h^2 b + theta sum nb) / (6 theta)
+                    const double sn = ((nb[j][0] + nb[j][1]) + (nb[j][2] + nb[j][3])) + (nb[j][4] + nb[j][5]);
+                    v[j] = fma(v[j], rh[j], sn * kSixth);
+                }
+                if (slow) {
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) {
+                        const int cx = P ? el.cxy[1][j] : el.cxy[0][j];
+                        if (cx == -1 || (cx >= 0 && bzu < 0)) {
+                            int I, J;
+                            el.coords(x0, y0, tid, P, j, I, J);
+                            v[j] = gs_general(g, s_th, BP, b, I, J, Kc, rh[j], nb[j][0], nb[j][1], nb[j][2], nb[j][3],
+                                              nb[j][4], nb[j][5]);
                         }
-                        yo[el.gxy[j]] = v;
-                        if (LAST) {
-                            yr = fma(v, rh, yr);
-                            yy = fma(v, v, yy);
-                        }
-                    } else if (LAST) {
-                        const double v = ldsd(yc + o);
-                        yr = fma(v, rh, yr);
-                        yy = fma(v, v, yy);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    if ((P ? el.cxy[1][j] : el.cxy[0][j]) == -2) continue;
+                    yo[P ? el.gxy[1][j] : el.gxy[0][j]] = v[j];
+                    if (LAST) {
+                        yr = fma(v[j], rh[j], yr);
+                        yy = fma(v[j], v[j], yy);
+                    }
+                }
+                if (LAST) {           // the other colour: unchanged values
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) {
+                        const double w = ldsd(yc + (P ? el.h[0][j] : el.h[1][j]));
+                        const double r2 = hasr ? ldsd(rb + (P ? el.ri[0][j] : el.ri[1][j])) : rconst;
+                        if ((P ? el.cxy[0][j] : el.cxy[1][j]) == -2) continue;
+                        yr = fma(w, r2, yr);
+                        yy = fma(w, w, yy);
                     }
                 }
             }
@@ -377,32 +487,42 @@ __global__ void __launch_bounds__(kZT, 1)
 
 // ===========================================================================
 // k_xrz: RBCG Steps 6-7 for 3D grids: x += alpha p, r -= alpha A p.
-//   step t (plane K = za-1+t of p arrives): x, r of plane K are loaded into registers
-//   (consumed at step t+1), plane K-1 is updated and stored.
+//   step t (plane K = za-1+t of p arrives, with the x and r tiles of plane K-1): plane K-1
+//   is updated and stored.  p: haloed ring of kXNA slots; x, r: interior rings of 3 slots;
+//   all three are issued 2 planes ahead.
 // ===========================================================================
+constexpr int kXDI = 2, kXNA = kXDI + 3, kXNR = 3;
 template <int BP>
 __global__ void __launch_bounds__(kZT, 1)
-    k_xrz(const __grid_constant__ CUtensorMap mP, ProjArgs a, ZPart zp) {
+    k_xrz(const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mX,
+          const __grid_constant__ CUtensorMap mR, const __grid_constant__ ProjArgs a, const ZPart zp) {
     using Z = ZGeom<BP>;
-    constexpr int NA = Z::NA, DI = Z::DI;
+    constexpr int NA = kXNA, NR = kXNR, DI = kXDI;
     extern __shared__ __align__(128) double smd[];
-    __shared__ __align__(8) uint64_t barA[NA];
+    __shared__ __align__(8) uint64_t barA[NA], barX[NR];
     if (a.done && ld_flag(a.done)) return;
     const Geo& g = a.g;
     const int m = g.m, tid = threadIdx.x, b = tid & (BP - 1);
-    double* s_th = smd + NA * Z::HP;
+    const double scale = g.scale;
+    double* s_th = smd + NA * Z::HP + 2 * NR * Z::IP;
     for (int t = tid; t < g.Q * BP; t += kZT) s_th[t] = a.theta[t];
+    const uint32_t sth = smem_u32(s_th) + 8u * b;
     if (tid == 0) {
         for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
+        for (int k = 0; k < NR; ++k) mbar_init(&barX[k], 1);
         mbar_fence_init();
         tma_prefetch_desc(&mP);
+        tma_prefetch_desc(&mX);
+        tma_prefetch_desc(&mR);
     }
     const bool act = a.active[b] != 0;
     const double al = a.alpha[b];
-    const uint32_t sA = smem_u32(smd);
+    double* const X = a.X;
+    double* const R = a.R;
+    const uint32_t sA = smem_u32(smd), sX = sA + 8u * NA * Z::HP, sR = sX + 8u * NR * Z::IP;
     const int64_t sz = (int64_t)m * m * BP;
     const int pxy = g.px * g.py;
-    constexpr uint32_t HPB = 8u * Z::HP;
+    constexpr uint32_t HPB = 8u * Z::HP, IPB = 8u * Z::IP;
     uint32_t G = 0;
     for (int u = blockIdx.x; u < zp.units; u += gridDim.x) {
         int x0, y0, za, zb;
@@ -414,63 +534,77 @@ __global__ void __launch_bounds__(kZT, 1)
         auto issue = [&](int t) {
             const int K = za - 1 + t;
             const uint32_t q = G + (uint32_t)t;
-            const bool in = K >= 1 && K <= m;
+            const bool in = K >= 1 && K <= m, own = K >= za && K < zb;
             fence_async_smem();
             mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
+            mbar_expect_tx(&barX[q % NR], own ? 2u * IPB : 0u);
             if (in) tma_load_4d(smd + (q % NA) * Z::HP, &mP, 0, x0 - 2, y0 - 2, K - 1, &barA[q % NA]);
+            if (own) {
+                tma_load_4d(smd + NA * Z::HP + (q % NR) * Z::IP, &mX, 0, x0 - 1, y0 - 1, K - 1, &barX[q % NR]);
+                tma_load_4d(smd + NA * Z::HP + NR * Z::IP + (q % NR) * Z::IP, &mR, 0, x0 - 1, y0 - 1, K - 1,
+                            &barX[q % NR]);
+            }
         };
         if (tid == 0)
             for (int t = 0; t < DI && t < T; ++t) issue(t);
-        double cx[Z::NE], cr[Z::NE];
-#pragma unroll
-        for (int j = 0; j < Z::NE; ++j) cx[j] = cr[j] = 0.0;
         for (int t = 0; t < T; ++t) {
             const int K = za - 1 + t;
             const uint32_t q = G + (uint32_t)t;
-            // x, r of plane K (owned) into registers: used at step t+1
-            double nx[Z::NE], nr[Z::NE];
-            const bool ownK = act && K >= za && K < zb;
-            const int64_t pk = (int64_t)(K - 1) * sz;
-#pragma unroll
-            for (int j = 0; j < Z::NE; ++j) {
-                nx[j] = nr[j] = 0.0;
-                if (ownK && el.ij[j] >= 0) {
-                    nx[j] = a.X[pk + el.gxy[j]];
-                    nr[j] = a.R[pk + el.gxy[j]];
-                }
-            }
             mbar_wait(&barA[q % NA], (q / NA) & 1);
+            if (t >= 1) mbar_wait(&barX[(q - 1) % NR], ((q - 1) / NR) & 1);   // x, r of plane K-1
             if (t >= 2 && act) {
                 const int Kc = K - 1;
                 const uint32_t ym = sA + ((q - 2) % NA) * HPB, yc = sA + ((q - 1) % NA) * HPB,
                                yp = sA + (q % NA) * HPB;
+                const uint32_t xs = sX + ((q - 1) % NR) * IPB + 8u * tid, rs = sR + ((q - 1) % NR) * IPB + 8u * tid;
                 const bool zm = Kc > 1, zpl = Kc < m;
                 const int bz0 = axis_block(g, Kc - 1, g.pz), bz1 = axis_block(g, Kc, g.pz);
                 const int bzu = bz0 == bz1 ? bz0 * pxy : -1;
-                const int64_t pc = (int64_t)(Kc - 1) * sz;
+                double* const Xc = X + (int64_t)(Kc - 1) * sz;
+                double* const Rc = R + (int64_t)(Kc - 1) * sz;
 #pragma unroll
-                for (int j = 0; j < Z::NE; ++j) {
-                    if (el.ij[j] < 0) continue;
-                    const uint32_t o = el.h[j];
-                    const double pp = ldsd(yc + o);
-                    const double nb[6] = {ldsd(yc + o - 8 * BP), ldsd(yc + o + 8 * BP),
-                                          ldsd(yc + o - 8 * Z::HX * BP), ldsd(yc + o + 8 * Z::HX * BP),
-                                          zm ? ldsd(ym + o) : 0.0, zpl ? ldsd(yp + o) : 0.0};
-                    double qv;
-                    if (el.cxy[j] >= 0 && bzu >= 0) {
-                        qv = stencil_c(g, s_th[(el.cxy[j] + bzu) * BP + b], pp, nb);
-                    } else {
-                        const int n = (tid + j * kZT) >> Z::LGB;
-                        qv = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp, nb);
+                for (int c = 0; c < Z::NE; c += 2) {
+                    double pp[2], nb[2][6], qv[2], xv[2], rv[2];
+                    bool slow = false;
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int j = c + i;
+                        const uint32_t o = el.h[j];
+                        pp[i] = ldsd(yc + o);
+                        nb[i][0] = ldsd(yc + o - 8 * BP);
+                        nb[i][1] = ldsd(yc + o + 8 * BP);
+                        nb[i][2] = ldsd(yc + o - 8 * Z::HX * BP);
+                        nb[i][3] = ldsd(yc + o + 8 * Z::HX * BP);
+                        const double zlo = ldsd(ym + o), zhi = ldsd(yp + o);
+                        nb[i][4] = zm ? zlo : 0.0;
+                        nb[i][5] = zpl ? zhi : 0.0;
+                        xv[i] = ldsd(xs + 8u * j * kZT);
+                        rv[i] = ldsd(rs + 8u * j * kZT);
+                        const bool fast = el.cxy[j] >= 0 && bzu >= 0;
+                        qv[i] = ldsd(sth + 8u * (uint32_t)((fast ? el.cxy[j] + bzu : 0) * BP));
+                        slow |= el.in(j) && !fast;
                     }
-                    a.X[pc + el.gxy[j]] = fma(al, pp, cx[j]);
-                    a.R[pc + el.gxy[j]] = fma(-al, qv, cr[j]);
-                }
-            }
 #pragma unroll
-            for (int j = 0; j < Z::NE; ++j) {
-                cx[j] = nx[j];
-                cr[j] = nr[j];
+                    for (int i = 0; i < 2; ++i) qv[i] = stencil_c(scale, qv[i], pp[i], nb[i]);
+                    if (slow) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) {
+                            const int j = c + i;
+                            if (el.in(j) && !(el.cxy[j] >= 0 && bzu >= 0)) {
+                                const int n = (tid + j * kZT) >> Z::LGB;
+                                qv[i] = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp[i],
+                                                        nb[i][0], nb[i][1], nb[i][2], nb[i][3], nb[i][4], nb[i][5]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int j = c + i;
+                        if (!el.in(j)) continue;
+                        Xc[el.gxy[j]] = fma(al, pp[i], xv[i]);
+                        Rc[el.gxy[j]] = fma(-al, qv[i], rv[i]);
+                    }
+                }
             }
             __syncthreads();
             if (tid == 0 && t + DI < T) issue(t + DI);

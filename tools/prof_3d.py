@@ -22,6 +22,7 @@ ap.add_argument("--ntrain", type=int, default=64)
 ap.add_argument("--random-basis", action="store_true",
                 help="random orthonormal W (timing only: fixed-iteration solves, no greedy build)")
 ap.add_argument("--B", type=int, default=16)
+ap.add_argument("--prof-only", action="store_true", help="skip the graph-mode timing (ncu captures)")
 a = ap.parse_args()
 blocks = (2, 2, 2)
 rng = np.random.default_rng(5)
@@ -49,6 +50,9 @@ out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False)
 torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 prof = {k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]] for k, v in out["profile"].items() if v[1]}
+if a.prof_only:
+    print(json.dumps(prof))
+    sys.exit(0)
 # graph-mode iteration time (the way bench.py runs): a fixed 200-iteration solve
 s.solve_batch(mus, tol=0.0, max_iter=50, want_a_n=False)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
