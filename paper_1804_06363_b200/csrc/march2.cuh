@@ -915,15 +915,19 @@ namespace rbs {
 // k_wtr<BP>: the projection W^T v and ||v||^2 as a stream over a contiguous node
 // range per CTA (any dimension; the 3D second half of K2, eq5).
 // Chunks of kWtCH nodes of W (ldw doubles per node) and v (BP per node) arrive by
-// TMA bulk copies into a kWtD-slot ring (mbarriers); warps own (8-basis x 8-query)
-// tiles and split the chunk's k-steps when there are fewer tiles than warps; the
-// k-parts and the per-thread ||v||^2 terms are summed in a fixed order.  Partials
-// go to part[b][j][col] exactly like k_proj (stage 2: k_reduce_solve).
+// TMA bulk copies into a kWtD-slot ring (mbarriers, kWtD-1 chunks in flight); each
+// chunk of v is first copied to a padded buffer (row stride BP+4: the DMMA B-fragment
+// reads of a half-warp then hit 16 distinct 8-byte banks; the dense rows are 4-way
+// conflicted) while ||v||^2 is accumulated; warps own (8-basis x 8-query) tiles with
+// two accumulator chains (even / odd k-steps) and split the chunk's k-steps when there
+// are fewer tiles than warps; chains, k-parts and the per-thread ||v||^2 terms are summed
+// in a fixed order.  Partials go to part[b][j][col] exactly like k_proj (stage 2:
+// k_reduce_solve).
 // ===========================================================================
-constexpr int kWtD = 3;
+constexpr int kWtD = 4;
 
 inline size_t wtr_smem_bytes(int Bp, int ldw, int ch) {
-    return (size_t)kWtD * ch * (ldw + Bp) * 8 + 256;
+    return (size_t)kWtD * ch * (ldw + Bp) * 8 + (size_t)ch * (Bp + 4) * 8 + 256;
 }
 
 template <int BP, int kWtCH>
@@ -936,6 +940,7 @@ __global__ void __launch_bounds__(kMT, 2) k_wtr(ProjArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int npad = a.npad, ldw = a.ldw, ntile = npad >> 3;
     constexpr int NBT = BP / 8;
+    constexpr int LDV = BP + 4;                               // padded v row
     const int T = ntile * NBT;                                // output tiles
     const int KP = T >= kNW ? 1 : min(kWtCH / 4, kNW / T);   // k-parts per tile (k-steps split)
     const int64_t N = a.g.N;
@@ -944,6 +949,7 @@ __global__ void __launch_bounds__(kMT, 2) k_wtr(ProjArgs a) {
     const int slotW = kWtCH * ldw, slotV = kWtCH * BP;
     double* wr = smd;
     double* vr = smd + kWtD * slotW;
+    double* vp = vr + kWtD * slotV;                           // padded copy of the current v chunk
     if (tid == 0) {
         for (int k = 0; k < kWtD; ++k) mbar_init(&bars[k], 1);
         mbar_fence_init();
@@ -966,9 +972,9 @@ __global__ void __launch_bounds__(kMT, 2) k_wtr(ProjArgs a) {
     const int tslot = warp % (T * KP >= kNW ? kNW : T * KP);
     const bool wact = warp < T * KP || T >= kNW;
     const int kp = T >= kNW ? 0 : tslot / T;
-    double acc[2][2];
+    double acc[2][2], acc2[2][2];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = 0.0;
+    for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = acc2[u][0] = acc2[u][1] = 0.0;
     double rr = 0.0;
     for (int c = 0; c < nch; ++c) {
         if (tid == 0 && c + kWtD - 1 < nch) issue(c + kWtD - 1);
@@ -978,28 +984,41 @@ __global__ void __launch_bounds__(kMT, 2) k_wtr(ProjArgs a) {
         const int cnt = (int)(n1 - i0 < (int64_t)kWtCH ? n1 - i0 : (int64_t)kWtCH);
         const double* W = wr + sl * slotW;
         const double* V = vr + sl * slotV;
-        // ||v||^2: element tid of the chunk (fixed node/query per thread)
-        for (int e = tid; e < kWtCH * BP; e += kMT)     // fixed element set per thread
-            if (e / BP < cnt) {
-                const double v = V[e];
-                rr = fma(v, v, rr);
-            }
+        // padded copy + ||v||^2: element e (fixed node/query per thread); rows past cnt are 0
+        for (int e = tid; e < kWtCH * BP; e += kMT) {
+            const int nd = e / BP, q = e - nd * BP;
+            const double v = nd < cnt ? V[e] : 0.0;
+            rr = fma(v, v, rr);
+            vp[nd * LDV + q] = v;
+        }
+        __syncthreads();
         if (wact) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {      // T <= 32 tiles: at most two per warp
                 const int t = T >= kNW ? warp + u * kNW : (u == 0 ? tslot % T : T);
                 if (t >= T) continue;
                 const int jt = t / NBT, bt = t - jt * NBT;
-                for (int ks = kp; ks < kWtCH / 4; ks += KP) {
+                for (int ks = kp; ks < kWtCH / 4; ks += 2 * KP) {
                     const int nd = ks * 4 + (lane & 3);           // node of this lane's k
-                    const bool in = nd < cnt;
-                    const double wa = in ? W[nd * ldw + jt * 8 + (lane >> 2)] : 0.0;   // A: basis x node
-                    const double vb = in ? V[nd * BP + bt * 8 + (lane >> 2)] : 0.0;    // B: node x query
+                    const double wa = nd < cnt ? W[nd * ldw + jt * 8 + (lane >> 2)] : 0.0;   // A: basis x node
+                    const double vb = vp[nd * LDV + bt * 8 + (lane >> 2)];                    // B: node x query
                     dmma_8x8x4(acc[u][0], acc[u][1], wa, vb);
+                    const int ks2 = ks + KP;
+                    if (ks2 < kWtCH / 4) {
+                        const int nd2 = ks2 * 4 + (lane & 3);
+                        const double wa2 = nd2 < cnt ? W[nd2 * ldw + jt * 8 + (lane >> 2)] : 0.0;
+                        const double vb2 = vp[nd2 * LDV + bt * 8 + (lane >> 2)];
+                        dmma_8x8x4(acc2[u][0], acc2[u][1], wa2, vb2);
+                    }
                 }
             }
         }
-        __syncthreads();   // slot sl is reissued kWtD - 1 chunks later
+        __syncthreads();   // slot sl is reissued kWtD - 1 chunks later; vp is rewritten
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {          // the two chains, fixed order
+        acc[u][0] += acc2[u][0];
+        acc[u][1] += acc2[u][1];
     }
     // ---- fixed-order combine: k-parts of each tile, then partial columns -----
     const int rows = npad + 1;
