@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--shard", default=None, choices=["weak", "strong"],
                    help="weak: every rank its own query set (c1/c2 default); strong: one fixed set split "
                         "over the ranks (c3/c4 default)")
+    p.add_argument("--order", default="contrast", choices=["contrast", "given"],
+                   help="query-to-batch schedule: group queries of similar coefficient contrast "
+                        "(paper_1804_06363_b200.dist.batch_order) or keep the seeded order")
     p.add_argument("--precond", default="post", choices=["post", "sym"],
                    help="RBCG preconditioner: the paper's post-smoothed RBI (default) or the symmetric "
                         "two-level RBI (NEXT(3), RBS_PRECOND_SYM)")
@@ -538,7 +541,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1804_06363_b200 as rbs
-    from paper_1804_06363_b200.dist import broadcast_basis, gather_counts, query_shard
+    from paper_1804_06363_b200.dist import batch_order, broadcast_basis, gather_counts, query_shard
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -580,6 +583,8 @@ def main():
         mus = query_set(c, nq_tot)[q0:q1]
         nq = q1 - q0
         Bq = min(c.B, nq)
+    if a.order == "contrast":     # batches of similar contrast (dist.batch_order): lanes finish together
+        mus = mus[batch_order(mus, Bq)]
     batches = [mus[i:i + Bq] for i in range(0, nq, Bq)]
     nb = len(batches)
     # S concurrent batch streams (DESIGN.md §7 "Concurrent batches"): batch k runs on stream
@@ -763,7 +768,7 @@ def main():
                        "queries_total": (a.queries or c.n_queries) if shard == "strong" else nq * world,
                        "step": "one pass over the rank's query shard" if shard == "strong" else "one batch of B queries",
                        "parallelism": f"query-shard x{world} ({shard})" if world > 1 else "1 GPU",
-                       "concurrent_batches": S,
+                       "concurrent_batches": S, "batch_order": a.order,
                        "l2": l2,
                        "its_min_med_max": [min(its), int(np.median(its)), max(its)],
                        "true_relres_max": max(trr),

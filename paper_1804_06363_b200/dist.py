@@ -52,3 +52,21 @@ def gather_counts(its, status, group=None):
     dist.all_gather(out_i, its, group=group)
     dist.all_gather(out_s, status, group=group)
     return torch.cat(out_i), torch.cat(out_s)
+
+
+def batch_order(mus, B: int):
+    """Host-side batch scheduling: the query order that groups queries of similar
+    coefficient contrast (max / min of the parameters, the spread of the diffusion
+    coefficient) into the same batch of B lanes.  A batch runs until its slowest
+    query converges (frozen lanes still stream through every pass), and the contrast
+    is a cheap proxy for a query's RBCG iteration count (correlation ~0.6 on c1), so
+    sorted batches waste fewer lane-iterations.  Every query's iterates are
+    independent of its batch (DESIGN.md AMB-26): only the schedule changes.
+    Returns a permutation of range(len(mus)), stable for equal contrast."""
+    import numpy as np
+    mus = np.asarray(mus, dtype=np.float64)
+    if mus.ndim != 2 or B < 1:
+        raise ValueError("mus must be (n_queries, P), B >= 1")
+    lm = np.log(np.maximum(mus, np.finfo(np.float64).tiny))
+    contrast = lm.max(axis=1) - lm.min(axis=1)
+    return np.argsort(contrast, kind="stable")

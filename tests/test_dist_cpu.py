@@ -84,3 +84,21 @@ def test_gloo_broadcast_and_gather_world2():
     for _, _, its, st in res:
         assert its == list(range(100, 110))
         assert st == [0] * 5 + [1] * 5
+
+
+def test_batch_order_is_a_contrast_sorted_permutation():
+    """the batch scheduler returns a permutation that sorts the queries by the spread of
+    their log-parameters (stable), so equal queries keep their seeded order"""
+    import numpy as np
+    from paper_1804_06363_b200.dist import batch_order
+    rng = np.random.default_rng(3)
+    mus = 0.1 * 100 ** rng.random((50, 9))
+    mus[7] = mus[3]
+    p = batch_order(mus, 8)
+    assert sorted(p.tolist()) == list(range(50))
+    lm = np.log(mus[p])
+    c = lm.max(1) - lm.min(1)
+    assert np.all(np.diff(c) >= 0)
+    assert p.tolist().index(3) < p.tolist().index(7)
+    with pytest.raises(ValueError):
+        batch_order(mus[0], 8)
