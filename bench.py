@@ -503,7 +503,9 @@ def run_c5(a, world, rank, local):
         tot_ms = sum(v[0] for v in prof.values())
         line["kernels"] = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
                                "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
-        iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)
+        # one K1 (k_cgp class) per RBCG iteration; the symmetric preconditioner launches the
+        # projection class twice per iteration (K2 and the residual-projection)
+        iter_us = 1e3 * tot_ms / max(prof["k_cgp"][1], 1)
         # minimum bytes per batch-iteration: the fused schedule's 80 B + 16n / B per node-query
         # (DESIGN.md §7); the symmetric two-level preconditioner's passes (3D flat schedule: K1,
         # K2, y = 0, 3 pre + 3 post half-sweeps, residual-projection, prolongation) 200 B + 24n / B

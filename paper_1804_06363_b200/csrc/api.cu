@@ -315,12 +315,16 @@ constexpr size_t kZMaxDyn = 217 * 1024;
 template <int BP>
 void set_attrs_z() {
     auto cap = [](size_t b) { return (int)std::min(b, kZMaxDyn); };
-    cudaFuncSetAttribute(k_cgz<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap(zsmem_bytes<BP>(0, RBS_MAX_Q)));
-    cudaFuncSetAttribute(k_gsz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         cap(zsmem_bytes<BP>(1, RBS_MAX_Q)));
-    cudaFuncSetAttribute(k_gsz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         cap(zsmem_bytes<BP>(1, RBS_MAX_Q)));
-    cudaFuncSetAttribute(k_xrz<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap(zsmem_bytes<BP>(2, RBS_MAX_Q)));
+    const int c0 = cap(zsmem_bytes<BP>(0, RBS_MAX_Q)), c1 = cap(zsmem_bytes<BP>(1, RBS_MAX_Q)),
+              c2 = cap(zsmem_bytes<BP>(2, RBS_MAX_Q));
+    cudaFuncSetAttribute(k_cgz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c0);
+    cudaFuncSetAttribute(k_cgz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c0);
+    cudaFuncSetAttribute(k_gsz<BP, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
+    cudaFuncSetAttribute(k_gsz<BP, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
+    cudaFuncSetAttribute(k_gsz<BP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
+    cudaFuncSetAttribute(k_gsz<BP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
+    cudaFuncSetAttribute(k_xrz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
+    cudaFuncSetAttribute(k_xrz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
 }
 
 // cudaFuncSetAttribute applies to the current device only: once per device
@@ -1094,10 +1098,11 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     const std::vector<int> seq = color_seq(o->smoother, o->sweeps);
     const int pgrid = grid_for(((g.N + 7) / 8) * (Bp / 8), 8, ctx->num_sms * 16);
 
-    // 3D z-plane marches fed by TMA tensor maps (zmarch.cuh): thermal-block operator on a
-    // full grid, B_pad 8 / 16 / 32 (RBS_DISABLE_V2 bit 16 keeps the row-segment kernels)
-    const bool zm3 = g.dim == 3 && !g.faces && g.kofs == 0 && g.mz == g.m && (Bp == 8 || Bp == 16 || Bp == 32) &&
-                     !(v2off & 65536) && tmap_encoder() != nullptr;
+    // 3D z-plane marches fed by TMA tensor maps (zmarch.cuh): full grid, B_pad 8 / 16 / 32, thermal
+    // blocks or face coefficients (RBS_DISABLE_V2 bit 16 keeps the row-segment kernels, bit 17 for faces)
+    const bool zm3 = g.dim == 3 && g.kofs == 0 && g.mz == g.m && (Bp == 8 || Bp == 16 || Bp == 32) &&
+                     !(v2off & 65536) && !(g.faces && (v2off & 131072)) && tmap_encoder() != nullptr;
+    const bool zf = g.faces != nullptr;   // face-coefficient instantiations (AMB-23)
     const int ztx = Bp == 8 ? ZShape<8>::TX : Bp == 16 ? ZShape<16>::TX : ZShape<32>::TX;
     const int zty = Bp == 8 ? ZShape<8>::TY : Bp == 16 ? ZShape<16>::TY : ZShape<32>::TY;
     ZPart zpt{};
@@ -1209,16 +1214,15 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 else k_gs<2, false><<<nctf, kFlat, fsm, st>>>(a);
             } else if (zm3 && a.color >= 0 && zsm(1) && zmap_h(&my, Yv) && zmap_i(&mr, rhs ? rhs : Yv)) {
                 // z-plane march: y tile with halo + r tile per plane by tensor-map copies
-                if (Bp == 8) {
-                    if (l) k_gsz<8, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
-                    else k_gsz<8, false><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
-                } else if (Bp == 16) {
-                    if (l) k_gsz<16, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
-                    else k_gsz<16, false><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
-                } else {
-                    if (l) k_gsz<32, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
-                    else k_gsz<32, false><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt);
-                }
+#define RBS_GSZ(BPV, L, F) k_gsz<BPV, L, F><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt)
+#define RBS_GSZ2(BPV) \
+    if (zf) { if (l) RBS_GSZ(BPV, true, true); else RBS_GSZ(BPV, false, true); } \
+    else { if (l) RBS_GSZ(BPV, true, false); else RBS_GSZ(BPV, false, false); }
+                if (Bp == 8) { RBS_GSZ2(8) }
+                else if (Bp == 16) { RBS_GSZ2(16) }
+                else { RBS_GSZ2(32) }
+#undef RBS_GSZ2
+#undef RBS_GSZ
             } else if (Bp <= 32 && !(v2off & 8) && a.color >= 0) {   // row pencils (x in registers)
                 // 4-node row segments, all loads of a segment in flight (128 registers,
                 // one CTA per SM: measured 2.2x the element-per-thread k_gs at 127^3, B = 16)
@@ -1279,9 +1283,16 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             CUtensorMap mpz, mxz, mrz;
             if (zm3 && zsm(2) && zmap_h(&mpz, P) && zmap_i(&mxz, a.X) && zmap_i(&mrz, a.R)) {
                 // z-plane march: p tile with halo, x and r tiles by tensor maps
-                if (Bp == 8) k_xrz<8><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
-                else if (Bp == 16) k_xrz<16><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
-                else k_xrz<32><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                if (Bp == 8) {
+                    if (zf) k_xrz<8, true><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                    else k_xrz<8, false><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                } else if (Bp == 16) {
+                    if (zf) k_xrz<16, true><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                    else k_xrz<16, false><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                } else {
+                    if (zf) k_xrz<32, true><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                    else k_xrz<32, false><<<zgrid, kZT, zsm(2), st>>>(mpz, mxz, mrz, a, zpt);
+                }
             } else if (g.faces) k_xr3r<4, true><<<nctf, kFlat, fsm, st>>>(a, lgB);
             else k_xr3r<4, false><<<nctf, kFlat, fsm, st>>>(a, lgB);
             ProjArgs b2 = a;
@@ -1329,9 +1340,16 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         } else if (g.dim == 2) k_cgp<2><<<nctf, kFlat, fsm, st>>>(a);
         else if (zm3 && zsm(0) && zmap_h(&zmy, L.Y) && zmap_h(&zmp, Pold)) {
             // one z-plane march: p = y + beta p_old on the haloed tiles, sigma = p^T A p
-            if (Bp == 8) k_cgz<8><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
-            else if (Bp == 16) k_cgz<16><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
-            else k_cgz<32><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+            if (Bp == 8) {
+                if (zf) k_cgz<8, true><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+                else k_cgz<8, false><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+            } else if (Bp == 16) {
+                if (zf) k_cgz<16, true><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+                else k_cgz<16, false><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+            } else {
+                if (zf) k_cgz<32, true><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+                else k_cgz<32, false><<<zgrid, kZT, zsm(0), st>>>(zmy, zmp, a, zpt);
+            }
         } else if (Bp <= 32 && !(v2off & 8)) {      // two passes: stream p_new, then sigma in row segments
             const int64_t nb2 = (int64_t)g.N * Bp / 2;
             k_pnew3<<<(unsigned)std::min<int64_t>((nb2 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(
@@ -1352,15 +1370,18 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     // the red-black half-sweep that follows every prolongation (none: Jacobi / no sweeps)
     const int first_col = (!jac && !seq.empty() && !(v2off & 32768)) ? seq[0] : -1;
     const bool use_march = g.dim == 2 && seq.size() <= (size_t)kMaxSweeps && !jac && !g.faces && !sym && !pr;
+    // use_e = false: no prolongation in the pass (y0 = Xold, prolongated beforehand by k_prolong):
+    // no W ring, no E tiles, the tensor warps only copy the x_old rows
     auto march = [&](const double* Xold, double* Yv, const double* rhs, double rconst, bool last,
-                     int init) {
+                     int init, bool use_e = true) {
         SmoothMarchArgs a{};
         const int TX = march_tx(Bp);
-        a.g = g; a.Bp = Bp; a.npad = npad; a.ldw = ctx->ldw; a.part = march_part(g, TX, ctx->num_sms);
+        a.g = g; a.Bp = Bp; a.npad = use_e ? npad : 0; a.ldw = use_e ? ctx->ldw : 0;
+        a.part = march_part(g, TX, ctx->num_sms);
         a.W = ctx->Wi; a.E = L.E; a.Xold = Xold; a.Rhs = rhs; a.rconst = rconst; a.Y = Yv;
         a.theta = L.theta; a.active = L.active; a.S = (int)seq.size();
         for (size_t t = 0; t < seq.size(); ++t) a.seq[t] = seq[t];
-        a.has_e = npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
+        a.has_e = use_e && npad > 0; a.last = last; a.init = init; a.s = S; a.done = done;
         pb(RBS_K_GS);
         const size_t kMaxDyn = (size_t)kSmooth2MaxDyn;
         // strip 32 with the 3-row W ring; else strip 32 with a 2-row ring (prefetch distance
@@ -1368,15 +1389,15 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         // at strip 24); else strip 24
         int var = 0, TX2 = 32;
         const bool hr = rhs != nullptr, ax = Xold != nullptr;
-        size_t sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 3).total;
+        size_t sm2 = Smooth2Smem(32, a.S, Bp, a.ldw, Q, hr, ax, a.npad, 3).total;
         if (sm2 > kMaxDyn) {
             var = 1;
-            sm2 = Smooth2Smem(32, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 2).total;
+            sm2 = Smooth2Smem(32, a.S, Bp, a.ldw, Q, hr, ax, a.npad, 2).total;
         }
         if (sm2 > kMaxDyn || (v2off & 128)) {
             var = 2;
             TX2 = 24;
-            sm2 = Smooth2Smem(24, a.S, Bp, ctx->ldw, Q, hr, ax, npad, 3).total;
+            sm2 = Smooth2Smem(24, a.S, Bp, a.ldw, Q, hr, ax, a.npad, 3).total;
         }
         if (!(v2off & 1) && Bp <= 32 && a.S <= 3 && sm2 <= kMaxDyn) {
             // v2: lagged one-barrier-per-row pipeline (march2.cuh)

@@ -23,9 +23,10 @@
 // neighbours)/6 with the h^2/(6 theta) table in shared memory (no division; within an ulp
 // of gs_value, AMB-4), block-interface nodes keep gs_value.  The half-sweep maps the
 // CTA's threads onto the sweep's colour only (every lane of a warp updates a node).
-// Kernel arguments are __grid_constant__ (the out-of-line interface path takes their
-// address without a local-memory copy).  Thermal-block operator on a full grid only (no
-// mesh slabs, no face coefficients): those keep the row-segment kernels.
+// FACES instantiations take the face-coefficient operator (AMB-23) with the coefficients
+// of every node loaded inline.  Kernel arguments are __grid_constant__ (the out-of-line interface path takes their
+// address without a local-memory copy).  Full grid only (mesh slabs keep the row-segment
+// kernels).
 #pragma once
 #include <cuda.h>
 
@@ -198,7 +199,7 @@ struct ZColour {
 //     the owned interior nodes are stored to Pnew
 //   then sigma += p^T A p on plane K-1 (slots of K-2, K-1, K)
 // ===========================================================================
-template <int BP>
+template <int BP, bool FACES>
 __global__ void __launch_bounds__(kZT, 1)
     k_cgz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
           const __grid_constant__ CGPArgs a, const ZPart zp) {
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(kZT, 1)
                         const double zlo = ldsd(ym + o), zhi = ldsd(ya + o);
                         nb[i][4] = zm ? zlo : 0.0;
                         nb[i][5] = zpl ? zhi : 0.0;
-                        const bool fast = el.cxy[j] >= 0 && bzu >= 0;
+                        const bool fast = !FACES && el.cxy[j] >= 0 && bzu >= 0;
                         qv[i] = ldsd(sth + 8u * (uint32_t)((fast ? el.cxy[j] + bzu : 0) * BP));
                         slow |= el.in(j) && !fast;
                     }
@@ -318,10 +319,17 @@ __global__ void __launch_bounds__(kZT, 1)
 #pragma unroll
                         for (int i = 0; i < 2; ++i) {
                             const int j = c + i;
-                            if (el.in(j) && !(el.cxy[j] >= 0 && bzu >= 0)) {
+                            if (el.in(j) && (FACES || !(el.cxy[j] >= 0 && bzu >= 0))) {
                                 const int n = (tid + j * kZT) >> Z::LGB;
-                                qv[i] = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp[i],
-                                                        nb[i][0], nb[i][1], nb[i][2], nb[i][3], nb[i][4], nb[i][5]);
+                                if (FACES) {      // face coefficients (AMB-23), inline
+                                    double k[6];
+                                    node_kappa_faces<3>(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, k);
+                                    qv[i] = stencil_apply<3>(g, k, pp[i], nb[i]);
+                                } else {
+                                    qv[i] = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc,
+                                                            pp[i], nb[i][0], nb[i][1], nb[i][2], nb[i][3], nb[i][4],
+                                                            nb[i][5]);
+                                }
                             }
                         }
                     }
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(kZT, 1)
 //   The threads map onto the sweep's colour only (ZColour); LAST also runs the other
 //   colour's y^T r, y^T y terms, then RBCG Step 10 in the last CTA.
 // ===========================================================================
-template <int BP, bool LAST>
+template <int BP, bool LAST, bool FACES>
 __global__ void __launch_bounds__(kZT, 1)
     k_gsz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mR,
           const __grid_constant__ GSArgs a, const ZPart zp) {
@@ -435,9 +443,9 @@ __global__ void __launch_bounds__(kZT, 1)
                     const double zlo = ldsd(ym + o), zhi = ldsd(yp + o);
                     nb[j][4] = zm ? zlo : 0.0;
                     nb[j][5] = zpl ? zhi : 0.0;
-                    const bool fast = cx >= 0 && bzu >= 0;
+                    const bool fast = !FACES && cx >= 0 && bzu >= 0;
                     v[j] = ldsd(st6 + 8u * (uint32_t)((fast ? cx + bzu : 0) * BP));
-                    slow |= cx == -1 || (cx >= 0 && bzu < 0);
+                    slow |= cx != -2 && !fast;
                 }
 #pragma unroll
                 for (int j = 0; j < NC; ++j) {
@@ -449,11 +457,17 @@ __global__ void __launch_bounds__(kZT, 1)
 #pragma unroll
                     for (int j = 0; j < NC; ++j) {
                         const int cx = P ? el.cxy[1][j] : el.cxy[0][j];
-                        if (cx == -1 || (cx >= 0 && bzu < 0)) {
+                        if (cx != -2 && (FACES || !(cx >= 0 && bzu >= 0))) {
                             int I, J;
                             el.coords(x0, y0, tid, P, j, I, J);
-                            v[j] = gs_general(g, s_th, BP, b, I, J, Kc, rh[j], nb[j][0], nb[j][1], nb[j][2], nb[j][3],
-                                              nb[j][4], nb[j][5]);
+                            if (FACES) {          // face coefficients (AMB-23), inline
+                                double k[6];
+                                node_kappa_faces<3>(g, s_th, BP, b, I, J, Kc, k);
+                                v[j] = gs_value<3>(g, k, rh[j], nb[j]);
+                            } else {
+                                v[j] = gs_general(g, s_th, BP, b, I, J, Kc, rh[j], nb[j][0], nb[j][1], nb[j][2],
+                                                  nb[j][3], nb[j][4], nb[j][5]);
+                            }
                         }
                     }
                 }
@@ -492,7 +506,7 @@ __global__ void __launch_bounds__(kZT, 1)
 //   all three are issued 2 planes ahead.
 // ===========================================================================
 constexpr int kXDI = 2, kXNA = kXDI + 3, kXNR = 3;
-template <int BP>
+template <int BP, bool FACES>
 __global__ void __launch_bounds__(kZT, 1)
     k_xrz(const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mX,
           const __grid_constant__ CUtensorMap mR, const __grid_constant__ ProjArgs a, const ZPart zp) {
@@ -580,7 +594,7 @@ __global__ void __launch_bounds__(kZT, 1)
                         nb[i][5] = zpl ? zhi : 0.0;
                         xv[i] = ldsd(xs + 8u * j * kZT);
                         rv[i] = ldsd(rs + 8u * j * kZT);
-                        const bool fast = el.cxy[j] >= 0 && bzu >= 0;
+                        const bool fast = !FACES && el.cxy[j] >= 0 && bzu >= 0;
                         qv[i] = ldsd(sth + 8u * (uint32_t)((fast ? el.cxy[j] + bzu : 0) * BP));
                         slow |= el.in(j) && !fast;
                     }
@@ -590,10 +604,17 @@ __global__ void __launch_bounds__(kZT, 1)
 #pragma unroll
                         for (int i = 0; i < 2; ++i) {
                             const int j = c + i;
-                            if (el.in(j) && !(el.cxy[j] >= 0 && bzu >= 0)) {
+                            if (el.in(j) && (FACES || !(el.cxy[j] >= 0 && bzu >= 0))) {
                                 const int n = (tid + j * kZT) >> Z::LGB;
-                                qv[i] = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, pp[i],
-                                                        nb[i][0], nb[i][1], nb[i][2], nb[i][3], nb[i][4], nb[i][5]);
+                                if (FACES) {      // face coefficients (AMB-23), inline
+                                    double k[6];
+                                    node_kappa_faces<3>(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc, k);
+                                    qv[i] = stencil_apply<3>(g, k, pp[i], nb[i]);
+                                } else {
+                                    qv[i] = stencil_general(g, s_th, BP, b, x0 + n % Z::TX, y0 + n / Z::TX, Kc,
+                                                            pp[i], nb[i][0], nb[i][1], nb[i][2], nb[i][3], nb[i][4],
+                                                            nb[i][5]);
+                                }
                             }
                         }
                     }

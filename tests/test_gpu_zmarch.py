@@ -3,9 +3,10 @@ k_gsz, k_xrz fed by 4-D TMA tensor-map copies) -- RBCG Steps 5-7, 11 and the red
 half-sweeps (eq8, 269-275 algorithm2) on grids that span several (x, y)
 tiles, several z-segments and ragged tile edges in x, y and z, for every batch width
 (B_pad 8 / 16 / 32).  Against the oracle (criteria of tests/test_gpu_parity.py) and against
-the row-segment kernels they replace (RBS_DISABLE_V2 bit 16): per node the arithmetic is
-the same, only the order of the per-CTA partial sums differs, so the two GPU paths agree
-to rounding and take the same number of iterations."""
+the row-segment kernels they replace (RBS_DISABLE_V2 bit 16): the stencil is the same per
+node, the uniform-block Gauss-Seidel update differs by rounding (AMB-27) and so does the
+order of the per-CTA partial sums, so the two GPU paths agree to rounding and take the
+same number of iterations."""
 import os
 
 import numpy as np
@@ -87,3 +88,38 @@ def test_zmarch_rbi(orc, rbs):
     mus = 0.1 * 100 ** np.random.default_rng(8).random((5, g.Q))
     out = s.solve_batch(mus, method=rbs.RBS_RBI, max_iter=500000, record_history=1)
     compare(out, g, res["W"], res["ANq"], res["fn"], mus, "rbi", max_iter=500000)
+
+
+@pytest.mark.parametrize("m,B", [(29, 16), (23, 5)])
+def test_zmarch_faces_from_blocks(orc, rbs, m, B):
+    """the face-coefficient instantiations of the z-plane marches (AMB-23: faces built
+    from the thermal blocks reproduce the block operator) against the oracle, the
+    block-operator z-march and the row-segment face kernels (RBS_DISABLE_V2 bit 17)"""
+    from synth import cases
+    blocks = (2, 2, 2)
+    g, res = oracle_basis(orc, 3, m, blocks, 10, 24, 6)
+    F = cases.faces_from_blocks(3, m, blocks)
+    sf = rbs.Solver(3, m, faces=F).load_basis(res["W"], res["ANq"], res["fn"])
+    sb = rbs.Solver(3, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
+    old = os.environ.get("RBS_DISABLE_V2")
+    os.environ["RBS_DISABLE_V2"] = "131072"
+    try:
+        sr = rbs.Solver(3, m, faces=F).load_basis(res["W"], res["ANq"], res["fn"])
+    finally:
+        if old is None:
+            del os.environ["RBS_DISABLE_V2"]
+        else:
+            os.environ["RBS_DISABLE_V2"] = old
+    mus = 0.1 * 100 ** np.random.default_rng(m + B).random((B, g.Q))
+    of = sf.solve_batch(mus, record_history=1)
+    ob = sb.solve_batch(mus)
+    orr = sr.solve_batch(mus)
+    assert np.all(np.abs(of["its"] - ob["its"]) <= 1)
+    assert np.array_equal(of["its"], orr["its"])
+    xf, xb, xr = (o["X"].cpu().numpy() for o in (of, ob, orr))
+    assert np.linalg.norm(xf - xb) <= 1e-9 * np.linalg.norm(xb)
+    assert np.linalg.norm(xf - xr) <= 1e-11 * np.linalg.norm(xr)
+    sample = [0, B - 1]
+    compare(dict(of, X=of["X"][sample], status=[of["status"][i] for i in sample], its=of["its"][sample],
+                 a_n=of["a_n"][sample], history=[of["history"][i] for i in sample]),
+            g, res["W"], res["ANq"], res["fn"], mus[sample], "rbcg")

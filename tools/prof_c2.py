@@ -41,3 +41,13 @@ if a.load:
     torch.cuda.synchronize()
     print(json.dumps({k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]]
                       for k, v in out["profile"].items()}))
+    if os.environ.get("PROF_GRAPH"):
+        # graph-mode iteration time (the way bench.py runs one batch): fixed 200 iterations
+        s.solve_batch(mus, tol=0.0, max_iter=50, method=meth, want_a_n=False)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        s.solve_batch(mus, tol=0.0, max_iter=200, method=meth, want_a_n=False)
+        e1.record()
+        torch.cuda.synchronize()
+        print(json.dumps({"graph_us_per_iter": round(e0.elapsed_time(e1) * 1e3 / 200, 1)}))
