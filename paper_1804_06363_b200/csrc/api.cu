@@ -325,6 +325,7 @@ void set_attrs_z() {
     cudaFuncSetAttribute(k_gsz<BP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
     cudaFuncSetAttribute(k_xrz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
     cudaFuncSetAttribute(k_xrz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
+    cudaFuncSetAttribute(k_prolz<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZMaxDyn);
 }
 
 // cudaFuncSetAttribute applies to the current device only: once per device
@@ -1115,6 +1116,24 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         const size_t b = Bp == 8 ? zsmem_bytes<8>(kind, Q) : Bp == 16 ? zsmem_bytes<16>(kind, Q) : zsmem_bytes<32>(kind, Q);
         return b <= kZMaxDyn ? b : (size_t)0;
     };
+    // 3D prolongation by TMA (k_prolz): odd m (colour = index parity), full grid, rows of at most
+    // kMaxN + 4 doubles, ring within the shared-memory budget (RBS_DISABLE_V2 bit 18 keeps k_prolong)
+    const bool zprol = g.dim == 3 && (g.m & 1) && g.kofs == 0 && g.mz == g.m && (Bp == 8 || Bp == 16 || Bp == 32) &&
+                       !(v2off & 262144) && tmap_encoder() != nullptr && ctx->ldw <= kMaxN + 4 &&
+                       prolz_smem_bytes(Bp, ctx->ldw) <= kZMaxDyn;
+    // W viewed as [pairs][2][ldw]: box [ldw][1][CH] = CH rows of one index parity
+    auto zmap_w = [&](CUtensorMap* mp) {
+        auto enc = tmap_encoder();
+        if (!enc) return false;
+        const int ch = 128 / (Bp / 8);
+        cuuint64_t dims[3] = {(cuuint64_t)ctx->ldw, 2, (cuuint64_t)((g.N + 1) / 2)};
+        cuuint64_t strides[2] = {(cuuint64_t)ctx->ldw * 8, (cuuint64_t)ctx->ldw * 16};
+        cuuint32_t box[3] = {(cuuint32_t)ctx->ldw, 1, (cuuint32_t)ch};
+        cuuint32_t es[3] = {1, 1, 1};
+        return enc(mp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->Wi, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
     // haloed (stencil operand) / interior (pointwise operand) plane-tile maps of a batch vector
     auto zmap_h = [&](CUtensorMap* mp, const double* v) { return zmap(mp, v, g, Bp, ztx + 2, zty + 2); };
     auto zmap_i = [&](CUtensorMap* mp, const double* v) { return zmap(mp, v, g, Bp, ztx, zty); };
@@ -1143,7 +1162,19 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
         a.Y = Yv; a.accumulate = acc; a.done = done;
         a.skip_color = skip; a.dim = g.dim; a.m = g.m; a.kofs = g.kofs; a.fm = g.fm;
         pb(RBS_K_PROLONG);
-        if (npad > 0) {
+        CUtensorMap mw;
+        if (npad > 0 && zprol && skip >= 0 && zmap_w(&mw)) {
+            // odd m: the rows outside the skipped colour are the rows of index parity `skip`
+            ProlzArgs z{};
+            z.N = g.N; z.npairs = (g.N + 1) / 2; z.Bp = Bp; z.npad = npad; z.ldw = ctx->ldw; z.par = skip;
+            z.E = L.E; z.active = L.active; z.Y = Yv; z.accumulate = acc; z.done = done;
+            const size_t sm = prolz_smem_bytes(Bp, ctx->ldw);
+            const int64_t nch = (z.npairs + (128 / (Bp / 8)) - 1) / (128 / (Bp / 8));
+            const int grid = (int)std::min<int64_t>(ctx->num_sms, nch);
+            if (Bp == 8) k_prolz<8><<<grid, kZT, sm, st>>>(mw, z);
+            else if (Bp == 16) k_prolz<16><<<grid, kZT, sm, st>>>(mw, z);
+            else k_prolz<32><<<grid, kZT, sm, st>>>(mw, z);
+        } else if (npad > 0) {
             k_prolong<<<pgrid, kThreads, 0, st>>>(a);
         } else if (!acc) {  // empty basis: y0 = 0
             k_fill_batch<<<fgrid, 256, 0, st>>>(Yv, g.N, ctx->N8, Bp, 0, nullptr, 0.0);

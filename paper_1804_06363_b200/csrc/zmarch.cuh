@@ -85,6 +85,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -631,6 +639,105 @@ __global__ void __launch_bounds__(kZT, 1)
             if (tid == 0 && t + DI < T) issue(t + DI);
         }
         G += (uint32_t)T;
+    }
+}
+
+// ===========================================================================
+// k_prolz: the prolongation y0 = W e (+ x_old when accumulating; eq7)
+// of a 3D grid with an odd number m of nodes per axis, for the nodes outside the colour of
+// the half-sweep that follows (those are overwritten unread, AMB-6).  With m odd the
+// red-black colour alternates with the linear node index ((I+J+K) odd <=> i even), so the
+// rows needed are every other row of W: a 3-D tensor map views W as [pairs][2][ldw] and
+// one copy of box [ldw][1][CH] brings the CH needed rows of a chunk -- half the W bytes,
+// dense in shared memory (row stride ldw = npad + 4: conflict-free A fragments).
+// Warps own (8-node x 8-query) tiles of a chunk; E fragments stay in registers; two
+// accumulator chains per tile (even / odd k-steps).  Persistent grid, NS-slot ring.
+// ===========================================================================
+struct ProlzArgs {
+    int64_t npairs;          // ceil(N / 2)
+    int64_t N;
+    int Bp, npad, ldw, par;  // par: index parity of the rows prolongated (= skip colour)
+    const double* E;         // [npad][Bp]
+    const int* active;
+    double* Y;               // [N8][Bp]
+    int accumulate;
+    const int* done;
+};
+constexpr int kPzNS = 4;
+template <int BP>
+struct PzShape {
+    static constexpr int CH = 128 / (BP / 8);          // node rows per chunk: 16 warp tasks
+};
+inline size_t prolz_smem_bytes(int Bp, int ldw) {
+    return (size_t)kPzNS * (128 / (Bp / 8)) * ldw * 8;
+}
+template <int BP>
+__global__ void __launch_bounds__(kZT, 1) k_prolz(const __grid_constant__ CUtensorMap mW, const ProlzArgs a) {
+    constexpr int NKC = kMaxN / 4;           // k-steps, predicated on npad / 4
+    constexpr int CH = PzShape<BP>::CH, NBT = BP / 8, NS = kPzNS;
+    extern __shared__ __align__(128) double smd[];
+    __shared__ __align__(8) uint64_t bars[NS];
+    if (a.done && ld_flag(a.done)) return;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ldw = a.ldw;
+    const uint32_t slot = (uint32_t)CH * ldw * 8;
+    if (tid == 0) {
+        for (int k = 0; k < NS; ++k) mbar_init(&bars[k], 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&mW);
+    }
+    // this warp's task in every chunk: node tile nt, query tile bt
+    const int bt = warp % NBT, nt = warp / NBT;
+    const int nk = a.npad >> 2;
+    double ef[NKC];
+    const double* ecol = a.E + (lane & 3) * BP + bt * 8 + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < NKC; ++kk) ef[kk] = kk < nk ? __ldg(ecol + (int64_t)kk * 4 * BP) : 0.0;
+    const int b = bt * 8 + 2 * (lane & 3);
+    const bool act0 = a.active[b] != 0, act1 = a.active[b + 1] != 0;
+    __syncthreads();
+    const int64_t nchunk = (a.npairs + CH - 1) / CH;
+    const int64_t c0 = blockIdx.x, cs = gridDim.x;
+    const int64_t mine = c0 < nchunk ? (nchunk - 1 - c0) / cs + 1 : 0;
+    auto issue = [&](int64_t k) {            // this CTA's k-th chunk -> slot k % NS
+        const int sl = (int)(k % NS);
+        fence_async_smem();
+        mbar_expect_tx(&bars[sl], slot);
+        tma_load_3d(smd + (size_t)sl * CH * ldw, &mW, 0, a.par, (int)((c0 + k * cs) * CH), &bars[sl]);
+    };
+    if (tid == 0)
+        for (int64_t k = 0; k < NS - 1 && k < mine; ++k) issue(k);
+    const uint32_t sb = smem_u32(smd) + 8u * ((nt * 8 + (lane >> 2)) * ldw + (lane & 3));
+    for (int64_t k = 0; k < mine; ++k) {
+        if (tid == 0 && k + NS - 1 < mine) issue(k + NS - 1);
+        const int sl = (int)(k % NS);
+        mbar_wait(&bars[sl], (uint32_t)((k / NS) & 1));
+        const uint32_t wb = sb + (uint32_t)sl * slot;
+        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NKC; kk += 2) {
+            if (kk < nk) dmma_8x8x4(d0, d1, ldsd(wb + 32u * kk), ef[kk]);
+            if (kk + 1 < nk) dmma_8x8x4(e0, e1, ldsd(wb + 32u * (kk + 1)), ef[kk + 1]);
+        }
+        d0 += e0;
+        d1 += e1;
+        const int64_t pair = (c0 + k * cs) * CH + nt * 8 + (lane >> 2);
+        const int64_t i = 2 * pair + a.par;
+        if (pair < a.npairs && i < a.N) {
+            double* y = a.Y + i * BP + b;
+            double2 v = make_double2(d0, d1);
+            if (a.accumulate) {
+                const double2 o = *reinterpret_cast<const double2*>(y);
+                v.x += o.x;
+                v.y += o.y;
+            }
+            if (act0 && act1) *reinterpret_cast<double2*>(y) = v;
+            else {
+                if (act0) y[0] = v.x;
+                if (act1) y[1] = v.y;
+            }
+        }
+        __syncthreads();            // slot sl is reissued NS - 1 chunks later
     }
 }
 
