@@ -224,7 +224,7 @@ def run_reference(a):
 # Case 1 with RB dimension 1 and 5, Case 2 with 2 and 10 (AMB-17: the
 # text's 10 over the caption's 20), 100 random parameters per case (96 = 6 batches of 16 here)
 CASE_M, CASE_B, CASE_TRAIN, CASE_QUERIES = 127, 16, 64, 96
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r2z_traffic.json")
 # the exact instantiation each kernel class runs as at each config (what the committed
 # ncu capture must name; a capture of another instantiation is not reported)
 TIMED_KERNEL = {("c2", "k_gs"): "void k_smooth2<32, 3, 1, 32, 3, 10>(SmoothMarchArgs)",
