@@ -527,6 +527,13 @@ def main():
         spawn(a)           # does not return
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RBS_BENCH_SMOKE_1GPU=1: code-path smoke of the N > 1 query-shard bench on a one-GPU box
+    # (every rank on cuda:0, gloo for the barrier / max-over-ranks plumbing).  The shards share
+    # no data-path collective, so no kernel waits on another rank; the timing is not a scaling
+    # number (the ranks share one GPU) and is never reported as one.
+    smoke1 = os.environ.get("RBS_BENCH_SMOKE_1GPU") == "1"
+    if smoke1:
+        local = 0
     if a.config in ("case1", "case2"):
         if a.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "case workloads: GPU measurement only"}))
@@ -547,7 +554,10 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if smoke1:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[a.config]
     shard = a.shard or ("strong" if a.config in ("c3", "c4") else "weak")
     s = rbs.Solver(c.dim, c.m, c.blocks, device=local)
@@ -645,6 +655,10 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches, its, trr, nsolved = 0, [], [], 0
+    # lane occupancy: useful node-query iterations / lane-iterations streamed (a batch runs until
+    # its slowest query; frozen lanes still stream their rows -- the case for batch compaction)
+    lane_used = sum(sum(int(i) for i in o["its"]) for o in outs)
+    lane_streamed = sum(len(o["its"]) * max(int(i) for i in o["its"]) for o in outs)
     for out in outs:
         launches += out["launches"]
         its += [int(i) for i in out["its"]]
@@ -773,6 +787,7 @@ def main():
                        "concurrent_batches": S, "batch_order": a.order,
                        "l2": l2,
                        "its_min_med_max": [min(its), int(np.median(its)), max(its)],
+                       "lane_occupancy": round(lane_used / max(lane_streamed, 1), 4),
                        "true_relres_max": max(trr),
                        "offline_greedy_s": round(offline_s, 2), "snapshot_its": snap[:6]},
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
