@@ -325,6 +325,8 @@ void set_attrs_z() {
     cudaFuncSetAttribute(k_gsz<BP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
     cudaFuncSetAttribute(k_xrz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
     cudaFuncSetAttribute(k_xrz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
+    cudaFuncSetAttribute(k_xrz<BP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
+    cudaFuncSetAttribute(k_xrz<BP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
     cudaFuncSetAttribute(k_prolz<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZMaxDyn);
 }
 
@@ -408,7 +410,10 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.X = cv.take<double>(vec);
     L.X2 = (!cg && c->g.dim == 2 && o->smoother != RBS_SMOOTH_JACOBI) ? cv.take<double>(vec)
                                                                         : nullptr;   // RBI ping-pong (march)
-    L.T = o->smoother == RBS_SMOOTH_JACOBI ? cv.take<double>(vec) : nullptr;   // Jacobi ping-pong
+    // Jacobi ping-pong; 3D symmetric two-level preconditioner: v = r - A y1 of the z-march
+    // residual-projection (k_xrz<RES> + k_wtr)
+    L.T = (o->smoother == RBS_SMOOTH_JACOBI || (cg && c->g.dim == 3 && o->precond == RBS_PRECOND_SYM))
+              ? cv.take<double>(vec) : nullptr;
     L.R = cg ? cv.take<double>(vec) : nullptr;
     L.P0 = cg ? cv.take<double>(vec) : nullptr;
     L.P1 = cg ? cv.take<double>(vec) : nullptr;
@@ -1345,6 +1350,43 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 launch_proj<MODE_PLAIN>(g, a.nct, psm, st, b2);
             }
             nl = 2;
+        } else if (mode == MODE_RESID && cg && o->precond == RBS_PRECOND_SYM && g.dim == 3 && use_active && L.T && Vv && !(v2off & 524288) &&
+                   zm3 && zsm(2) && npad <= 64 && wtr_smem_bytes(Bp, ctx->ldw, 32) <= (size_t)110 * 1024) {
+            // symmetric preconditioner's W^T (r - A y1), 3D full grid (RBS_DISABLE_V2 bit 19 keeps
+            // the flat k_proj<MODE_RESID>): v = r - A y1 by the z-plane march into the scratch
+            // vector T, then the streamed W^T v, ||v||^2 (two passes, as K2)
+            CUtensorMap myz, mrz;
+            if (zmap_h(&myz, Xv) && zmap_i(&mrz, Vv)) {
+                ProjArgs ar = a;
+                ar.X = L.T;
+                if (Bp == 8) {
+                    if (zf) k_xrz<8, true, true><<<zgrid, kZT, zsm(2), st>>>(myz, mrz, mrz, ar, zpt);
+                    else k_xrz<8, false, true><<<zgrid, kZT, zsm(2), st>>>(myz, mrz, mrz, ar, zpt);
+                } else if (Bp == 16) {
+                    if (zf) k_xrz<16, true, true><<<zgrid, kZT, zsm(2), st>>>(myz, mrz, mrz, ar, zpt);
+                    else k_xrz<16, false, true><<<zgrid, kZT, zsm(2), st>>>(myz, mrz, mrz, ar, zpt);
+                } else {
+                    if (zf) k_xrz<32, true, true><<<zgrid, kZT, zsm(2), st>>>(myz, mrz, mrz, ar, zpt);
+                    else k_xrz<32, false, true><<<zgrid, kZT, zsm(2), st>>>(myz, mrz, mrz, ar, zpt);
+                }
+                ProjArgs b2 = a;
+                b2.V = L.T;
+                // 64-node chunks, 32 when W rows are long (as K2)
+                const int ch = wtr_smem_bytes(Bp, ctx->ldw, 64) <= (size_t)110 * 1024 ? 64 : 32;
+                const size_t wsm = wtr_smem_bytes(Bp, ctx->ldw, ch);
+                if (ch == 64) {
+                    if (Bp == 8) k_wtr<8, 64><<<a.nct, kMT, wsm, st>>>(b2);
+                    else if (Bp == 16) k_wtr<16, 64><<<a.nct, kMT, wsm, st>>>(b2);
+                    else k_wtr<32, 64><<<a.nct, kMT, wsm, st>>>(b2);
+                } else {
+                    if (Bp == 8) k_wtr<8, 32><<<a.nct, kMT, wsm, st>>>(b2);
+                    else if (Bp == 16) k_wtr<16, 32><<<a.nct, kMT, wsm, st>>>(b2);
+                    else k_wtr<32, 32><<<a.nct, kMT, wsm, st>>>(b2);
+                }
+                nl = 2;
+            } else {
+                launch_proj<MODE_RESID>(g, a.nct, psm, st, a);
+            }
         } else if (mode == MODE_CG) launch_proj<MODE_CG>(g, a.nct, psm, st, a);
         else launch_proj<MODE_RESID>(g, a.nct, psm, st, a);
         pe();

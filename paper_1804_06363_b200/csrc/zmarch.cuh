@@ -512,9 +512,13 @@ __global__ void __launch_bounds__(kZT, 1)
 //   step t (plane K = za-1+t of p arrives, with the x and r tiles of plane K-1): plane K-1
 //   is updated and stored.  p: haloed ring of kXNA slots; x, r: interior rings of 3 slots;
 //   all three are issued 2 planes ahead.
+// RES = true: the residual v = b - A y of the symmetric two-level preconditioner's coarse
+//   correction (PAPER.md:161 Step 2 form, NEXT(3)): mP maps y (haloed), mR the right-hand
+//   side b; v is stored to a.X (a scratch vector), no x tiles are loaded.  Same value as
+//   k_proj<MODE_RESID> (c1 - q, the same stencil); W^T v then streams through k_wtr.
 // ===========================================================================
 constexpr int kXDI = 2, kXNA = kXDI + 3, kXNR = 3;
-template <int BP, bool FACES>
+template <int BP, bool FACES, bool RES = false>
 __global__ void __launch_bounds__(kZT, 1)
     k_xrz(const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mX,
           const __grid_constant__ CUtensorMap mR, const __grid_constant__ ProjArgs a, const ZPart zp) {
@@ -559,10 +563,11 @@ __global__ void __launch_bounds__(kZT, 1)
             const bool in = K >= 1 && K <= m, own = K >= za && K < zb;
             fence_async_smem();
             mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
-            mbar_expect_tx(&barX[q % NR], own ? 2u * IPB : 0u);
+            mbar_expect_tx(&barX[q % NR], own ? (RES ? 1u : 2u) * IPB : 0u);
             if (in) tma_load_4d(smd + (q % NA) * Z::HP, &mP, 0, x0 - 2, y0 - 2, K - 1, &barA[q % NA]);
             if (own) {
-                tma_load_4d(smd + NA * Z::HP + (q % NR) * Z::IP, &mX, 0, x0 - 1, y0 - 1, K - 1, &barX[q % NR]);
+                if (!RES)
+                    tma_load_4d(smd + NA * Z::HP + (q % NR) * Z::IP, &mX, 0, x0 - 1, y0 - 1, K - 1, &barX[q % NR]);
                 tma_load_4d(smd + NA * Z::HP + NR * Z::IP + (q % NR) * Z::IP, &mR, 0, x0 - 1, y0 - 1, K - 1,
                             &barX[q % NR]);
             }
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(kZT, 1)
                         const double zlo = ldsd(ym + o), zhi = ldsd(yp + o);
                         nb[i][4] = zm ? zlo : 0.0;
                         nb[i][5] = zpl ? zhi : 0.0;
-                        xv[i] = ldsd(xs + 8u * j * kZT);
+                        xv[i] = RES ? 0.0 : ldsd(xs + 8u * j * kZT);
                         rv[i] = ldsd(rs + 8u * j * kZT);
                         const bool fast = !FACES && el.cxy[j] >= 0 && bzu >= 0;
                         qv[i] = ldsd(sth + 8u * (uint32_t)((fast ? el.cxy[j] + bzu : 0) * BP));
@@ -630,8 +635,12 @@ __global__ void __launch_bounds__(kZT, 1)
                     for (int i = 0; i < 2; ++i) {
                         const int j = c + i;
                         if (!el.in(j)) continue;
-                        Xc[el.gxy[j]] = fma(al, pp[i], xv[i]);
-                        Rc[el.gxy[j]] = fma(-al, qv[i], rv[i]);
+                        if (RES) {
+                            Xc[el.gxy[j]] = rv[i] - qv[i];
+                        } else {
+                            Xc[el.gxy[j]] = fma(al, pp[i], xv[i]);
+                            Rc[el.gxy[j]] = fma(-al, qv[i], rv[i]);
+                        }
                     }
                 }
             }

@@ -17,10 +17,10 @@ from test_gpu_parity import compare, oracle_basis, oracle_refs, rbs  # noqa: F40
 pytestmark = pytest.mark.gpu
 
 
-def _solver_pair(rbs, dim, m, blocks, res):
+def _solver_pair(rbs, dim, m, blocks, res, bits="65536"):
     z = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
     old = os.environ.get("RBS_DISABLE_V2")
-    os.environ["RBS_DISABLE_V2"] = "65536"          # read once at rbs_create
+    os.environ["RBS_DISABLE_V2"] = bits             # read once at rbs_create
     try:
         r = rbs.Solver(dim, m, blocks).load_basis(res["W"], res["ANq"], res["fn"])
     finally:
@@ -123,3 +123,30 @@ def test_zmarch_faces_from_blocks(orc, rbs, m, B):
     compare(dict(of, X=of["X"][sample], status=[of["status"][i] for i in sample], its=of["its"][sample],
                  a_n=of["a_n"][sample], history=[of["history"][i] for i in sample]),
             g, res["W"], res["ANq"], res["fn"], mus[sample], "rbcg")
+
+
+@pytest.mark.parametrize("B", [5, 16, 27])
+def test_zmarch_sym_precond_residual_projection(orc, rbs, B):
+    """The symmetric two-level preconditioner's coarse correction W^T (r - A y1) on a 3D full
+    grid: v = r - A y1 by k_xrz<RES> (z-plane march into the scratch vector) + the streamed
+    k_wtr, against the flat k_proj<MODE_RESID> (RBS_DISABLE_V2 bit 19; same v per node, the
+    W^T v partial sums in another order) and against the oracle's RB-PCG with the same
+    preconditioner (NEXT(3)); m = 37 spans several ragged tiles and z-segments."""
+    g, res = oracle_basis(orc, 3, 37, (2, 2, 2), 12, 24, 5)
+    z, f = _solver_pair(rbs, 3, 37, (2, 2, 2), res, bits="524288")
+    mus = 0.1 * 100 ** np.random.default_rng(71 + B).random((B, g.Q))
+    kw = dict(record_history=1, max_iter=20000, precond=1)
+    oz = z.solve_batch(mus, **kw)
+    of = f.solve_batch(mus, **kw)
+    assert all(st == "CONVERGED" for st in oz["status"]), oz["status"]
+    assert np.max(np.abs(np.asarray(oz["its"]) - np.asarray(of["its"]))) <= 1
+    Xz, Xf = oz["X"].cpu().numpy(), of["X"].cpu().numpy()
+    assert np.max(np.linalg.norm(Xz - Xf, axis=1) / np.linalg.norm(Xf, axis=1)) <= 1e-9
+    sample = list(range(min(B, 3)))
+    compare(dict(oz, X=oz["X"][sample], status=[oz["status"][i] for i in sample], its=oz["its"][sample],
+                 a_n=oz["a_n"][sample], history=[oz["history"][i] for i in sample]),
+            g, res["W"], res["ANq"], res["fn"], mus[sample], "rbcg", max_iter=20000, precond=1)
+    # fixed iterations (tol 0): the two GPU paths to rounding at every lane
+    k = dict(tol=0.0, max_iter=6, precond=1)
+    a, b = z.solve_batch(mus, **k)["X"].cpu().numpy(), f.solve_batch(mus, **k)["X"].cpu().numpy()
+    assert np.max(np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)) <= 1e-12
