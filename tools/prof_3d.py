@@ -23,6 +23,7 @@ ap.add_argument("--random-basis", action="store_true",
                 help="random orthonormal W (timing only: fixed-iteration solves, no greedy build)")
 ap.add_argument("--B", type=int, default=16)
 ap.add_argument("--precond", type=int, default=0, help="1: symmetric two-level preconditioner")
+ap.add_argument("--rbi", action="store_true", help="stand-alone RBI instead of RBCG")
 ap.add_argument("--prof-only", action="store_true", help="skip the graph-mode timing (ncu captures)")
 a = ap.parse_args()
 blocks = (2, 2, 2)
@@ -46,8 +47,9 @@ else:
     if os.environ.get("PROF3D_BASIS"):
         torch.save({"W": gr["W"].cpu(), "ANq": gr["ANq"], "fn": gr["fn"]}, os.environ["PROF3D_BASIS"])
 mus = 0.1 * 100 ** rng.random((a.B, 8))
+mkw = dict(method=rbs.RBS_RBI) if a.rbi else {}
 torch.cuda.nvtx.range_push("solve")      # ncu --nvtx --nvtx-include "solve/" captures only this
-out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False, precond=a.precond)
+out = s.solve_batch(mus, profile=1, tol=0.0, max_iter=a.iters, want_a_n=False, precond=a.precond, **mkw)
 torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 prof = {k: [round(v[0] / max(v[1], 1) * 1e3, 2), v[1]] for k, v in out["profile"].items() if v[1]}
@@ -55,11 +57,11 @@ if a.prof_only:
     print(json.dumps(prof))
     sys.exit(0)
 # graph-mode iteration time (the way bench.py runs): a fixed 200-iteration solve
-s.solve_batch(mus, tol=0.0, max_iter=50, want_a_n=False, precond=a.precond)
+s.solve_batch(mus, tol=0.0, max_iter=50, want_a_n=False, precond=a.precond, **mkw)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
 e0.record()
-s.solve_batch(mus, tol=0.0, max_iter=200, want_a_n=False, precond=a.precond)
+s.solve_batch(mus, tol=0.0, max_iter=200, want_a_n=False, precond=a.precond, **mkw)
 e1.record()
 torch.cuda.synchronize()
 prof["graph_us_per_iter"] = round(e0.elapsed_time(e1) * 1e3 / 200, 1)
