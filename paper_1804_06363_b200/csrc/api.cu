@@ -410,9 +410,10 @@ SolveLayout solve_layout(const rbs_ctx* c, int B, const rbs_solve_opts* o, bool 
     L.X = cv.take<double>(vec);
     L.X2 = (!cg && c->g.dim == 2 && o->smoother != RBS_SMOOTH_JACOBI) ? cv.take<double>(vec)
                                                                         : nullptr;   // RBI ping-pong (march)
-    // Jacobi ping-pong; 3D symmetric two-level preconditioner: v = r - A y1 of the z-march
-    // residual-projection (k_xrz<RES> + k_wtr)
-    L.T = (o->smoother == RBS_SMOOTH_JACOBI || (cg && c->g.dim == 3 && o->precond == RBS_PRECOND_SYM))
+    // Jacobi ping-pong; 3D z-march residual-projection (k_xrz<RES> + k_wtr) of the symmetric
+    // two-level preconditioner (v = r - A y1) and of RBI (v = f - A x)
+    L.T = (o->smoother == RBS_SMOOTH_JACOBI ||
+           (c->g.dim == 3 && (!cg || o->precond == RBS_PRECOND_SYM)))
               ? cv.take<double>(vec) : nullptr;
     L.R = cg ? cv.take<double>(vec) : nullptr;
     L.P0 = cg ? cv.take<double>(vec) : nullptr;
@@ -1350,13 +1351,14 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
                 launch_proj<MODE_PLAIN>(g, a.nct, psm, st, b2);
             }
             nl = 2;
-        } else if (mode == MODE_RESID && cg && o->precond == RBS_PRECOND_SYM && g.dim == 3 && use_active && L.T && Vv && !(v2off & 524288) &&
+        } else if (mode == MODE_RESID && (!cg || o->precond == RBS_PRECOND_SYM) && g.dim == 3 && use_active && L.T &&
+                   !(v2off & 524288) &&
                    zm3 && zsm(2) && npad <= 64 && wtr_smem_bytes(Bp, ctx->ldw, 32) <= (size_t)110 * 1024) {
-            // symmetric preconditioner's W^T (r - A y1), 3D full grid (RBS_DISABLE_V2 bit 19 keeps
-            // the flat k_proj<MODE_RESID>): v = r - A y1 by the z-plane march into the scratch
-            // vector T, then the streamed W^T v, ||v||^2 (two passes, as K2)
+            // symmetric preconditioner's W^T (r - A y1) / RBI's W^T (f - A x), 3D full grid
+            // (RBS_DISABLE_V2 bit 19 keeps the flat k_proj<MODE_RESID>): v by the z-plane march
+            // into the scratch vector T, then the streamed W^T v, ||v||^2 (two passes, as K2)
             CUtensorMap myz, mrz;
-            if (zmap_h(&myz, Xv) && zmap_i(&mrz, Vv)) {
+            if (zmap_h(&myz, a.X) && zmap_i(&mrz, a.V ? a.V : a.X)) {
                 ProjArgs ar = a;
                 ar.X = L.T;
                 if (Bp == 8) {

@@ -514,8 +514,9 @@ __global__ void __launch_bounds__(kZT, 1)
 //   all three are issued 2 planes ahead.
 // RES = true: the residual v = b - A y of the symmetric two-level preconditioner's coarse
 //   correction (PAPER.md:161 Step 2 form, NEXT(3)): mP maps y (haloed), mR the right-hand
-//   side b; v is stored to a.X (a scratch vector), no x tiles are loaded.  Same value as
-//   k_proj<MODE_RESID> (c1 - q, the same stencil); W^T v then streams through k_wtr.
+//   side b (a.V == nullptr: the constant a.vconst, no r tiles); v is stored to a.X (a
+//   scratch vector), no x tiles are loaded.  Same value as k_proj<MODE_RESID> (c1 - q, the
+//   same stencil); W^T v then streams through k_wtr.  Also RBI Step 2 (v = f - A x).
 // ===========================================================================
 constexpr int kXDI = 2, kXNA = kXDI + 3, kXNR = 3;
 template <int BP, bool FACES, bool RES = false>
@@ -542,7 +543,8 @@ __global__ void __launch_bounds__(kZT, 1)
         tma_prefetch_desc(&mR);
     }
     const bool act = a.active[b] != 0;
-    const double al = a.alpha[b];
+    const double al = RES ? 1.0 : a.alpha[b];
+    const bool vc = RES && a.V == nullptr;     // constant right-hand side: no r tiles
     double* const X = a.X;
     double* const R = a.R;
     const uint32_t sA = smem_u32(smd), sX = sA + 8u * NA * Z::HP, sR = sX + 8u * NR * Z::IP;
@@ -563,13 +565,14 @@ __global__ void __launch_bounds__(kZT, 1)
             const bool in = K >= 1 && K <= m, own = K >= za && K < zb;
             fence_async_smem();
             mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
-            mbar_expect_tx(&barX[q % NR], own ? (RES ? 1u : 2u) * IPB : 0u);
+            mbar_expect_tx(&barX[q % NR], own ? (RES ? (vc ? 0u : 1u) : 2u) * IPB : 0u);
             if (in) tma_load_4d(smd + (q % NA) * Z::HP, &mP, 0, x0 - 2, y0 - 2, K - 1, &barA[q % NA]);
             if (own) {
                 if (!RES)
                     tma_load_4d(smd + NA * Z::HP + (q % NR) * Z::IP, &mX, 0, x0 - 1, y0 - 1, K - 1, &barX[q % NR]);
-                tma_load_4d(smd + NA * Z::HP + NR * Z::IP + (q % NR) * Z::IP, &mR, 0, x0 - 1, y0 - 1, K - 1,
-                            &barX[q % NR]);
+                if (!vc)
+                    tma_load_4d(smd + NA * Z::HP + NR * Z::IP + (q % NR) * Z::IP, &mR, 0, x0 - 1, y0 - 1, K - 1,
+                                &barX[q % NR]);
             }
         };
         if (tid == 0)
@@ -606,7 +609,7 @@ __global__ void __launch_bounds__(kZT, 1)
                         nb[i][4] = zm ? zlo : 0.0;
                         nb[i][5] = zpl ? zhi : 0.0;
                         xv[i] = RES ? 0.0 : ldsd(xs + 8u * j * kZT);
-                        rv[i] = ldsd(rs + 8u * j * kZT);
+                        rv[i] = vc ? a.vconst : ldsd(rs + 8u * j * kZT);
                         const bool fast = !FACES && el.cxy[j] >= 0 && bzu >= 0;
                         qv[i] = ldsd(sth + 8u * (uint32_t)((fast ? el.cxy[j] + bzu : 0) * BP));
                         slow |= el.in(j) && !fast;

@@ -150,3 +150,31 @@ def test_zmarch_sym_precond_residual_projection(orc, rbs, B):
     k = dict(tol=0.0, max_iter=6, precond=1)
     a, b = z.solve_batch(mus, **k)["X"].cpu().numpy(), f.solve_batch(mus, **k)["X"].cpu().numpy()
     assert np.max(np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)) <= 1e-12
+
+
+@pytest.mark.parametrize("B", [5, 16])
+def test_zmarch_rbi_residual_projection(orc, rbs, B):
+    """Stand-alone RBI in 3D with Step 2's residual v = f - A x by k_xrz<RES> + k_wtr
+    (PAPER.md:161-163): f = 1 (constant, no r tiles) against the oracle and the flat
+    k_proj<MODE_RESID> (RBS_DISABLE_V2 bit 19); a given right-hand side (r tiles from
+    rhs_dev) against the flat path in fixed-iteration mode."""
+    import torch
+    g, res = oracle_basis(orc, 3, 23, (2, 2, 2), 10, 20, 2)
+    z, f = _solver_pair(rbs, 3, 23, (2, 2, 2), res, bits="524288")
+    mus = 0.1 * 100 ** np.random.default_rng(90 + B).random((B, g.Q))
+    kw = dict(method=rbs.RBS_RBI, max_iter=500000, record_history=1)
+    oz = z.solve_batch(mus, **kw)
+    of = f.solve_batch(mus, **kw)
+    assert all(st == "CONVERGED" for st in oz["status"]), oz["status"]
+    assert np.max(np.abs(np.asarray(oz["its"]) - np.asarray(of["its"]))) <= 1
+    Xz, Xf = oz["X"].cpu().numpy(), of["X"].cpu().numpy()
+    assert np.max(np.linalg.norm(Xz - Xf, axis=1) / np.linalg.norm(Xf, axis=1)) <= 1e-9
+    sample = [0, B - 1]
+    compare(dict(oz, X=oz["X"][sample], status=[oz["status"][i] for i in sample], its=oz["its"][sample],
+                 a_n=oz["a_n"][sample], history=[oz["history"][i] for i in sample]),
+            g, res["W"], res["ANq"], res["fn"], mus[sample], "rbi", max_iter=500000)
+    rhs = torch.tensor(np.random.default_rng(3).standard_normal((B, g.N)), device="cuda")
+    k = dict(method=rbs.RBS_RBI, tol=0.0, max_iter=8)
+    a = z.solve_batch(mus, rhs=rhs, **k)["X"].cpu().numpy()
+    b = f.solve_batch(mus, rhs=rhs, **k)["X"].cpu().numpy()
+    assert np.max(np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)) <= 1e-12
