@@ -725,7 +725,13 @@ def main():
     alg = {"k_cgp": 24 * Bp_ * N,                    # y, p_old read; p_new written
            "k_proj": 40 * Bp_ * N + 8 * N * n,       # p, x, r read; x, r written; W
            "k_gs": 16 * Bp_ * N + 8 * N * n}         # 2D fused smoother: r read, y written; W
-    if a.method == "rbi":   # RBI: K3' x_new = S(x_old + W e) (x_old, W read; x written), resid f - A x + W^T (x, W)
+    if a.method == "rbi" and c.dim == 3:
+        # 3D RBI: x_old + W e for the nodes outside the first half-sweep's colour (x_old, W
+        # rows read, x written: half), one half-sweep per k_gs launch (x read, one colour of x
+        # written; f constant), Step 2's residual-projection at its minimum (x, W read)
+        alg = {"k_prolong": (16 * Bp_ * N + 8 * N * n) // 2, "k_gs": 12 * Bp_ * N,
+               "k_proj": 8 * Bp_ * N + 8 * N * n}
+    elif a.method == "rbi":   # RBI: K3' x_new = S(x_old + W e) (x_old, W read; x written), resid f - A x + W^T (x, W)
         alg = {"k_gs": 16 * Bp_ * N + 8 * N * n, "k_proj": 8 * Bp_ * N + 8 * N * n}
     elif c.dim == 3:   # separate prolongation pass; k_gs is one red-black half-sweep per launch
         # W read, y0 written -- for the nodes outside the first half-sweep's colour only (the
@@ -733,6 +739,8 @@ def main():
         alg["k_prolong"] = (8 * Bp_ * N + 8 * N * n) // 2
         alg["k_gs"] = 16 * Bp_ * N                   # y read, r and y of one colour
     flops = {"k_proj": 2.0 * N * n * Bp_, "k_gs": 2.0 * N * n * Bp_}   # W^T r / W e on DMMA
+    if c.dim == 3:   # 3D: W e in its own pass (half the rows: colour skip); k_gs is a half-sweep
+        flops = {"k_proj": 2.0 * N * n * Bp_, "k_prolong": 1.0 * N * n * Bp_}
     tot_ms = sum(v[0] for v in prof.values())
     kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
                    "share": v[0] / tot_ms if tot_ms else None} for k, v in prof.items() if v[1]}
