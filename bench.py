@@ -508,8 +508,10 @@ def run_c5(a, world, rank, local):
         iter_us = 1e3 * tot_ms / max(prof["k_cgp"][1], 1)
         # minimum bytes per batch-iteration: the fused schedule's 80 B + 16n / B per node-query
         # (DESIGN.md §7); the symmetric two-level preconditioner's passes (3D flat schedule: K1,
-        # K2, y = 0, 3 pre + 3 post half-sweeps, residual-projection, prolongation) 200 B + 24n / B
-        iter_bytes = ((200 * c.B + 24 * n) if a.precond == "sym" else (80 * c.B + 16 * n)) * c.N
+        # K2, y = 0, 3 pre + 3 post half-sweeps, residual-projection, prolongation) 200 B + 24n / B;
+        # 3D z-plane marches: the first pre half-sweep from y = 0 as k_gsz<ZERO> (r of the
+        # colour 4 B + both colours' stores 8 B instead of the fill 8 B + a half-sweep 12 B): 192 B
+        iter_bytes = ((192 * c.B + 24 * n) if a.precond == "sym" else (80 * c.B + 16 * n)) * c.N
         line["roofline"] = {"bound": "hbm", "kernel": "iteration", "achieved": iter_bytes / (iter_us * 1e-6) / 1e9,
                             "peak": hbm, "unit": "GB/s", "frac": iter_bytes / (iter_us * 1e-6) / 1e9 / hbm,
                             "traffic": None, "peak_source": hbm_src, "alg_bytes_per_launch": iter_bytes,
@@ -756,7 +758,8 @@ def main():
     kt = kernels[top]
     iter_us = 1e3 * tot_ms / max(prof["k_proj"][1], 1)     # per pass-iteration of Bp_ queries
     iter_bytes = ((24 * Bp_ + 16 * n) if a.method == "rbi" else
-                  (200 * Bp_ + 24 * n) if a.precond == "sym" else (80 * Bp_ + 16 * n)) * N   # per batch-iteration
+                  ((192 if c.dim == 3 else 200) * Bp_ + 24 * n) if a.precond == "sym" else
+                  (80 * Bp_ + 16 * n)) * N   # per batch-iteration (3D sym: k_gsz<ZERO> pre-sweep)
     traffic, traffic_src = ncu_traffic(a.config, top)
     roof = {"bound": "hbm", "kernel": top, "timed_instantiation": TIMED_KERNEL.get((a.config, top)),
             "achieved": kt["GBps"], "peak": hbm, "unit": "GB/s",

@@ -323,6 +323,8 @@ void set_attrs_z() {
     cudaFuncSetAttribute(k_gsz<BP, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
     cudaFuncSetAttribute(k_gsz<BP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
     cudaFuncSetAttribute(k_gsz<BP, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
+    cudaFuncSetAttribute(k_gsz<BP, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
+    cudaFuncSetAttribute(k_gsz<BP, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1);
     cudaFuncSetAttribute(k_xrz<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
     cudaFuncSetAttribute(k_xrz<BP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
     cudaFuncSetAttribute(k_xrz<BP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2);
@@ -1232,14 +1234,28 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     };
     // sq: the colour sequence (default: the smoother's; the adjoint sweep of the symmetric
     // preconditioner passes it reversed)
+    // zero0: the sweep starts from Yv = 0 (the symmetric preconditioner's pre-sweep).  On the
+    // 3D z-plane march the first half-sweep then runs as k_gsz<ZERO> (no fill, no y tiles;
+    // RBS_DISABLE_V2 bit 20 keeps the k_fill_batch + half-sweep pair, as does init: the
+    // solve's first call also zeroes the padding rows); every other path fills Yv first
     auto smooth = [&](double* Yv, const double* rhs, double rconst, bool last, int init,
-                      const std::vector<int>* sq = nullptr) {
-        if (jac) return smooth_jac(Yv, Yv, rhs, rconst, last, init);
+                      const std::vector<int>* sq = nullptr, bool zero0 = false) {
+        int cnt = 0;
+        std::vector<int> cs = sq ? *sq : seq;
+        bool z0 = zero0 && !jac && zm3 && !init && !last && !cs.empty() && cs[0] >= 0 && zsm(1) &&
+                  !(v2off & 1048576);
+        if (z0) {
+            CUtensorMap probe;
+            z0 = zmap_h(&probe, Yv) && zmap_i(&probe, rhs ? rhs : Yv);
+        }
+        if (zero0 && !z0) {
+            k_fill_batch<<<fgrid, 256, 0, st>>>(Yv, g.N, ctx->N8, Bp, 0, nullptr, 0.0);
+            ++cnt;
+        }
+        if (jac) return cnt + smooth_jac(Yv, Yv, rhs, rconst, last, init);
         GSArgs a{};
         a.g = g; a.Bp = Bp; a.lgB = lgB; a.NB = g.N * Bp; a.theta = L.theta; a.active = L.active;
         a.Y = Yv; a.Rhs = rhs; a.rconst = rconst; a.init = init; a.s = S; a.done = done;
-        int cnt = 0;
-        std::vector<int> cs = sq ? *sq : seq;
         if (cs.empty() && last) cs.push_back(-1);
         for (size_t t = 0; t < cs.size(); ++t) {
             a.color = cs[t];
@@ -1252,13 +1268,16 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             } else if (zm3 && a.color >= 0 && zsm(1) && zmap_h(&my, Yv) && zmap_i(&mr, rhs ? rhs : Yv)) {
                 // z-plane march: y tile with halo + r tile per plane by tensor-map copies
 #define RBS_GSZ(BPV, L, F) k_gsz<BPV, L, F><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt)
+#define RBS_GSZ0(BPV, F) k_gsz<BPV, false, F, true><<<zgrid, kZT, zsm(1), st>>>(my, mr, a, zpt)
 #define RBS_GSZ2(BPV) \
-    if (zf) { if (l) RBS_GSZ(BPV, true, true); else RBS_GSZ(BPV, false, true); } \
+    if (z0 && t == 0) { if (zf) RBS_GSZ0(BPV, true); else RBS_GSZ0(BPV, false); } \
+    else if (zf) { if (l) RBS_GSZ(BPV, true, true); else RBS_GSZ(BPV, false, true); } \
     else { if (l) RBS_GSZ(BPV, true, false); else RBS_GSZ(BPV, false, false); }
                 if (Bp == 8) { RBS_GSZ2(8) }
                 else if (Bp == 16) { RBS_GSZ2(16) }
                 else { RBS_GSZ2(32) }
 #undef RBS_GSZ2
+#undef RBS_GSZ0
 #undef RBS_GSZ
             } else if (Bp <= 32 && !(v2off & 8) && a.color >= 0) {   // row pencils (x in registers)
                 // 4-node row segments, all loads of a segment in flight (128 registers,
@@ -1352,7 +1371,8 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             }
             nl = 2;
         } else if (mode == MODE_RESID && (!cg || o->precond == RBS_PRECOND_SYM) && g.dim == 3 && use_active && L.T &&
-                   !(v2off & 524288) &&
+                   !(v2off & 524288) && !jac &&   // Jacobi: T is the sweeps' ping-pong buffer, whose copy-back
+                                                  // (smooth_jac, not guarded by `done`) must not find v in it
                    zm3 && zsm(2) && npad <= 64 && wtr_smem_bytes(Bp, ctx->ldw, 32) <= (size_t)110 * 1024) {
             // symmetric preconditioner's W^T (r - A y1) / RBI's W^T (f - A x), 3D full grid
             // (RBS_DISABLE_V2 bit 19 keeps the flat k_proj<MODE_RESID>): v by the z-plane march
@@ -1500,9 +1520,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
     // y1 = S*(A, r, 0), y2 = y1 + W A_n^{-1} W^T (r - A y1), y = S(A, r, y2) (+ Step 10)
     auto precond_sym = [&](int init) {
         int c = 0;
-        k_fill_batch<<<fgrid, 256, 0, st>>>(L.Y, g.N, ctx->N8, Bp, 0, nullptr, 0.0);
-        ++c;
-        c += smooth(L.Y, L.R, 0.0, false, init, &rseq);           // pre: the adjoint sweep from 0
+        c += smooth(L.Y, L.R, 0.0, false, init, &rseq, true);     // pre: the adjoint sweep from 0
         if (npad > 0) {
             c += proj(MODE_RESID, nullptr, true, L.Y, L.R);        // W^T (r - A y1)
             pb(RBS_K_REDUCE_SOLVE);

@@ -358,14 +358,19 @@ __global__ void __launch_bounds__(kZT, 1)
 //   their neighbours (all of the other colour, unchanged by this half-sweep) and stored.
 //   The threads map onto the sweep's colour only (ZColour); LAST also runs the other
 //   colour's y^T r, y^T y terms, then RBCG Step 10 in the last CTA.
+//   ZERO: the half-sweep from y = 0 (the symmetric two-level preconditioner's pre-sweep,
+//   y1 = S*(A, r, 0), first colour): no y tiles are loaded (all neighbours are 0), the
+//   sweep's colour gets the same value the loaded zeros would give, the other colour and
+//   the frozen lanes get 0 -- the k_fill_batch + half-sweep pair in one pass.
 // ===========================================================================
-template <int BP, bool LAST, bool FACES>
+template <int BP, bool LAST, bool FACES, bool ZERO = false>
 __global__ void __launch_bounds__(kZT, 1)
     k_gsz(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mR,
           const __grid_constant__ GSArgs a, const ZPart zp) {
     using Z = ZGeom<BP>;
     using C = ZColour<BP>;
     constexpr int NA = Z::NA, NB = Z::DI + 1, DI = Z::DI, NC = C::NC;
+    static_assert(!(ZERO && LAST), "the pre-sweep from zero is never the last half-sweep");
     extern __shared__ __align__(128) double smd[];
     __shared__ __align__(8) uint64_t barA[NA], barB[NB];
     if (a.done && ld_flag(a.done)) return;
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(kZT, 1)
         for (int k = 0; k < NA; ++k) mbar_init(&barA[k], 1);
         for (int k = 0; k < NB; ++k) mbar_init(&barB[k], 1);
         mbar_fence_init();
-        tma_prefetch_desc(&mY);
+        if (!ZERO) tma_prefetch_desc(&mY);
         if (hasr) tma_prefetch_desc(&mR);
     }
     const bool act = a.active[b] != 0;
@@ -409,7 +414,7 @@ __global__ void __launch_bounds__(kZT, 1)
         auto issue = [&](int t) {
             const int K = za - 1 + t;
             const uint32_t q = G + (uint32_t)t;
-            const bool in = K >= 1 && K <= m, own = hasr && K >= za && K < zb;
+            const bool in = !ZERO && K >= 1 && K <= m, own = hasr && K >= za && K < zb;
             fence_async_smem();
             mbar_expect_tx(&barA[q % NA], in ? HPB : 0u);
             mbar_expect_tx(&barB[q % NB], own ? IPB : 0u);
@@ -424,7 +429,7 @@ __global__ void __launch_bounds__(kZT, 1)
             const uint32_t q = G + (uint32_t)t;
             mbar_wait(&barA[q % NA], (q / NA) & 1);
             if (t >= 1) mbar_wait(&barB[(q - 1) % NB], ((q - 1) / NB) & 1);   // r of plane K-1
-            if (t >= 2 && act) {
+            if (t >= 2 && (act || ZERO)) {
                 const int Kc = K - 1;
                 const uint32_t ym = sA + ((q - 2) % NA) * HPB, yc = sA + ((q - 1) % NA) * HPB,
                                yp = sA + (q % NA) * HPB;
@@ -444,13 +449,18 @@ __global__ void __launch_bounds__(kZT, 1)
                     const uint32_t o = P ? el.h[1][j] : el.h[0][j];
                     const int cx = P ? el.cxy[1][j] : el.cxy[0][j];
                     rh[j] = hasr ? ldsd(rb + (P ? el.ri[1][j] : el.ri[0][j])) : rconst;
-                    nb[j][0] = ldsd(yc + o - 8 * BP);
-                    nb[j][1] = ldsd(yc + o + 8 * BP);
-                    nb[j][2] = ldsd(yc + o - 8 * Z::HX * BP);
-                    nb[j][3] = ldsd(yc + o + 8 * Z::HX * BP);
-                    const double zlo = ldsd(ym + o), zhi = ldsd(yp + o);
-                    nb[j][4] = zm ? zlo : 0.0;
-                    nb[j][5] = zpl ? zhi : 0.0;
+                    if (ZERO) {
+#pragma unroll
+                        for (int e = 0; e < 6; ++e) nb[j][e] = 0.0;
+                    } else {
+                        nb[j][0] = ldsd(yc + o - 8 * BP);
+                        nb[j][1] = ldsd(yc + o + 8 * BP);
+                        nb[j][2] = ldsd(yc + o - 8 * Z::HX * BP);
+                        nb[j][3] = ldsd(yc + o + 8 * Z::HX * BP);
+                        const double zlo = ldsd(ym + o), zhi = ldsd(yp + o);
+                        nb[j][4] = zm ? zlo : 0.0;
+                        nb[j][5] = zpl ? zhi : 0.0;
+                    }
                     const bool fast = !FACES && cx >= 0 && bzu >= 0;
                     v[j] = ldsd(st6 + 8u * (uint32_t)((fast ? cx + bzu : 0) * BP));
                     slow |= cx != -2 && !fast;
@@ -482,10 +492,17 @@ __global__ void __launch_bounds__(kZT, 1)
 #pragma unroll
                 for (int j = 0; j < NC; ++j) {
                     if ((P ? el.cxy[1][j] : el.cxy[0][j]) == -2) continue;
-                    yo[P ? el.gxy[1][j] : el.gxy[0][j]] = v[j];
+                    yo[P ? el.gxy[1][j] : el.gxy[0][j]] = (ZERO && !act) ? 0.0 : v[j];
                     if (LAST) {
                         yr = fma(v[j], rh[j], yr);
                         yy = fma(v[j], v[j], yy);
+                    }
+                }
+                if (ZERO) {           // the other colour stays at the start value 0
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) {
+                        if ((P ? el.cxy[0][j] : el.cxy[1][j]) == -2) continue;
+                        yo[P ? el.gxy[0][j] : el.gxy[1][j]] = 0.0;
                     }
                 }
                 if (LAST) {           // the other colour: unchanged values

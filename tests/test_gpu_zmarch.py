@@ -178,3 +178,44 @@ def test_zmarch_rbi_residual_projection(orc, rbs, B):
     a = z.solve_batch(mus, rhs=rhs, **k)["X"].cpu().numpy()
     b = f.solve_batch(mus, rhs=rhs, **k)["X"].cpu().numpy()
     assert np.max(np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)) <= 1e-12
+
+
+@pytest.mark.parametrize("B,faces", [(5, False), (16, False), (27, False), (6, True)])
+def test_zmarch_sym_presweep_from_zero(orc, rbs, B, faces):
+    """The symmetric two-level preconditioner's pre-sweep y1 = S*(A, r, 0) (PAPER.md:161 in
+    its pre+post-smoothed form, NEXT(3)): the first half-sweep from y = 0 as k_gsz<ZERO> (no
+    fill, no y tiles: the sweep's colour gets D^{-1} r, the other colour and the frozen lanes
+    0) against the k_fill_batch + half-sweep pair it replaces (RBS_DISABLE_V2 bit 20).  The
+    same operations on the same operands: bitwise equal iterates, converged solves (queries
+    freeze at different iterations) and fixed-iteration mode, and against the oracle."""
+    from synth import cases
+    m, blocks = 37, (2, 2, 2)
+    g, res = oracle_basis(orc, 3, m, blocks, 12, 24, 5)
+    kwf = dict(faces=cases.faces_from_blocks(3, m, blocks)) if faces else {}
+    mk = (lambda: rbs.Solver(3, m, **kwf)) if faces else (lambda: rbs.Solver(3, m, blocks))
+    z = mk().load_basis(res["W"], res["ANq"], res["fn"])
+    old = os.environ.get("RBS_DISABLE_V2")
+    os.environ["RBS_DISABLE_V2"] = "1048576"
+    try:
+        f = mk().load_basis(res["W"], res["ANq"], res["fn"])
+    finally:
+        if old is None:
+            del os.environ["RBS_DISABLE_V2"]
+        else:
+            os.environ["RBS_DISABLE_V2"] = old
+    mus = 0.1 * 100 ** np.random.default_rng(171 + B).random((B, g.Q))
+    kw = dict(record_history=1, max_iter=20000, precond=1)
+    oz = z.solve_batch(mus, **kw)
+    of = f.solve_batch(mus, **kw)
+    assert all(st == "CONVERGED" for st in oz["status"]), oz["status"]
+    assert len(set(int(i) for i in oz["its"])) > 1 or B == 1     # lanes freeze at different iterations
+    assert np.array_equal(oz["its"], of["its"])
+    assert np.array_equal(oz["X"].cpu().numpy(), of["X"].cpu().numpy())
+    for hz, hf in zip(oz["history"], of["history"]):
+        assert np.array_equal(np.asarray(hz), np.asarray(hf))
+    k = dict(tol=0.0, max_iter=6, precond=1)
+    assert np.array_equal(z.solve_batch(mus, **k)["X"].cpu().numpy(), f.solve_batch(mus, **k)["X"].cpu().numpy())
+    sample = [0, B - 1]
+    compare(dict(oz, X=oz["X"][sample], status=[oz["status"][i] for i in sample], its=oz["its"][sample],
+                 a_n=oz["a_n"][sample], history=[oz["history"][i] for i in sample]),
+            g, res["W"], res["ANq"], res["fn"], mus[sample], "rbcg", max_iter=20000, precond=1)
