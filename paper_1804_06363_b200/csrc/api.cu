@@ -1219,7 +1219,7 @@ static rbs_status solve_batch_impl(rbs_ctx* ctx, int B, const double* mu_host, c
             ++cnt;
         }
         if (buf[nu & 1] != Yf) {
-            cudaMemcpyAsync(Yf, buf[nu & 1], (size_t)ctx->N8 * Bp * 8, cudaMemcpyDeviceToDevice, st);  // CKL after
+            k_copy_unless_done<<<fgrid, 256, 0, st>>>(Yf, buf[nu & 1], (int64_t)ctx->N8 * Bp, done);  // CKL after
         }
         if (nu == 0 && last) {   // no sweep: y = y0, Step 10 partials by an empty GS pass
             a.Y = Yf;

@@ -1405,6 +1405,17 @@ __global__ void k_unpack_W(const double* __restrict__ Wi, int64_t N, int n, int 
     }
 }
 
+// dst <- src (tot doubles) unless the solve's done flag is set: the Jacobi ping-pong's copy-back
+// inside the iteration graph (after the last query froze the sweeps are no-ops and the
+// scratch buffer is not the iterate any more)
+__global__ void k_copy_unless_done(double* __restrict__ dst, const double* __restrict__ src, int64_t tot,
+                                   const int* done) {
+    if (done && ld_flag(done)) return;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x)
+        dst[t] = src[t];
+}
+
 // v[N8][Bp] <- value (or from src [B][N] query-major when src != nullptr)
 __global__ void k_fill_batch(double* __restrict__ v, int64_t N, int64_t N8, int Bp, int B,
                              const double* __restrict__ src, double value) {
